@@ -1,0 +1,485 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a (bf16 in, f32 accumulate in TMEM).
+//
+// C[z](m,n) = epilogue(alpha * sum_k A[z](m,k) * B[z](n,k))
+//
+// This is the B200 replacement of the reference's fp64 `matmul`
+// (proj/src/numerics.cpp:13-24) for every GEMM of the TMP layer: the
+// column-parallel QKV/FC1, row-parallel proj/FC2, their dgrad/wgrad
+// (numerics.cpp:202-206) and the batched attention contractions. Transposes
+// (numerics.cpp:26-32) are expressed as operand major-ness in the TMA box and
+// the UMMA smem descriptor, never as a kernel.
+//
+// Roles (192 threads, 1 CTA per SM, grid = min(tiles, SMs)):
+//   warp 0      TMA producer  (one elected lane): gmem -> smem ring, mbarrier tx
+//   warp 1      MMA issuer    (one elected lane): tcgen05.mma into a double-buffered
+//               TMEM accumulator; also owns TMEM alloc/dealloc
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> regs, fused bias/GeLU/dGeLU/accumulate,
+//               vectorised global stores
+// Tile 128 x BN x 64, BN in {128, 256}, SWIZZLE_128B operand tiles.
+#include <cstdio>
+#include <mutex>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace oases {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
+};
+
+struct TcParams {
+  int M, N, K;
+  int batch, batch_inner;
+  int tiles_m, tiles_n;
+  int kblocks;
+  int a_x_off[2], a_y_off[2], b_x_off[2], b_y_off[2];
+  void* c;
+  void* c2;
+  const void* aux;
+  const void* bias;
+  long long ldc;
+  long long c_row_off[2], c_col_off[2];
+  int c_f32;
+  int epilogue;
+  int causal;
+  int accumulate;
+  float alpha;
+};
+
+struct TileInfo {
+  int z, m0, n0, kb0, kb1;
+};
+
+template <int BN>
+__device__ __forceinline__ bool decode_tile(const TcParams& p, int t, TileInfo& ti) {
+  const int per_z = p.tiles_m * p.tiles_n;
+  ti.z = t / per_z;
+  const int r = t - ti.z * per_z;
+  const int mt = r / p.tiles_n;
+  const int nt = r - mt * p.tiles_n;
+  ti.m0 = mt * BM;
+  ti.n0 = nt * BN;
+  if (p.causal == OASES_CAUSAL_SKIP_UPPER && ti.n0 > ti.m0 + BM - 1) return false;
+  ti.kb0 = 0;
+  ti.kb1 = p.kblocks;
+  if (p.causal == OASES_CAUSAL_K_UPTO_M) {
+    const int lim = (ti.m0 + BM + BK - 1) / BK;
+    ti.kb1 = lim < ti.kb1 ? lim : ti.kb1;
+  } else if (p.causal == OASES_CAUSAL_K_FROM_M) {
+    ti.kb0 = ti.m0 / BK;
+  }
+  return ti.kb0 < ti.kb1;
+}
+
+// ----------------------------------------------------------------- epilogue
+template <typename OutT>
+__device__ __forceinline__ void store32(OutT* dst, const float (&v)[32], int valid);
+
+template <>
+__device__ __forceinline__ void store32<float>(float* dst, const float (&v)[32], int valid) {
+  if (valid >= 32) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  } else {
+    for (int i = 0; i < valid; ++i) dst[i] = v[i];
+  }
+}
+template <>
+__device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[32], int valid) {
+  if (valid >= 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 u;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+      u.x = *reinterpret_cast<uint32_t*>(&h0);
+      u.y = *reinterpret_cast<uint32_t*>(&h1);
+      u.z = *reinterpret_cast<uint32_t*>(&h2);
+      u.w = *reinterpret_cast<uint32_t*>(&h3);
+      reinterpret_cast<uint4*>(dst)[i] = u;
+    }
+  } else {
+    for (int i = 0; i < valid; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load32(const T* src, float (&v)[32], int valid);
+template <>
+__device__ __forceinline__ void load32<float>(const float* src, float (&v)[32], int valid) {
+  if (valid >= 32) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 f = reinterpret_cast<const float4*>(src)[i];
+      v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+    }
+  } else {
+    for (int i = 0; i < 32; ++i) v[i] = i < valid ? src[i] : 0.f;
+  }
+}
+template <>
+__device__ __forceinline__ void load32<__nv_bfloat16>(const __nv_bfloat16* src, float (&v)[32], int valid) {
+  if (valid >= 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 u = reinterpret_cast<const uint4*>(src)[i];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+        const float2 f = __bfloat1622float2(h);
+        v[8 * i + 2 * j] = f.x;
+        v[8 * i + 2 * j + 1] = f.y;
+      }
+    }
+  } else {
+    for (int i = 0; i < 32; ++i) v[i] = i < valid ? __bfloat162float(src[i]) : 0.f;
+  }
+}
+
+template <typename OutT>
+__device__ __forceinline__ void epilogue_chunk(const TcParams& p, int z, int m, int n, float (&v)[32]) {
+  const int valid = p.N - n < 32 ? p.N - n : 32;
+  const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
+  const long long row = p.c_row_off[0] * zo + p.c_row_off[1] * zi + m;
+  const long long col = p.c_col_off[0] * zo + p.c_col_off[1] * zi + n;
+  const long long off = row * p.ldc + col;
+  OutT* c = reinterpret_cast<OutT*>(p.c) + off;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+  if (p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) {
+    float b[32];
+    load32<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(p.bias) + n, b, valid);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += b[i];
+  }
+  if (p.epilogue == OASES_EPI_DGELU) {
+    float a[32];
+    load32<OutT>(reinterpret_cast<const OutT*>(p.aux) + off, a, valid);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(a[i]);
+  }
+  if (p.accumulate) {
+    float o[32];
+    load32<OutT>(c, o, valid);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] += o[i];
+  }
+  store32<OutT>(c, v, valid);
+  if (p.epilogue == OASES_EPI_BIAS_GELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+    store32<OutT>(reinterpret_cast<OutT*>(p.c2) + off, v, valid);
+  }
+}
+
+// ----------------------------------------------------------------- kernel
+template <int BN, int A_MN, int B_MN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                   const TcParams p) {
+  using Cfg = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int total_tiles = p.batch * p.tiles_m * p.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma_a);
+    tma_prefetch(&tma_b);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        TileInfo ti;
+        if (!decode_tile<BN>(p, t, ti)) continue;
+        const int zo = ti.z / p.batch_inner, zi = ti.z - zo * p.batch_inner;
+        const int ax = p.a_x_off[0] * zo + p.a_x_off[1] * zi;
+        const int ay = p.a_y_off[0] * zo + p.a_y_off[1] * zi;
+        const int bx = p.b_x_off[0] * zo + p.b_x_off[1] * zi;
+        const int by = p.b_y_off[0] * zo + p.b_y_off[1] * zi;
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, &tma_a, &full[stage], ax + ti.m0 + 64 * j, ay + k0);
+          } else {
+            tma_load_2d(sa, &tma_a, &full[stage], ax + k0, ay + ti.m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tma_b, &full[stage], bx + ti.n0 + 64 * j, by + k0);
+          } else {
+            tma_load_2d(sb, &tma_b, &full[stage], bx + k0, by + ti.n0);
+          }
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t smem_base = smem_u32(smem);
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        TileInfo ti;
+        if (!decode_tile<BN>(p, t, ti)) continue;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_base + stage * Cfg::STAGE_BYTES;
+          const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(sb + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb > ti.kb0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      TileInfo ti;
+      if (!decode_tile<BN>(p, t, ti)) continue;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int m = ti.m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+        tmem_wait_ld();
+        const int n = ti.n0 + c * 32;
+        if (m < p.M && n < p.N) {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (p.c_f32) epilogue_chunk<float>(p, ti.z, m, n, v);
+          else epilogue_chunk<__nv_bfloat16>(p, ti.z, m, n, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ----------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const oases_gemm_operand& o, uint32_t box_inner, uint32_t box_outer,
+              std::string* err) {
+  auto enc = get_encode();
+  if (!enc) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(o.ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")";
+    return false;
+  }
+  return true;
+}
+
+template <int BN, int A_MN, int B_MN>
+cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p, int grid,
+                      cudaStream_t stream) {
+  using Cfg = TcCfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, A_MN, B_MN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gemm_tc_kernel<BN, A_MN, B_MN><<<grid, 192, Cfg::SMEM, stream>>>(ma, mb, p);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t dispatch_major(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
+                           int grid, cudaStream_t s) {
+  if (!a_mn && !b_mn) return launch_tc<BN, 0, 0>(ma, mb, p, grid, s);
+  if (!a_mn && b_mn) return launch_tc<BN, 0, 1>(ma, mb, p, grid, s);
+  if (a_mn && !b_mn) return launch_tc<BN, 1, 0>(ma, mb, p, grid, s);
+  return launch_tc<BN, 1, 1>(ma, mb, p, grid, s);
+}
+
+int sm_count() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
+  GemmStatus st;
+  // Shape / alignment checks: TMA needs 16 B aligned strides and bases; the
+  // vectorised epilogue needs 16 B aligned output rows.
+  auto aligned = [](const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; };
+  if (d.a.ld % 8 || d.b.ld % 8 || !aligned(d.a.ptr, 16) || !aligned(d.b.ptr, 16)) {
+    st.err = "gemm_tc: operand base/ld must be 16-byte aligned (ld % 8 == 0)";
+    return st;
+  }
+  if (d.ldc % 8 || !aligned(d.c, 16) || (d.c_col_off[0] % 8) || (d.c_col_off[1] % 8)) {
+    st.err = "gemm_tc: output base/ld/column offsets must be 16-byte aligned";
+    return st;
+  }
+  if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0 || d.batch_inner <= 0) {
+    st.err = "gemm_tc: empty problem";
+    return st;
+  }
+  const int BN = (d.N <= 128) ? 128 : 256;
+  if (d.batch > 1 && (d.M % BM || d.N % BN || d.K % BK)) {
+    st.err = "gemm_tc: batched problems need M%128, N%BN, K%64 == 0 (tiles must not cross batches)";
+    return st;
+  }
+  if (d.causal != OASES_CAUSAL_NONE && d.M != d.K && d.causal != OASES_CAUSAL_SKIP_UPPER) {
+    st.err = "gemm_tc: causal K-range modes need M == K";
+    return st;
+  }
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, d.a, 64, d.a.mn_major ? 64 : BM, &st.err)) return st;
+  if (!make_map(&mb, d.b, 64, d.b.mn_major ? 64 : BN, &st.err)) return st;
+
+  TcParams p{};
+  p.M = static_cast<int>(d.M);
+  p.N = static_cast<int>(d.N);
+  p.K = static_cast<int>(d.K);
+  p.batch = static_cast<int>(d.batch);
+  p.batch_inner = static_cast<int>(d.batch_inner);
+  p.tiles_m = static_cast<int>((d.M + BM - 1) / BM);
+  p.tiles_n = static_cast<int>((d.N + BN - 1) / BN);
+  p.kblocks = static_cast<int>((d.K + BK - 1) / BK);
+  for (int i = 0; i < 2; ++i) {
+    p.a_x_off[i] = static_cast<int>(d.a.col_off[i]);
+    p.a_y_off[i] = static_cast<int>(d.a.row_off[i]);
+    p.b_x_off[i] = static_cast<int>(d.b.col_off[i]);
+    p.b_y_off[i] = static_cast<int>(d.b.row_off[i]);
+    p.c_row_off[i] = d.c_row_off[i];
+    p.c_col_off[i] = d.c_col_off[i];
+  }
+  p.c = d.c;
+  p.c2 = d.c2;
+  p.aux = d.aux;
+  p.bias = d.bias;
+  p.ldc = d.ldc;
+  p.c_f32 = d.c_dtype == OASES_F32;
+  p.epilogue = d.epilogue;
+  p.causal = d.causal;
+  p.accumulate = d.accumulate;
+  p.alpha = d.alpha;
+  const long long tiles = static_cast<long long>(p.batch) * p.tiles_m * p.tiles_n;
+  int grid = sm_count();
+  if (d.max_ctas > 0 && d.max_ctas < grid) grid = d.max_ctas;
+  if (tiles < grid) grid = static_cast<int>(tiles);
+  cudaError_t e = BN == 128 ? dispatch_major<128>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream)
+                            : dispatch_major<256>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream);
+  if (e != cudaSuccess) {
+    st.err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
+    st.cuda = true;
+    return st;
+  }
+  st.ok = true;
+  return st;
+}
+
+}  // namespace oases

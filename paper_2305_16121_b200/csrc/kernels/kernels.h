@@ -1,0 +1,35 @@
+// Internal launchers of the HBM-bound kernels (rowwise.cu, elementwise.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../../include/oases.h"
+
+namespace oases {
+
+cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, long long rows,
+                          int cols, float eps, cudaStream_t st);
+size_t layernorm_bwd_workspace(long long rows, int cols);
+cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,
+                          float* dgamma, float* dbeta, int acc_params, void* workspace, long long rows, int cols,
+                          float eps, cudaStream_t st);
+cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,
+                        float dropout_p, uint64_t seed, uint64_t offset, cudaStream_t st);
+cudaError_t softmax_bwd(int dtype, const void* p, const void* dpd, void* ds, long long batch, int seq, float scale,
+                        float dropout_p, uint64_t seed, uint64_t offset, cudaStream_t st);
+cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias, const void* res, void* out,
+                                      long long rows, int cols, float p, uint64_t seed, uint64_t offset,
+                                      cudaStream_t st);
+size_t colsum_workspace(long long rows, int cols);
+// dx = dropout'(in) (if dx), out (+)= column sums of dx (if out).
+cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, void* ws, long long rows, int cols,
+                     float p, uint64_t seed, uint64_t offset, cudaStream_t st);
+cudaError_t gelu_fwd(int dtype, const void* x, void* y, long long n, cudaStream_t st);
+cudaError_t gelu_bwd(int dtype, const void* x, const void* dy, void* dx, long long n, cudaStream_t st);
+size_t loss_workspace();
+cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int acc, double* ws, long long n,
+                         cudaStream_t st);
+cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cudaStream_t st);
+
+}  // namespace oases

@@ -1,0 +1,136 @@
+"""Thin torch-tensor front end over the kernel entry points of include/oases.h.
+
+torch is used only for device memory and the current stream (plumbing); every
+call lands in liboases.so. Used by the kernel-level parity tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi as capi
+from ._capi import check
+
+_DT = {torch.float32: capi.F32, torch.bfloat16: capi.BF16}
+
+
+def _dtype(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError as e:
+        raise TypeError(f"unsupported dtype {t.dtype}") from e
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def operand(t: torch.Tensor, mn_major: bool = False, row_off=(0, 0), col_off=(0, 0), col_base: int = 0):
+    """GEMM operand over a 2-D row-major storage tensor (optionally starting at column col_base)."""
+    assert t.dim() == 2 and t.stride(1) == 1
+    o = capi.GemmOperand()
+    o.ptr = t.data_ptr() + col_base * t.element_size()
+    o.rows = t.shape[0]
+    o.cols = t.shape[1] - col_base
+    o.ld = t.stride(0)
+    o.mn_major = int(mn_major)
+    o.row_off[0], o.row_off[1] = row_off
+    o.col_off[0], o.col_off[1] = col_off
+    return o
+
+
+def gemm(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_off=(0, 0), c_col_off=(0, 0),
+         c_col_base=0, epilogue=capi.EPI_NONE, causal=capi.CAUSAL_NONE, alpha=1.0, accumulate=False,
+         bias=None, aux=None, c2=None, max_ctas=0, dtype=capi.BF16, stream=None):
+    """dtype: operand dtype (capi.BF16 -> tcgen05 kernel, capi.F32 -> FFMA kernel)."""
+    d = capi.GemmDesc()
+    d.dtype = dtype
+    d.c_dtype = _dtype(c)
+    d.M, d.N, d.K = M, N, K
+    d.batch, d.batch_inner = batch, batch_inner
+    d.a, d.b = a, b
+    esz = c.element_size()
+    d.c = c.data_ptr() + c_col_base * esz
+    d.ldc = c.stride(0)
+    d.c_row_off[0], d.c_row_off[1] = c_row_off
+    d.c_col_off[0], d.c_col_off[1] = c_col_off
+    d.epilogue = epilogue
+    d.causal = causal
+    d.alpha = alpha
+    d.accumulate = int(accumulate)
+    d.bias = None if bias is None else bias.data_ptr()
+    d.aux = None if aux is None else aux.data_ptr() + c_col_base * esz
+    d.c2 = None if c2 is None else c2.data_ptr() + c_col_base * esz
+    d.max_ctas = max_ctas
+    check(capi.lib().oases_gemm(C.byref(d), _stream(stream)))
+
+
+def layernorm_fwd(x, gamma, beta, y, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    check(capi.lib().oases_layernorm_fwd(_dtype(x), _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), rows, cols, eps,
+                                         _stream(stream)))
+
+
+def layernorm_bwd(x, gamma, dy, dx, dgamma, dbeta, accumulate_dx=False, acc_params=False, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    ws = torch.empty(capi.lib().oases_layernorm_bwd_workspace(rows, cols) // 4 + 64, dtype=torch.float32,
+                     device=x.device)
+    check(capi.lib().oases_layernorm_bwd(_dtype(x), _ptr(x), _ptr(gamma), _ptr(dy), _ptr(dx), int(accumulate_dx),
+                                         _ptr(dgamma), _ptr(dbeta), int(acc_params), _ptr(ws), rows, cols, eps,
+                                         _stream(stream)))
+
+
+def softmax_fwd(s, p, p_drop, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, stream=None):
+    check(capi.lib().oases_softmax_fwd(_dtype(s), _ptr(s), _ptr(p), _ptr(p_drop), batch, seq, scale, dropout_p, seed,
+                                       offset, _stream(stream)))
+
+
+def softmax_bwd(p, dp_drop, ds, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, stream=None):
+    check(capi.lib().oases_softmax_bwd(_dtype(p), _ptr(p), _ptr(dp_drop), _ptr(ds), batch, seq, scale, dropout_p,
+                                       seed, offset, _stream(stream)))
+
+
+def bias_dropout_residual_fwd(x, bias, residual, out, dropout_p=0.0, seed=0, offset=0, stream=None):
+    rows, cols = x.shape
+    check(capi.lib().oases_bias_dropout_residual_fwd(_dtype(x), _ptr(x), _ptr(bias), _ptr(residual), _ptr(out), rows,
+                                                     cols, dropout_p, seed, offset, _stream(stream)))
+
+
+def bias_dropout_residual_bwd(dout, dx, dbias, acc_bias=False, dropout_p=0.0, seed=0, offset=0, stream=None):
+    rows, cols = dout.shape
+    ws = torch.empty(capi.lib().oases_colsum_workspace(rows, cols) // 4 + 64, dtype=torch.float32,
+                     device=dout.device)
+    check(capi.lib().oases_bias_dropout_residual_bwd(_dtype(dout), _ptr(dout), _ptr(dx), _ptr(dbias), int(acc_bias),
+                                                     _ptr(ws), rows, cols, dropout_p, seed, offset, _stream(stream)))
+
+
+def colsum(x, out, accumulate=False, stream=None):
+    rows, cols = x.shape
+    ws = torch.empty(capi.lib().oases_colsum_workspace(rows, cols) // 4 + 64, dtype=torch.float32, device=x.device)
+    check(capi.lib().oases_colsum(_dtype(x), _ptr(x), _ptr(out), int(accumulate), _ptr(ws), rows, cols,
+                                  _stream(stream)))
+
+
+def gelu_fwd(x, y, stream=None):
+    check(capi.lib().oases_gelu_fwd(_dtype(x), _ptr(x), _ptr(y), x.numel(), _stream(stream)))
+
+
+def gelu_bwd(x, dy, dx, stream=None):
+    check(capi.lib().oases_gelu_bwd(_dtype(x), _ptr(x), _ptr(dy), _ptr(dx), x.numel(), _stream(stream)))
+
+
+def gelu_sq_loss(z, dz, loss_out, accumulate=False, stream=None):
+    ws = torch.empty(1024, dtype=torch.float64, device=z.device)
+    check(capi.lib().oases_gelu_sq_loss(_dtype(z), _ptr(z), _ptr(dz), _ptr(loss_out), int(accumulate), _ptr(ws),
+                                        z.numel(), _stream(stream)))
+
+
+def local_allreduce(bufs, stream=None):
+    arr = (C.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+    check(capi.lib().oases_local_allreduce(_dtype(bufs[0]), arr, len(bufs), bufs[0].numel(), _stream(stream)))
