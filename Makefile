@@ -4,15 +4,15 @@
 #   make ref        -> oracle/_ref/* (the reference built from /root/reference, test-only)
 CUDA    ?= /usr/local/cuda
 NVCC    ?= $(CUDA)/bin/nvcc
-CXX     ?= g++
+CXX     := /usr/bin/g++
 PYTHON  ?= python
 PKG     := paper_2305_16121_b200
 SRC     := $(PKG)/csrc
 BUILD   := build
-JSON_INC ?= $(shell $(PYTHON) -c "import os,cudnn_frontend as c;print(os.path.join(os.path.dirname(c.__file__),'..','include','cudnn_frontend','thirdparty'))" 2>/dev/null || echo /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty)
+JSON_INC ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
 NCCL_INC ?= /usr/include
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr -Iinclude
+NVFLAGS := -ccbin /usr/bin/g++ -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr -Iinclude
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(CUDA)/include -I$(JSON_INC)
 
 CU_SRCS  := $(wildcard $(SRC)/kernels/*.cu) $(wildcard $(SRC)/runtime/*.cu)
@@ -35,7 +35,7 @@ $(BUILD)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/runtime/*.h $(SRC)/host/*.h include
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
-	$(NVCC) -shared $(ARCH) -o $@ $^ -L$(CUDA)/lib64 -lcudart -Xlinker -rpath,$(CUDA)/lib64 -lnccl
+	$(NVCC) -ccbin /usr/bin/g++ -shared $(ARCH) -o $@ $^ -L$(CUDA)/lib64 -lcudart -Xlinker -rpath,$(CUDA)/lib64 -lnccl
 
 $(CORE): $(SRC)/python/bindings.cpp $(LIB) include/oases/tmpsim.hpp include/oases/runtime.hpp
 	$(CXX) -std=c++20 -O2 -shared -fPIC $(PYBIND_INC) -Iinclude -I$(CUDA)/include -I$(JSON_INC) $< -o $@ \

@@ -2,7 +2,7 @@
  * oases.h -- C-ABI of the B200-native Oases TMP hot path.
  *
  * This is the drop-in boundary. The reference (tmpsim) has no
- * C-ABI; its operator API is the C++ header set proj/include/tmpsim/*.hpp,
+ * C-ABI; its operator API is the C++ header set proj/include/tmpsim/ *.hpp,
  * mirrored 1:1 by pybind11 in proj/python/bindings.cpp:28-236. Every entry
  * point below either replaces one of those functions with a real-hardware
  * counterpart, or exposes one kernel of the layer arithmetic that the reference
@@ -119,14 +119,19 @@ oases_status oases_layernorm_bwd(int dtype, const void* x, const void* gamma, co
                                  float eps, void* stream);
 size_t oases_layernorm_bwd_workspace(int64_t rows, int64_t cols);
 
-/* Causal scaled softmax over rows of S viewed as [batch*s, s] (row r has
- * query position r % s); optional Philox dropout writes P_drop. */
+/* Causal scaled softmax over rows of S viewed as [batch*s, s], batch =
+ * samples * heads_local (row r has query position r % s); optional Philox
+ * dropout writes P_drop, keyed by the GLOBAL head (head_offset + local head of
+ * heads_total) so masks do not depend on the TMP degree. s_in may alias p_out. */
 oases_status oases_softmax_fwd(int dtype, const void* s_in, void* p_out, void* p_drop,
                                int64_t batch, int64_t seq, float scale, float dropout_p,
-                               uint64_t seed, uint64_t offset, void* stream);
+                               uint64_t seed, uint64_t offset, int32_t heads_local,
+                               int32_t heads_total, int32_t head_offset, void* stream);
+/* dS = scale * P o (dP - rowsum(P o dP)), dP = dropout'(dP_drop); ds may alias dp_drop. */
 oases_status oases_softmax_bwd(int dtype, const void* p, const void* dp_drop, void* ds,
                                int64_t batch, int64_t seq, float scale, float dropout_p,
-                               uint64_t seed, uint64_t offset, void* stream);
+                               uint64_t seed, uint64_t offset, int32_t heads_local,
+                               int32_t heads_total, int32_t head_offset, void* stream);
 
 /* out = residual + dropout(x + bias): the Megatron bias-dropout-add. */
 oases_status oases_bias_dropout_residual_fwd(int dtype, const void* x, const void* bias,

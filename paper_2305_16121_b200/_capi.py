@@ -155,9 +155,9 @@ _SIGNATURES = [
                                        C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_float, C.c_void_p]),
     ("oases_layernorm_bwd_workspace", C.c_size_t, [C.c_int64, C.c_int64]),
     ("oases_softmax_fwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_float,
-                                     C.c_float, C.c_uint64, C.c_uint64, C.c_void_p]),
+                                     C.c_float, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     ("oases_softmax_bwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_float,
-                                     C.c_float, C.c_uint64, C.c_uint64, C.c_void_p]),
+                                     C.c_float, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     ("oases_bias_dropout_residual_fwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                    C.c_int64, C.c_float, C.c_uint64, C.c_uint64, C.c_void_p]),
     ("oases_bias_dropout_residual_bwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,

@@ -1,0 +1,45 @@
+// Calibration boundary: measured rows out (-> load_measured_costs), and the
+// B200 hardware preset in the reference's HardwareProfile schema.
+#include <fstream>
+
+#include "json.hpp"
+#include "oases/runtime.hpp"
+
+namespace tmpsim {
+
+void write_measured_costs(const std::vector<MeasuredRow>& rows, const std::filesystem::path& path) {
+  nlohmann::json arr = nlohmann::json::array();
+  for (const MeasuredRow& r : rows) {
+    static const char* fields[] = {"d_fwd", "d_bwd", "c_fwd", "c_bwd", "m_param", "m_saved", "m_runtime"};
+    bool ok = false;
+    for (const char* f : fields) ok = ok || r.field == f;
+    if (!ok) throw ConfigError("measured-cost row: unknown field '" + r.field + "'");
+    if (r.seconds_or_bytes < 0.0) throw ConfigError("measured-cost row: negative value");
+    arr.push_back({{"block_index", r.block_index},
+                   {"degree", r.degree},
+                   {"field", r.field},
+                   {"seconds_or_bytes", r.seconds_or_bytes}});
+  }
+  std::ofstream out(path);
+  if (!out) throw IoError("cannot write " + path.string());
+  out << arr.dump(1) << "\n";
+}
+
+HardwareProfile b200_profile(int num_devices, double nvlink_bytes_per_s, double latency_s) {
+  if (num_devices < 1) throw ConfigError("b200_profile: num_devices must be positive");
+  HardwareProfile hp;
+  hp.num_devices = num_devices;
+  hp.memory_capacity = 180LL * 1000 * 1000 * 1000;
+  hp.compute_throughput = 0.5 * 1611.4e12;  // MAC/s at the measured bf16 dense burst (MEASURED_PEAKS.json)
+  for (int d = 1; d <= num_devices; d *= 2) {
+    hp.candidate_degrees.push_back(d);
+    if (d > 1) {
+      hp.bandwidth_by_group[d] = nvlink_bytes_per_s;
+      hp.latency_by_group[d] = latency_s;
+    }
+  }
+  hp.validate();
+  return hp;
+}
+
+}  // namespace tmpsim

@@ -229,3 +229,70 @@ cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cu
 }
 
 }  // namespace oases
+
+namespace oases {
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fill_uniform_kernel(T* p, long long n, float scale, uint64_t seed,
+                                                                uint64_t offset) {
+  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x * 4) {
+    uint32_t u[4];
+    Philox::gen(seed, offset, static_cast<unsigned long long>(i) >> 2, u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i + q >= n) break;
+      const float r = (static_cast<float>(u[q] >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0,1)
+      p[i + q] = from_f<T>((2.f * r - 1.f) * scale);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fill_const_kernel(T* p, long long n, float v) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = from_f<T>(v);
+}
+
+template <typename S, typename D>
+__global__ void __launch_bounds__(kThreads) convert_kernel(const S* src, D* dst, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = from_f<D>(to_f(src[i]));
+}
+
+}  // namespace
+
+cudaError_t fill_uniform(int dtype, void* p, long long n, float scale, uint64_t seed, uint64_t offset,
+                         cudaStream_t st) {
+  const unsigned g = grid_for(n, kThreads * 4);
+  if (dtype == OASES_BF16)
+    fill_uniform_kernel<<<g, kThreads, 0, st>>>(static_cast<__nv_bfloat16*>(p), n, scale, seed, offset);
+  else
+    fill_uniform_kernel<<<g, kThreads, 0, st>>>(static_cast<float*>(p), n, scale, seed, offset);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_const(int dtype, void* p, long long n, float v, cudaStream_t st) {
+  const unsigned g = grid_for(n, kThreads);
+  if (dtype == OASES_BF16) fill_const_kernel<<<g, kThreads, 0, st>>>(static_cast<__nv_bfloat16*>(p), n, v);
+  else fill_const_kernel<<<g, kThreads, 0, st>>>(static_cast<float*>(p), n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t convert(int sd, const void* src, int dd, void* dst, long long n, cudaStream_t st) {
+  const unsigned g = grid_for(n, kThreads);
+  if (sd == OASES_F32 && dd == OASES_BF16)
+    convert_kernel<<<g, kThreads, 0, st>>>(static_cast<const float*>(src), static_cast<__nv_bfloat16*>(dst), n);
+  else if (sd == OASES_BF16 && dd == OASES_F32)
+    convert_kernel<<<g, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(src), static_cast<float*>(dst), n);
+  else if (sd == OASES_F32 && dd == OASES_F32)
+    return cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  else
+    return cudaMemcpyAsync(dst, src, n * 2, cudaMemcpyDeviceToDevice, st);
+  return cudaGetLastError();
+}
+
+}  // namespace oases

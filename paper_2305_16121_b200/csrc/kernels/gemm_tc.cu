@@ -165,7 +165,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcParams& p, int z, int m, 
   OutT* c = reinterpret_cast<OutT*>(p.c) + off;
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-  if (p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) {
+  if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias) {
     float b[32];
     load32<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(p.bias) + n, b, valid);
 #pragma unroll
@@ -428,9 +428,16 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
     return st;
   }
   const int BN = (d.N <= 128) ? 128 : 256;
-  if (d.batch > 1 && (d.M % BM || d.N % BN || d.K % BK)) {
-    st.err = "gemm_tc: batched problems need M%128, N%BN, K%64 == 0 (tiles must not cross batches)";
-    return st;
+  // Reads past the logical K would pull in neighbouring data (TMA zero-fills
+  // only at the storage edge): K must be a multiple of 64 unless it spans the
+  // whole storage extent of both operands. M/N tails are masked in the epilogue.
+  if (d.K % BK) {
+    const int64_t ka = d.a.mn_major ? d.a.rows : d.a.cols;
+    const int64_t kb = d.b.mn_major ? d.b.rows : d.b.cols;
+    if (d.batch > 1 || ka != d.K || kb != d.K) {
+      st.err = "gemm_tc: K % 64 != 0 requires K to span both operands' full extent (unbatched)";
+      return st;
+    }
   }
   if (d.causal != OASES_CAUSAL_NONE && d.M != d.K && d.causal != OASES_CAUSAL_SKIP_UPPER) {
     st.err = "gemm_tc: causal K-range modes need M == K";

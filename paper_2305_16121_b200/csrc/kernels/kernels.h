@@ -14,10 +14,18 @@ size_t layernorm_bwd_workspace(long long rows, int cols);
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,
                           float* dgamma, float* dbeta, int acc_params, void* workspace, long long rows, int cols,
                           float eps, cudaStream_t st);
+// batch = n_samples * heads_local; rows are (sample, local head, query).
 cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,
-                        float dropout_p, uint64_t seed, uint64_t offset, cudaStream_t st);
+                        float dropout_p, uint64_t seed, uint64_t offset, int heads_local, int heads_total,
+                        int head_offset, cudaStream_t st);
 cudaError_t softmax_bwd(int dtype, const void* p, const void* dpd, void* ds, long long batch, int seq, float scale,
-                        float dropout_p, uint64_t seed, uint64_t offset, cudaStream_t st);
+                        float dropout_p, uint64_t seed, uint64_t offset, int heads_local, int heads_total,
+                        int head_offset, cudaStream_t st);
+// Device-side U(-scale, scale) fill (Philox keyed by seed/offset) and constant fill.
+cudaError_t fill_uniform(int dtype, void* p, long long n, float scale, uint64_t seed, uint64_t offset, cudaStream_t st);
+cudaError_t fill_const(int dtype, void* p, long long n, float v, cudaStream_t st);
+// Elementwise dtype conversion of a contiguous buffer (f32 <-> bf16).
+cudaError_t convert(int src_dtype, const void* src, int dst_dtype, void* dst, long long n, cudaStream_t st);
 cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias, const void* res, void* out,
                                       long long rows, int cols, float p, uint64_t seed, uint64_t offset,
                                       cudaStream_t st);

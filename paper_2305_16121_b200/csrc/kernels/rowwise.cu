@@ -199,11 +199,21 @@ __global__ void colpair_finalize_kernel(const float* __restrict__ part, int chun
 // Row r of S (viewed [batch*seq, seq]) is query position i = r % seq; keys
 // j <= i are valid. P = softmax(scale * S) over valid keys, zeros elsewhere.
 // The row is cached in registers: NV vectors per lane.
+// Dropout element index uses the GLOBAL head (head_offset + local head) so the
+// mask does not depend on the TMP degree: row r = (n*Hl + jl)*seq + i maps to
+// global row (n*Hg + head_offset + jl)*seq + i.
+__device__ __forceinline__ unsigned long long global_row(long long row, int seq, int hl, int hg, int hoff) {
+  const long long per = static_cast<long long>(hl) * seq;
+  const long long n = row / per, rem = row - n * per;
+  const long long jl = rem / seq, i = rem - jl * seq;
+  return static_cast<unsigned long long>((n * hg + hoff + jl) * seq + i);
+}
+
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const T* __restrict__ s, T* __restrict__ p,
                                                           T* __restrict__ pd, long long rows, int seq, float scale,
                                                           uint32_t thr, float keep_scale, uint64_t seed,
-                                                          uint64_t offset) {
+                                                          uint64_t offset, int hl, int hg, int hoff) {
   constexpr int V = Vec<T>::N;
   const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const T* __restrict__ 
     for (int e = 0; e < V; ++e) v[t][e] *= inv;
     vstore(pr + c, v[t]);
     if (pdr) {
-      const unsigned long long base = static_cast<unsigned long long>(row) * seq + c;
+      const unsigned long long base = global_row(row, seq, hl, hg, hoff) * seq + c;
 #pragma unroll
       for (int e = 0; e < V; e += 4) {
         uint32_t u[4];
@@ -267,7 +277,7 @@ template <typename T, int NV>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ p, const T* __restrict__ dpd,
                                                           T* __restrict__ ds, long long rows, int seq, float scale,
                                                           uint32_t thr, float keep_scale, int use_dropout,
-                                                          uint64_t seed, uint64_t offset) {
+                                                          uint64_t seed, uint64_t offset, int hl, int hg, int hoff) {
   constexpr int V = Vec<T>::N;
   const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ 
       vload(p + row * seq + c, pv[t]);
       vload(dpd + row * seq + c, dv[t]);
       if (use_dropout) {
-        const unsigned long long base = static_cast<unsigned long long>(row) * seq + c;
+        const unsigned long long base = global_row(row, seq, hl, hg, hoff) * seq + c;
 #pragma unroll
         for (int e = 0; e < V; e += 4) {
           uint32_t u[4];
@@ -397,7 +407,7 @@ cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const voi
 }
 
 cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,
-                        float dropout_p, uint64_t seed, uint64_t offset, cudaStream_t st) {
+                        float dropout_p, uint64_t seed, uint64_t offset, int hl, int hg, int hoff, cudaStream_t st) {
   const long long rows = batch * seq;
   const uint32_t thr = dropout_threshold(dropout_p);
   const float ks = dropout_p > 0.f ? 1.f / (1.f - dropout_p) : 1.f;
@@ -405,13 +415,13 @@ cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long b
   if (dtype == OASES_BF16)
     return launch_rows_nv<__nv_bfloat16, SoftmaxFwdL>(seq, rows, st, static_cast<const __nv_bfloat16*>(s),
                                                       static_cast<__nv_bfloat16*>(p), static_cast<__nv_bfloat16*>(pd),
-                                                      rows, seq, scale, thr, ks, seed, offset);
+                                                      rows, seq, scale, thr, ks, seed, offset, hl, hg, hoff);
   return launch_rows_nv<float, SoftmaxFwdL>(seq, rows, st, static_cast<const float*>(s), static_cast<float*>(p),
-                                            static_cast<float*>(pd), rows, seq, scale, thr, ks, seed, offset);
+                                            static_cast<float*>(pd), rows, seq, scale, thr, ks, seed, offset, hl, hg, hoff);
 }
 
 cudaError_t softmax_bwd(int dtype, const void* p, const void* dpd, void* ds, long long batch, int seq, float scale,
-                        float dropout_p, uint64_t seed, uint64_t offset, cudaStream_t st) {
+                        float dropout_p, uint64_t seed, uint64_t offset, int hl, int hg, int hoff, cudaStream_t st) {
   const long long rows = batch * seq;
   const uint32_t thr = dropout_threshold(dropout_p);
   const float ks = dropout_p > 0.f ? 1.f / (1.f - dropout_p) : 1.f;
@@ -420,9 +430,9 @@ cudaError_t softmax_bwd(int dtype, const void* p, const void* dpd, void* ds, lon
     return launch_rows_nv<__nv_bfloat16, SoftmaxBwdL>(seq, rows, st, static_cast<const __nv_bfloat16*>(p),
                                                       static_cast<const __nv_bfloat16*>(dpd),
                                                       static_cast<__nv_bfloat16*>(ds), rows, seq, scale, thr, ks, use,
-                                                      seed, offset);
+                                                      seed, offset, hl, hg, hoff);
   return launch_rows_nv<float, SoftmaxBwdL>(seq, rows, st, static_cast<const float*>(p), static_cast<const float*>(dpd),
-                                            static_cast<float*>(ds), rows, seq, scale, thr, ks, use, seed, offset);
+                                            static_cast<float*>(ds), rows, seq, scale, thr, ks, use, seed, offset, hl, hg, hoff);
 }
 
 }  // namespace oases

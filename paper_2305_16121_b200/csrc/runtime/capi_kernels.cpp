@@ -96,25 +96,29 @@ oases_status oases_layernorm_bwd(int dtype, const void* x, const void* gamma, co
 }
 
 oases_status oases_softmax_fwd(int dtype, const void* s_in, void* p_out, void* p_drop, int64_t batch, int64_t seq,
-                               float scale, float dropout_p, uint64_t seed, uint64_t offset, void* stream) {
+                               float scale, float dropout_p, uint64_t seed, uint64_t offset, int32_t heads_local,
+                               int32_t heads_total, int32_t head_offset, void* stream) {
   return guarded([&] {
     check_dtype(dtype);
     need_device();
     if (seq % 8) throw tmpsim::ConfigError("softmax: seq must be a multiple of 8");
+    if (heads_local < 1 || batch % heads_local) throw tmpsim::ConfigError("softmax: batch must be samples * heads_local");
     check_cuda(oases::softmax_fwd(dtype, s_in, p_out, p_drop, batch, static_cast<int>(seq), scale, dropout_p, seed,
-                                  offset, S(stream)),
+                                  offset, heads_local, heads_total, head_offset, S(stream)),
                "softmax_fwd");
   });
 }
 
 oases_status oases_softmax_bwd(int dtype, const void* p, const void* dp_drop, void* ds, int64_t batch, int64_t seq,
-                               float scale, float dropout_p, uint64_t seed, uint64_t offset, void* stream) {
+                               float scale, float dropout_p, uint64_t seed, uint64_t offset, int32_t heads_local,
+                               int32_t heads_total, int32_t head_offset, void* stream) {
   return guarded([&] {
     check_dtype(dtype);
     need_device();
     if (seq % 8) throw tmpsim::ConfigError("softmax: seq must be a multiple of 8");
+    if (heads_local < 1 || batch % heads_local) throw tmpsim::ConfigError("softmax: batch must be samples * heads_local");
     check_cuda(oases::softmax_bwd(dtype, p, dp_drop, ds, batch, static_cast<int>(seq), scale, dropout_p, seed, offset,
-                                  S(stream)),
+                                  heads_local, heads_total, head_offset, S(stream)),
                "softmax_bwd");
   });
 }

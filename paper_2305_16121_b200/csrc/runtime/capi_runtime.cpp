@@ -1,0 +1,208 @@
+// extern "C" runtime entry points of include/oases.h: context, stack, plan
+// binding and the measured step. Handles are opaque; every call maps C++
+// exceptions to status codes (status.h).
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+
+#include "../../../include/oases.h"
+#include "stack.h"
+#include "status.h"
+
+struct oases_ctx {
+  std::unique_ptr<oases::Context> ctx;
+};
+
+struct oases_stack {
+  oases_ctx* owner = nullptr;
+  std::unique_ptr<oases::Stack> stack;
+  std::unique_ptr<oases::Executor> exec;
+  std::vector<oases_trace_event> events;
+};
+
+using oases::guarded;
+using tmpsim::ConfigError;
+
+namespace {
+
+oases::ModelCfg to_cfg(const oases_model_desc& m) {
+  oases::ModelCfg c;
+  c.h = m.hidden_size;
+  c.f = m.ffn_hidden > 0 ? m.ffn_hidden : 4 * m.hidden_size;
+  c.heads = m.attention_heads;
+  c.s = m.seq_len;
+  c.b = m.global_batch;
+  c.layers = m.num_layers;
+  c.bytes = m.bytes_per_element;
+  c.recompute = m.recompute_enabled != 0;
+  c.attention = m.use_attention != 0;
+  c.ln = m.use_layernorm != 0;
+  c.bias = m.use_bias != 0;
+  c.residual = m.use_residual != 0;
+  c.p_hidden = m.hidden_dropout;
+  c.p_attn = m.attention_dropout;
+  c.eps = m.ln_eps > 0.f ? m.ln_eps : 1e-5f;
+  c.seed = m.seed;
+  return c;
+}
+
+tmpsim::SchedulePlan unflatten(const oases_flat_plan& f) {
+  if (f.n_ops < 0 || f.n_forward < 0 || f.n_forward > f.n_ops || (f.n_ops && !f.ops))
+    throw ConfigError("plan_bind: malformed flat plan");
+  tmpsim::SchedulePlan p;
+  p.variant = static_cast<tmpsim::ScheduleVariant>(f.variant);
+  p.split_batch = f.split_batch != 0;
+  p.has_recompute = f.has_recompute != 0;
+  for (int i = 0; i < f.n_ops; ++i) {
+    const oases_plan_op& o = f.ops[i];
+    tmpsim::ScheduledOp op;
+    op.id = o.id;
+    op.base_id = o.base_id;
+    op.kind = static_cast<tmpsim::OpKind>(o.kind);
+    op.pass = static_cast<tmpsim::Pass>(o.pass);
+    op.stream = static_cast<tmpsim::Stream>(o.stream);
+    op.block = o.block;
+    op.sub_batch = o.sub_batch;
+    op.blocking = o.blocking != 0;
+    if (o.dep_begin < 0 || o.dep_count < 0 || o.dep_begin + o.dep_count > f.n_deps)
+      throw ConfigError("plan_bind: dependency range out of bounds");
+    op.deps.assign(f.deps + o.dep_begin, f.deps + o.dep_begin + o.dep_count);
+    (i < f.n_forward ? p.forward_ops : p.backward_ops).push_back(std::move(op));
+  }
+  return p;
+}
+
+oases::Stack& S(oases_stack* s) {
+  if (!s || !s->stack) throw ConfigError("null stack");
+  return *s->stack;
+}
+
+}  // namespace
+
+extern "C" {
+
+oases_status oases_get_unique_id(void* out) {
+  return guarded([&] {
+    if (!out) throw ConfigError("null output");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw oases::NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+oases_status oases_ctx_create(const oases_ctx_desc* desc, oases_ctx** out) {
+  return guarded([&] {
+    if (!desc || !out) throw ConfigError("null argument");
+    auto h = std::make_unique<oases_ctx>();
+    h->ctx = oases::make_context(*desc);
+    *out = h.release();
+  });
+}
+
+oases_status oases_ctx_destroy(oases_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+oases_status oases_stack_create(oases_ctx* ctx, const oases_model_desc* model, oases_stack** out) {
+  return guarded([&] {
+    if (!ctx || !ctx->ctx || !model || !out) throw ConfigError("null argument");
+    auto h = std::make_unique<oases_stack>();
+    h->owner = ctx;
+    h->stack = std::make_unique<oases::Stack>(*ctx->ctx, to_cfg(*model));
+    *out = h.release();
+  });
+}
+
+oases_status oases_stack_destroy(oases_stack* s) {
+  return guarded([&] {
+    if (s) {
+      if (s->stack) cudaStreamSynchronize(s->stack->ctx().compute);
+      s->exec.reset();
+      s->stack.reset();
+      delete s;
+    }
+  });
+}
+
+int64_t oases_stack_param_numel(const oases_stack* s, int block, int param) {
+  return (s && s->stack) ? s->stack->param_numel(block, param) : 0;
+}
+int oases_stack_num_blocks(const oases_stack* s) { return (s && s->stack) ? s->stack->num_blocks() : 0; }
+int oases_stack_num_workers(const oases_stack* s) { return (s && s->stack) ? s->stack->num_workers() : 0; }
+
+oases_status oases_stack_set_param(oases_stack* s, int worker, int block, int param, const double* host) {
+  return guarded([&] { S(s).set_param(worker, block, param, host); });
+}
+
+oases_status oases_stack_get_grad(oases_stack* s, int worker, int block, int param, double* host) {
+  return guarded([&] { S(s).get_grad(worker, block, param, host); });
+}
+
+oases_status oases_stack_init_random(oases_stack* s, uint64_t seed) {
+  return guarded([&] { S(s).init_random(seed); });
+}
+
+oases_status oases_plan_bind(oases_stack* s, const oases_flat_plan* plan) {
+  return guarded([&] {
+    if (!plan) throw ConfigError("null plan");
+    oases::Stack& st = S(s);
+    s->exec.reset();
+    s->exec = std::make_unique<oases::Executor>(st, unflatten(*plan));
+  });
+}
+
+oases_status oases_stack_set_input(oases_stack* s, const void* host, int input_dtype) {
+  return guarded([&] {
+    oases::Stack& st = S(s);
+    st.set_input(host, input_dtype, st.ctx().compute);
+    oases::check_cuda(cudaStreamSynchronize(st.ctx().compute), "set_input");
+  });
+}
+
+oases_status oases_step(oases_stack* s, const void* input_host, int input_dtype, int trace, oases_step_result* out) {
+  return guarded([&] {
+    oases::Stack& st = S(s);
+    if (!s->exec) throw ConfigError("oases_step: no plan bound");
+    if (input_host) st.set_input(input_host, input_dtype, st.ctx().compute);
+    tmpsim::SimResult r = s->exec->step(trace != 0);
+    if (out) {
+      std::memset(out, 0, sizeof(*out));
+      out->makespan = r.makespan;
+      out->compute_busy_fraction = r.compute_busy_fraction;
+      out->comm_exposed = r.comm_exposed;
+      out->peak_memory = r.peak_memory;
+      out->loss = st.read_loss();
+      s->events = s->exec->events();
+      out->n_events = static_cast<int32_t>(s->events.size());
+      out->events = s->events.empty() ? nullptr : s->events.data();
+    }
+  });
+}
+
+oases_status oases_stack_get_input_grad(oases_stack* s, double* host) {
+  return guarded([&] { S(s).get_input_grad(host); });
+}
+
+oases_status oases_stack_get_activation(oases_stack* s, int worker, int block, int sb, double* host) {
+  return guarded([&] { S(s).get_activation(worker, block, sb, host); });
+}
+
+oases_status oases_stack_capture_graph(oases_stack* s) {
+  return guarded([&] {
+    S(s);
+    if (!s->exec) throw ConfigError("capture_graph: no plan bound");
+    s->exec->capture_graph();
+  });
+}
+
+oases_status oases_stack_sync(oases_stack* s) {
+  return guarded([&] { oases::check_cuda(cudaDeviceSynchronize(), "sync"); (void)S(s); });
+}
+
+int oases_stack_kernel_launches(const oases_stack* s) {
+  return (s && s->stack) ? static_cast<int>(s->stack->kernel_launches()) : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// Plan executor: a tmpsim::SchedulePlan becomes kernels on the compute stream
+// and AllReduces on the comm stream. Every cross-stream plan dependency --
+// data edges AND the weave gates of Alg. 1 (the host `Sync(handler)`,
+// PAPER.md:239-240) -- becomes a cudaStreamWaitEvent, never a host sync, so
+// one sub-batch's AllReduce runs under the other sub-batch's GEMMs.
+//
+// The measured step is reported in the reference's SimResult shape
+// (sim.hpp:13-26): per-op cudaEvent intervals, makespan, compute-busy
+// fraction, exposed communication by the same interval algebra as
+// simulate() (sim.cpp:178-199), and the device bytes of the stack.
+#include <algorithm>
+#include <map>
+#include <set>
+
+#include "stack.h"
+#include "status.h"
+
+namespace oases {
+
+using tmpsim::ConfigError;
+using tmpsim::OpKind;
+using tmpsim::Pass;
+
+Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stack), plan_(plan) {
+  const auto bad = tmpsim::validate_plan(plan);
+  if (!bad.empty()) throw ConfigError("plan_bind: invalid plan: " + bad.front().code + ": " + bad.front().detail);
+  if (plan.has_recompute != stack.cfg().recompute)
+    throw ConfigError("plan_bind: plan.has_recompute must match the stack's recompute_enabled");
+  const int n = plan.total_ops();
+  int max_block = -1;
+  std::set<std::pair<int, int>> rec_comm;
+  for (int id = 0; id < n; ++id) {
+    const auto& op = plan.op(id);
+    max_block = std::max(max_block, op.block);
+    if (op.kind == OpKind::AllGather)
+      throw ConfigError("plan_bind: resharding AllGathers (mixed per-block degrees) are not executable yet");
+    if (tmpsim::is_comm(op.kind) && op.pass == Pass::Recompute) rec_comm.emplace(op.block, op.sub_batch);
+  }
+  if (n > 0 && max_block + 1 != stack.num_blocks())
+    throw ConfigError("plan_bind: plan has " + std::to_string(max_block + 1) + " blocks, stack has " +
+                      std::to_string(stack.num_blocks()));
+  // WAR protection: a compute op that writes an AllReduce buffer waits for the
+  // last comm op that used the same buffer (the plan's data edges cover RAW).
+  std::map<std::tuple<int, int, int>, int> last_comm_on;
+  auto buf_key = [](Pass p, int block, int sb) { return std::make_tuple(static_cast<int>(p), block % 2, sb); };
+  ops_.reserve(static_cast<size_t>(n));
+  for (int id = 0; id < n; ++id) {
+    const auto& op = plan.op(id);
+    ExecOp e;
+    e.id = id;
+    e.kind = op.kind;
+    e.pass = op.pass;
+    e.stream = op.stream == tmpsim::Stream::Comm ? 1 : 0;
+    e.block = op.block;
+    e.sb = op.sub_batch;
+    e.both_halves = !plan.split_batch;
+    if (op.kind == OpKind::RecomputeCompute) {
+      e.with_row = rec_comm.count({op.block, op.sub_batch}) > 0;
+      for (int d : op.deps) {
+        const auto& dop = plan.op(d);
+        if (tmpsim::is_comm(dop.kind) && dop.pass == Pass::Recompute) e.rebuild_x = true;
+      }
+    }
+    std::set<int> waits;
+    for (int d : op.deps) {
+      const int ds = plan.op(d).stream == tmpsim::Stream::Comm ? 1 : 0;
+      if (ds != e.stream) waits.insert(d);
+    }
+    if (e.stream == 0) {
+      const bool writes = op.kind == OpKind::ForwardCompute || op.kind == OpKind::BackwardCompute ||
+                          (op.kind == OpKind::RecomputeCompute && e.with_row);
+      if (writes) {
+        auto it = last_comm_on.find(buf_key(op.pass, op.block, op.sub_batch));
+        if (it != last_comm_on.end()) waits.insert(it->second);
+      }
+    } else {
+      last_comm_on[buf_key(op.pass, op.block, op.sub_batch)] = id;
+    }
+    e.waits.assign(waits.begin(), waits.end());
+    ops_.push_back(std::move(e));
+  }
+  // LN_0 backward tail: after the last backward comm (or compute) of block 0.
+  for (int id = 0; id < n; ++id) {
+    const auto& op = plan.op(id);
+    if (op.pass == Pass::Backward && op.block == 0) tail_wait_[static_cast<size_t>(op.sub_batch)] = id;
+  }
+  const int nev = n + 2;
+  t0_.resize(static_cast<size_t>(nev));
+  t1_.resize(static_cast<size_t>(nev));
+  for (int i = 0; i < nev; ++i) {
+    check_cuda(cudaEventCreate(&t0_[static_cast<size_t>(i)]), "event");
+    check_cuda(cudaEventCreate(&t1_[static_cast<size_t>(i)]), "event");
+  }
+  check_cuda(cudaEventCreate(&begin_), "event");
+  check_cuda(cudaEventCreate(&end_), "event");
+  check_cuda(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "event");
+}
+
+Executor::~Executor() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  for (auto e : t0_) cudaEventDestroy(e);
+  for (auto e : t1_) cudaEventDestroy(e);
+  if (begin_) cudaEventDestroy(begin_);
+  if (end_) cudaEventDestroy(end_);
+  if (fork_) cudaEventDestroy(fork_);
+}
+
+void Executor::issue(bool trace) {
+  Context& c = stack_.ctx();
+  check_cuda(cudaEventRecord(begin_, c.compute), "record");
+  check_cuda(cudaStreamWaitEvent(c.comm, begin_, 0), "fork");
+  stack_.begin_step();
+  const int W = stack_.num_workers();
+  for (const ExecOp& op : ops_) {
+    cudaStream_t s = op.stream ? c.comm : c.compute;
+    for (int d : op.waits) check_cuda(cudaStreamWaitEvent(s, t1_[static_cast<size_t>(d)], 0), "wait");
+    if (trace) check_cuda(cudaEventRecord(t0_[static_cast<size_t>(op.id)], s), "record");
+    if (op.stream == 1) {
+      stack_.allreduce(op.pass, op.block, op.sb, op.both_halves);
+    } else {
+      const int sb0 = op.both_halves ? 0 : op.sb, sb1 = op.both_halves ? 1 : op.sb;
+      for (int w = 0; w < W; ++w) {
+        for (int sb = sb0; sb <= sb1; ++sb) {
+          switch (op.kind) {
+            case OpKind::ForwardCompute: stack_.forward(w, op.block, sb, true, true); break;
+            case OpKind::RecomputeCompute: stack_.recompute(w, op.block, sb, op.rebuild_x, op.with_row); break;
+            case OpKind::BackwardCompute: stack_.backward(w, op.block, sb); break;
+            default: break;
+          }
+        }
+      }
+    }
+    check_cuda(cudaEventRecord(t1_[static_cast<size_t>(op.id)], s), "record");
+  }
+  const int n = static_cast<int>(ops_.size());
+  for (int k = 0; k < 2; ++k) {
+    const int wait = plan_.split_batch ? tail_wait_[static_cast<size_t>(k)] : tail_wait_[0];
+    if (wait >= 0 && ops_[static_cast<size_t>(wait)].stream == 1)
+      check_cuda(cudaStreamWaitEvent(c.compute, t1_[static_cast<size_t>(wait)], 0), "wait tail");
+    if (trace) check_cuda(cudaEventRecord(t0_[static_cast<size_t>(n + k)], c.compute), "record");
+    for (int w = 0; w < W; ++w) stack_.tail(w, k);
+    check_cuda(cudaEventRecord(t1_[static_cast<size_t>(n + k)], c.compute), "record");
+  }
+  check_cuda(cudaEventRecord(fork_, c.comm), "record");
+  check_cuda(cudaStreamWaitEvent(c.compute, fork_, 0), "join");
+  check_cuda(cudaEventRecord(end_, c.compute), "record");
+}
+
+bool Executor::capture_graph() {
+  Context& c = stack_.ctx();
+  if (graph_exec_) return true;
+  check_cuda(cudaStreamSynchronize(c.compute), "sync");
+  check_cuda(cudaStreamBeginCapture(c.compute, cudaStreamCaptureModeRelaxed), "begin capture");
+  try {
+    issue(false);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c.compute, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  check_cuda(cudaStreamEndCapture(c.compute, &graph_), "end capture");
+  check_cuda(cudaGraphInstantiate(&graph_exec_, graph_, 0), "instantiate");
+  return true;
+}
+
+tmpsim::SimResult Executor::step(bool trace) {
+  Context& c = stack_.ctx();
+  tmpsim::SimResult r;
+  if (graph_exec_ && !trace) {
+    check_cuda(cudaEventRecord(begin_, c.compute), "record");
+    check_cuda(cudaGraphLaunch(graph_exec_, c.compute), "graph launch");
+    check_cuda(cudaEventRecord(end_, c.compute), "record");
+  } else {
+    issue(trace);
+  }
+  check_cuda(cudaEventSynchronize(end_), "step sync");
+  float ms = 0.f;
+  check_cuda(cudaEventElapsedTime(&ms, begin_, end_), "elapsed");
+  r.makespan = ms * 1e-3;
+  r.peak_memory = static_cast<double>(stack_.device_bytes());
+  events_.clear();
+  if (trace) {
+    std::vector<std::pair<double, double>> comp, comm;
+    double busy = 0.0;
+    const int n = static_cast<int>(ops_.size());
+    for (int i = 0; i < n + 2; ++i) {
+      float a = 0.f, b = 0.f;
+      check_cuda(cudaEventElapsedTime(&a, begin_, t0_[static_cast<size_t>(i)]), "elapsed");
+      check_cuda(cudaEventElapsedTime(&b, begin_, t1_[static_cast<size_t>(i)]), "elapsed");
+      const int stream = i < n ? ops_[static_cast<size_t>(i)].stream : 0;
+      const double s0 = a * 1e-3, s1 = std::max(a, b) * 1e-3;
+      events_.push_back({i, stream, s0, s1});
+      r.trace.push_back({i, stream ? tmpsim::Stream::Comm : tmpsim::Stream::Compute, s0, s1});
+      if (stream) {
+        // tp == 1 AllReduces are empty: they contribute no interval
+        if (stack_.ctx().tp > 1) comm.emplace_back(s0, s1);
+      } else {
+        comp.emplace_back(s0, s1);
+        busy += s1 - s0;
+      }
+    }
+    r.comm_exposed = tmpsim::exposed_comm_time(comp, comm);
+    r.compute_busy_fraction = r.makespan > 0.0 ? busy / r.makespan : 0.0;
+  }
+  return r;
+}
+
+}  // namespace oases

@@ -1,0 +1,766 @@
+// TMP transformer layer stack on one device: parameters, the saved post-
+// AllReduce boundary tensors, workspaces, and the kernel list of every plan op
+// (F_b forward, R_b recompute, B_b backward, the LN_0 tail) for one worker.
+//
+// Block partition (SURVEY.md §8(a) note; the value semantics are the fp64
+// oracle's, oracle/gpt_oracle.cpp, whose FFN-only reduction is the reference
+// toy numerics.cpp:158-210):
+//   F_b : x_b = (res ? x_{b-1} : 0) + dropout(AR_{b-1} + bias_row_{b-1})   [bdr, b > 0]
+//         ln = LN(x_b); col = ln W_col^T + b_col; attention(qkv) | gelu(pre);
+//         partial_b = act W_row^T  -> AR_b (forward g)
+//   R_b : same from the STORED x_b, without the row GEMM and without any
+//         collective (Oases elision, Eq. 1 / numerics.cpp:198-199); CrossPass
+//         replays the unit, rebuilding x_b from the replayed AR_{b-1}.
+//   B_b : LN_{b+1} backward on the all-reduced d_ln_{b+1} (+ residual add),
+//         or the loss head for the last block; dropout'/bias grad; row GEMM
+//         wgrad/dgrad; attention or dGeLU backward; column GEMM wgrad;
+//         d_ln partial -> AR_b (backward f).
+//   tail: LN_0 backward after the last backward AR -> dX.
+// Weight gradients accumulate in f32 across the two sub-batches in issue
+// order; column reductions (bias, LN gamma/beta) are deterministic.
+#include "stack.h"
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../kernels/gemm.h"
+#include "../kernels/kernels.h"
+#include "status.h"
+
+namespace oases {
+
+using tmpsim::ConfigError;
+
+// ================================================================== context
+Context::~Context() {
+  if (nccl) ncclCommDestroy(nccl);
+  if (compute) cudaStreamDestroy(compute);
+  if (comm) cudaStreamDestroy(comm);
+}
+
+static void check_nccl(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw NcclError(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+std::unique_ptr<Context> make_context(const oases_ctx_desc& d) {
+  if (d.tp < 1) throw ConfigError("ctx: tp must be >= 1");
+  if (d.local_workers != 1 && d.local_workers != d.tp)
+    throw ConfigError("ctx: local_workers must be 1 (one rank per process) or equal tp (in-process emulation)");
+  if (d.local_workers > 8) throw ConfigError("ctx: at most 8 in-process workers");
+  if (d.tp > 1 && d.local_workers == 1 && !d.unique_id)
+    throw ConfigError("ctx: tp > 1 with one rank per process needs the NCCL unique id");
+  if (d.rank < 0 || (d.local_workers == 1 && d.rank >= d.tp)) throw ConfigError("ctx: rank out of range");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw CudaError("no CUDA device: the Oases runtime has no CPU fallback");
+  }
+  check_cuda(cudaSetDevice(d.device), "cudaSetDevice");
+  auto ctx = std::make_unique<Context>();
+  ctx->tp = d.tp;
+  ctx->rank = d.local_workers == 1 ? d.rank : 0;
+  ctx->device = d.device;
+  ctx->local_workers = d.local_workers;
+  ctx->gemm_max_ctas = d.gemm_max_ctas;
+  ctx->nccl_max_ctas = d.nccl_max_ctas;
+  int lo = 0, hi = 0;
+  check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+  check_cuda(cudaStreamCreateWithPriority(&ctx->compute, cudaStreamNonBlocking, lo), "compute stream");
+  // The comm stream gets the highest priority so NCCL's CTAs are scheduled as
+  // soon as the overlapped GEMM frees SMs.
+  check_cuda(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi), "comm stream");
+  if (d.tp > 1 && d.local_workers == 1) {
+    ncclUniqueId id;
+    static_assert(sizeof(ncclUniqueId) == OASES_UNIQUE_ID_BYTES, "unique id size");
+    std::memcpy(&id, d.unique_id, sizeof(id));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (d.nccl_max_ctas > 0) cfg.maxCTAs = d.nccl_max_ctas;
+    check_nccl(ncclCommInitRankConfig(&ctx->nccl, d.tp, id, d.rank, &cfg), "ncclCommInitRankConfig");
+  }
+  return ctx;
+}
+
+// ================================================================== arena
+DeviceArena::~DeviceArena() {
+  for (void* p : blocks_) cudaFree(p);
+}
+
+void* DeviceArena::alloc(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (bytes == 0) bytes = 256;
+  void* p = nullptr;
+  check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+  check_cuda(cudaMemset(p, 0, bytes), "cudaMemset");
+  blocks_.push_back(p);
+  total_ += bytes;
+  return p;
+}
+
+// ================================================================== stack
+namespace {
+uint64_t drop_offset(int block, int sb, int kind) { return (static_cast<uint64_t>(block) * 2 + sb) * 4 + kind; }
+
+oases_gemm_operand operand(const void* ptr, int64_t rows, int64_t cols, int64_t ld, bool mn, int64_t r0 = 0,
+                           int64_t r1 = 0, int64_t c0 = 0, int64_t c1 = 0) {
+  oases_gemm_operand o{};
+  o.ptr = ptr;
+  o.rows = rows;
+  o.cols = cols;
+  o.ld = ld;
+  o.mn_major = mn ? 1 : 0;
+  o.row_off[0] = r0;
+  o.row_off[1] = r1;
+  o.col_off[0] = c0;
+  o.col_off[1] = c1;
+  return o;
+}
+}  // namespace
+
+Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
+  const int t = ctx.tp;
+  if (cfg.h <= 0 || cfg.s <= 0 || cfg.b <= 0 || cfg.layers < 0) throw ConfigError("stack: sizes must be positive");
+  if (cfg.b % 2) throw ConfigError("stack: global_batch must be even (two sub-batches)");
+  if (cfg.bytes != 2 && cfg.bytes != 4) throw ConfigError("stack: bytes_per_element must be 2 (bf16) or 4 (f32)");
+  if (cfg.f % t) throw ConfigError("stack: ffn hidden must be divisible by tp");
+  if (cfg.attention) {
+    if (cfg.heads < 1 || cfg.h % cfg.heads || cfg.heads % t)
+      throw ConfigError("stack: hidden % heads and heads % tp must be 0");
+  }
+  if (cfg.h % 8 || (cfg.attention && cfg.s % 8)) throw ConfigError("stack: hidden and seq must be multiples of 8");
+  nblocks_ = cfg.layers * (cfg.attention ? 2 : 1);
+  hl_ = cfg.attention ? cfg.heads / t : 0;
+  dh_ = cfg.attention ? cfg.h / cfg.heads : 0;
+  ncol_attn_ = cfg.attention ? 3 * hl_ * dh_ : 0;
+  nrow_attn_ = cfg.attention ? hl_ * dh_ : 0;
+  ncol_ffn_ = cfg.f / t;
+  nrow_ffn_ = cfg.f / t;
+  if (dtype() == OASES_BF16) {
+    // tcgen05 tiles: K extents must be multiples of 64 (TMA zero-fill only at
+    // buffer edges), attention sequences whole 128-row tiles.
+    const int64_t k_dims[] = {cfg.h, ncol_ffn_, tokens_sub()};
+    for (int64_t k : k_dims)
+      if (k % 64) throw ConfigError("stack: bf16 mode needs hidden, ffn/tp and tokens per sub-batch % 64 == 0");
+    if (cfg.attention && (cfg.s % 128 || dh_ % 64 || nrow_attn_ % 64))
+      throw ConfigError("stack: bf16 attention needs seq % 128 == 0 and head dim % 64 == 0");
+  }
+  const int W = ctx.local_workers;
+  workers_.resize(static_cast<size_t>(W));
+  for (int w = 0; w < W; ++w) workers_[static_cast<size_t>(w)].rank = W > 1 ? w : ctx.rank;
+  alloc_all();
+  touched_.assign(static_cast<size_t>(nblocks_), {});
+  loss_touched_.assign(static_cast<size_t>(W), false);
+}
+
+Stack::~Stack() = default;
+
+int64_t Stack::param_numel(int block, int p) const {
+  if (block < 0 || block >= nblocks_ || p < 0 || p >= OASES_P_COUNT) return 0;
+  return workers_.front().params[static_cast<size_t>(block)].numel[p];
+}
+
+void* Stack::half(void* base, int sb, int64_t cols) const {
+  return static_cast<char*>(base) + static_cast<size_t>(sb) * tokens_sub() * cols * esize();
+}
+
+void Stack::alloc_all() {
+  const int64_t Ts = tokens_sub(), T = 2 * Ts, h = cfg_.h;
+  const size_t es = esize();
+  const int64_t ncol_max = std::max(ncol_attn_, ncol_ffn_), nrow_max = std::max(nrow_attn_, nrow_ffn_);
+  const int64_t bh = cfg_.b / 2;
+  const int64_t prob = cfg_.attention ? bh * hl_ * cfg_.s * static_cast<int64_t>(cfg_.s) : 0;
+  const int nslots = cfg_.recompute ? std::min(2, nblocks_) : nblocks_;
+  for (Worker& w : workers_) {
+    w.params.resize(static_cast<size_t>(nblocks_));
+    for (int b = 0; b < nblocks_; ++b) {
+      BlockParams& bp = w.params[static_cast<size_t>(b)];
+      const bool att = is_attention(b);
+      const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+      bp.numel[OASES_P_LN_GAMMA] = cfg_.ln ? h : 0;
+      bp.numel[OASES_P_LN_BETA] = cfg_.ln ? h : 0;
+      bp.numel[OASES_P_W_COL] = ncol * h;
+      bp.rows[OASES_P_W_COL] = static_cast<int>(ncol);
+      bp.numel[OASES_P_B_COL] = cfg_.bias ? ncol : 0;
+      bp.numel[OASES_P_W_ROW] = h * nrow;
+      bp.rows[OASES_P_W_ROW] = static_cast<int>(h);
+      bp.numel[OASES_P_B_ROW] = cfg_.bias ? h : 0;
+      for (int p = 0; p < OASES_P_COUNT; ++p) {
+        if (!bp.numel[p]) continue;
+        bp.p[p] = arena_.alloc(static_cast<size_t>(bp.numel[p]) * es);
+        bp.g[p] = static_cast<float*>(arena_.alloc(static_cast<size_t>(bp.numel[p]) * sizeof(float)));
+      }
+      if (cfg_.ln) {
+        check_cuda(fill_const(dtype(), bp.p[OASES_P_LN_GAMMA], h, 1.f, nullptr), "fill gamma");
+      }
+    }
+    w.input = arena_.alloc(static_cast<size_t>(T * h) * es);
+    w.grad = arena_.alloc(static_cast<size_t>(T * h) * es);
+    w.xs.resize(static_cast<size_t>(nblocks_));
+    for (int b = 0; b < nblocks_; ++b) {
+      void* base = b == 0 ? w.input : arena_.alloc(static_cast<size_t>(T * h) * es);
+      w.xs[static_cast<size_t>(b)] = {half(base, 0, h), half(base, 1, h)};
+    }
+    for (int par = 0; par < 2; ++par) {
+      void* f = arena_.alloc(static_cast<size_t>(T * h) * es);
+      void* bb = arena_.alloc(static_cast<size_t>(T * h) * es);
+      w.fwd_ar[par] = {half(f, 0, h), half(f, 1, h)};
+      w.bwd_ar[par] = {half(bb, 0, h), half(bb, 1, h)};
+      if (cfg_.recompute) {
+        void* r = arena_.alloc(static_cast<size_t>(T * h) * es);
+        w.rec_ar[par] = {half(r, 0, h), half(r, 1, h)};
+      }
+    }
+    w.ws.resize(static_cast<size_t>(nslots));
+    for (auto& per_sb : w.ws) {
+      for (Workspace& ws : per_sb) {
+        ws.ln = cfg_.ln ? arena_.alloc(static_cast<size_t>(Ts * h) * es) : nullptr;
+        ws.col = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
+        ws.act = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
+        if (prob) {
+          ws.p = arena_.alloc(static_cast<size_t>(prob) * es);
+          ws.pd = cfg_.p_attn > 0.f ? arena_.alloc(static_cast<size_t>(prob) * es) : ws.p;
+        }
+      }
+    }
+    w.gar = arena_.alloc(static_cast<size_t>(Ts * h) * es);
+    w.du = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
+    w.dcol = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
+    if (prob) w.dp = arena_.alloc(static_cast<size_t>(prob) * es);
+    w.y = arena_.alloc(static_cast<size_t>(Ts * h) * es);
+    w.ln_ws = arena_.alloc(layernorm_bwd_workspace(Ts, static_cast<int>(h)));
+    w.col_ws = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
+                                     colsum_workspace(Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
+    w.loss = static_cast<double*>(arena_.alloc(sizeof(double)));
+    w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
+  }
+  check_cuda(cudaDeviceSynchronize(), "stack allocation");
+}
+
+Workspace& Stack::ws_for(Worker& w, int block, int sb) {
+  const size_t slot = cfg_.recompute ? static_cast<size_t>(block % 2) : static_cast<size_t>(block);
+  return w.ws[std::min(slot, w.ws.size() - 1)][static_cast<size_t>(sb)];
+}
+
+bool Stack::touch(int block, int p) {
+  bool& t = touched_[static_cast<size_t>(block)][static_cast<size_t>(p)];
+  const bool was = t;
+  t = true;
+  return was;
+}
+
+void Stack::begin_step() {
+  for (auto& a : touched_) a.fill(false);
+  std::fill(loss_touched_.begin(), loss_touched_.end(), false);
+}
+
+void Stack::gemm(const oases_gemm_desc& d0) {
+  oases_gemm_desc d = d0;
+  d.dtype = dtype();
+  d.max_ctas = ctx_.gemm_max_ctas;
+  GemmStatus st = d.dtype == OASES_BF16 ? gemm_tc(d, ctx_.compute) : gemm_simt(d, ctx_.compute);
+  if (!st.ok) {
+    if (st.cuda) throw CudaError(st.err);
+    throw ConfigError(st.err);
+  }
+  ++launches_;
+}
+
+void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y) {
+  check_cuda(layernorm_fwd(dtype(), x, g, b, y, tokens_sub(), cfg_.h, cfg_.eps, ctx_.compute), "layernorm_fwd");
+  ++launches_;
+}
+
+// ------------------------------------------------------------------ params / io
+// Host views use the oracle layout [in, out] (f64); the device keeps [out, in].
+
+void Stack::set_param(int worker, int block, int p, const double* host) {
+  if (worker < 0 || worker >= num_workers() || block < 0 || block >= nblocks_ || p < 0 || p >= OASES_P_COUNT)
+    throw ConfigError("set_param: index out of range");
+  BlockParams& bp = workers_[static_cast<size_t>(worker)].params[static_cast<size_t>(block)];
+  const int64_t n = bp.numel[p];
+  if (!n) throw ConfigError("set_param: block has no such parameter");
+  std::vector<float> f(static_cast<size_t>(n));
+  if (p == OASES_P_W_COL || p == OASES_P_W_ROW) {
+    const int64_t out = bp.rows[p], in = n / out;  // device [out, in]; host [in, out]
+    for (int64_t o = 0; o < out; ++o)
+      for (int64_t i = 0; i < in; ++i) f[static_cast<size_t>(o * in + i)] = static_cast<float>(host[i * out + o]);
+  } else {
+    for (int64_t i = 0; i < n; ++i) f[static_cast<size_t>(i)] = static_cast<float>(host[i]);
+  }
+  void* staging = nullptr;
+  check_cuda(cudaMalloc(&staging, static_cast<size_t>(n) * sizeof(float)), "staging");
+  check_cuda(cudaMemcpy(staging, f.data(), static_cast<size_t>(n) * sizeof(float), cudaMemcpyHostToDevice), "H2D");
+  check_cuda(convert(OASES_F32, staging, dtype(), bp.p[p], n, nullptr), "convert");
+  check_cuda(cudaDeviceSynchronize(), "set_param");
+  cudaFree(staging);
+}
+
+void Stack::get_grad(int worker, int block, int p, double* host) {
+  if (worker < 0 || worker >= num_workers() || block < 0 || block >= nblocks_ || p < 0 || p >= OASES_P_COUNT)
+    throw ConfigError("get_grad: index out of range");
+  BlockParams& bp = workers_[static_cast<size_t>(worker)].params[static_cast<size_t>(block)];
+  const int64_t n = bp.numel[p];
+  if (!n) throw ConfigError("get_grad: block has no such parameter");
+  std::vector<float> f(static_cast<size_t>(n));
+  check_cuda(cudaDeviceSynchronize(), "get_grad sync");
+  check_cuda(cudaMemcpy(f.data(), bp.g[p], static_cast<size_t>(n) * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+  if (p == OASES_P_W_COL || p == OASES_P_W_ROW) {
+    const int64_t out = bp.rows[p], in = n / out;
+    for (int64_t o = 0; o < out; ++o)
+      for (int64_t i = 0; i < in; ++i) host[i * out + o] = f[static_cast<size_t>(o * in + i)];
+  } else {
+    for (int64_t i = 0; i < n; ++i) host[i] = f[static_cast<size_t>(i)];
+  }
+}
+
+void Stack::init_random(uint64_t seed) {
+  // numerics.cpp:146-152 conventions: input U(-1,1), W_col U(+-1/sqrt(h)),
+  // W_row U(+-1/sqrt(fan_in)); LN gamma 1, beta 0, biases 0.
+  const int64_t T = 2 * tokens_sub();
+  for (Worker& w : workers_) {
+    const uint64_t wr = static_cast<uint64_t>(w.rank);
+    check_cuda(fill_uniform(dtype(), w.input, T * cfg_.h, 1.f, seed, 0x1000000, ctx_.compute), "init input");
+    for (int b = 0; b < nblocks_; ++b) {
+      BlockParams& bp = w.params[static_cast<size_t>(b)];
+      const uint64_t off = 0x2000000 + (static_cast<uint64_t>(b) * 64 + wr) * 8;
+      check_cuda(fill_uniform(dtype(), bp.p[OASES_P_W_COL], bp.numel[OASES_P_W_COL],
+                              1.f / std::sqrt(static_cast<float>(cfg_.h)), seed, off, ctx_.compute),
+                 "init w_col");
+      const float fan = static_cast<float>(is_attention(b) ? cfg_.h : cfg_.f);
+      check_cuda(fill_uniform(dtype(), bp.p[OASES_P_W_ROW], bp.numel[OASES_P_W_ROW], 1.f / std::sqrt(fan), seed,
+                              off + 1, ctx_.compute),
+                 "init w_row");
+    }
+  }
+  // every worker sees the same input (replicated across the TMP group)
+  for (size_t w = 1; w < workers_.size(); ++w)
+    check_cuda(cudaMemcpyAsync(workers_[w].input, workers_[0].input, static_cast<size_t>(T * cfg_.h) * esize(),
+                               cudaMemcpyDeviceToDevice, ctx_.compute),
+               "replicate input");
+  check_cuda(cudaStreamSynchronize(ctx_.compute), "init_random");
+}
+
+void Stack::set_input(const void* host, int host_dtype, cudaStream_t st) {
+  const int64_t n = 2 * tokens_sub() * cfg_.h;
+  const int my = dtype();
+  const void* src = host;
+  std::vector<float> f32;
+  std::vector<uint16_t> b16;
+  int src_dtype = host_dtype;
+  if (host_dtype == 2) {  // f64 -> activation dtype on the host
+    const double* d = static_cast<const double*>(host);
+    if (my == OASES_F32) {
+      f32.resize(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) f32[static_cast<size_t>(i)] = static_cast<float>(d[i]);
+      src = f32.data();
+    } else {
+      b16.resize(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) {
+        const float v = static_cast<float>(d[i]);
+        uint32_t u;
+        std::memcpy(&u, &v, 4);
+        u += 0x7FFFu + ((u >> 16) & 1u);  // round to nearest even
+        b16[static_cast<size_t>(i)] = static_cast<uint16_t>(u >> 16);
+      }
+      src = b16.data();
+    }
+    src_dtype = my;
+  }
+  if (src_dtype != my) throw ConfigError("set_input: host dtype must match the activation dtype (or be f64)");
+  for (Worker& w : workers_)
+    check_cuda(cudaMemcpyAsync(w.input, src, static_cast<size_t>(n) * esize(), cudaMemcpyHostToDevice, st), "H2D input");
+  if (host_dtype == 2) check_cuda(cudaStreamSynchronize(st), "set_input");
+}
+
+namespace {
+void download(const void* dev, int dtype, int64_t n, double* host) {
+  check_cuda(cudaDeviceSynchronize(), "download sync");
+  if (dtype == OASES_F32) {
+    std::vector<float> f(static_cast<size_t>(n));
+    check_cuda(cudaMemcpy(f.data(), dev, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < n; ++i) host[i] = f[static_cast<size_t>(i)];
+  } else {
+    std::vector<uint16_t> b(static_cast<size_t>(n));
+    check_cuda(cudaMemcpy(b.data(), dev, static_cast<size_t>(n) * 2, cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < n; ++i) {
+      const uint32_t u = static_cast<uint32_t>(b[static_cast<size_t>(i)]) << 16;
+      float v;
+      std::memcpy(&v, &u, 4);
+      host[i] = v;
+    }
+  }
+}
+}  // namespace
+
+void Stack::get_input_grad(double* host) { download(workers_[0].grad, dtype(), 2 * tokens_sub() * cfg_.h, host); }
+
+void Stack::get_activation(int worker, int block, int sb, double* host) {
+  if (worker < 0 || worker >= num_workers() || block < 0 || block > nblocks_ || sb < 0 || sb > 1)
+    throw ConfigError("get_activation: index out of range");
+  Worker& w = workers_[static_cast<size_t>(worker)];
+  if (block == nblocks_) {
+    download(w.y, dtype(), tokens_sub() * cfg_.h, host);  // final output of the last traced sub-batch
+    return;
+  }
+  download(w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)], dtype(), tokens_sub() * cfg_.h, host);
+}
+
+double Stack::read_loss() {
+  double l = 0.0;
+  check_cuda(cudaMemcpy(&l, workers_[0].loss, sizeof(double), cudaMemcpyDeviceToHost), "loss D2H");
+  return l;
+}
+
+// ------------------------------------------------------------------ attention
+void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws) {
+  const int64_t s = cfg_.s, Ts = tokens_sub(), bh = cfg_.b / 2, Z = bh * hl_, nc = ncol_attn_, nr = nrow_attn_;
+  const int64_t hd = static_cast<int64_t>(hl_) * dh_;
+  const char* qkv = static_cast<const char*>(ws.col);
+  const size_t es = esize();
+  oases_gemm_desc d{};
+  // S = Q K^T per (sample, head); tiles above the diagonal are skipped.
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = s; d.N = s; d.K = dh_;
+  d.batch = Z; d.batch_inner = hl_;
+  d.a = operand(qkv, Ts, nc, nc, false, s, 0, 0, dh_);
+  d.b = operand(qkv + hd * es, Ts, nc - hd, nc, false, s, 0, 0, dh_);
+  d.c = ws.p; d.ldc = s; d.c_row_off[0] = hl_ * s; d.c_row_off[1] = s;
+  d.alpha = 1.f; d.causal = OASES_CAUSAL_SKIP_UPPER;
+  gemm(d);
+  check_cuda(softmax_fwd(dtype(), ws.p, ws.p, cfg_.p_attn > 0.f ? ws.pd : nullptr, Z, static_cast<int>(s),
+                         1.f / std::sqrt(static_cast<float>(dh_)), cfg_.p_attn, cfg_.seed, drop_offset(block, sb, 1),
+                         hl_, cfg_.heads, w.rank * hl_, ctx_.compute),
+             "softmax_fwd");
+  ++launches_;
+  // ctx = P_drop V  (K limited to the causal prefix of each 128-row tile)
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = s; d.N = dh_; d.K = s;
+  d.batch = Z; d.batch_inner = hl_;
+  d.a = operand(ws.pd, Z * s, s, s, false, hl_ * s, s);
+  d.b = operand(qkv + 2 * hd * es, Ts, nc - 2 * hd, nc, true, s, 0, 0, dh_);
+  d.c = ws.act; d.ldc = nr; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
+  d.alpha = 1.f; d.causal = OASES_CAUSAL_K_UPTO_M;
+  gemm(d);
+}
+
+void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
+  const int64_t s = cfg_.s, Ts = tokens_sub(), bh = cfg_.b / 2, Z = bh * hl_, nc = ncol_attn_, nr = nrow_attn_;
+  const int64_t hd = static_cast<int64_t>(hl_) * dh_;
+  const size_t es = esize();
+  const char* qkv = static_cast<const char*>(ws.col);
+  char* dqkv = static_cast<char*>(w.dcol);
+  oases_gemm_desc d{};
+  // dP_drop = dctx V^T
+  d.c_dtype = dtype();
+  d.M = s; d.N = s; d.K = dh_;
+  d.batch = Z; d.batch_inner = hl_;
+  d.a = operand(w.du, Ts, nr, nr, false, s, 0, 0, dh_);
+  d.b = operand(qkv + 2 * hd * es, Ts, nc - 2 * hd, nc, false, s, 0, 0, dh_);
+  d.c = w.dp; d.ldc = s; d.c_row_off[0] = hl_ * s; d.c_row_off[1] = s;
+  d.alpha = 1.f; d.causal = OASES_CAUSAL_SKIP_UPPER;
+  gemm(d);
+  // dV = P_drop^T dctx
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = s; d.N = dh_; d.K = s;
+  d.batch = Z; d.batch_inner = hl_;
+  d.a = operand(ws.pd, Z * s, s, s, true, hl_ * s, s);
+  d.b = operand(w.du, Ts, nr, nr, true, s, 0, 0, dh_);
+  d.c = dqkv + 2 * hd * es; d.ldc = nc; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
+  d.alpha = 1.f; d.causal = OASES_CAUSAL_K_FROM_M;
+  gemm(d);
+  // dS (in place over dP)
+  check_cuda(softmax_bwd(dtype(), ws.p, w.dp, w.dp, Z, static_cast<int>(s), 1.f / std::sqrt(static_cast<float>(dh_)),
+                         cfg_.p_attn, cfg_.seed, drop_offset(block, sb, 1), hl_, cfg_.heads, w.rank * hl_,
+                         ctx_.compute),
+             "softmax_bwd");
+  ++launches_;
+  // dQ = dS K
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = s; d.N = dh_; d.K = s;
+  d.batch = Z; d.batch_inner = hl_;
+  d.a = operand(w.dp, Z * s, s, s, false, hl_ * s, s);
+  d.b = operand(qkv + hd * es, Ts, nc - hd, nc, true, s, 0, 0, dh_);
+  d.c = dqkv; d.ldc = nc; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
+  d.alpha = 1.f; d.causal = OASES_CAUSAL_K_UPTO_M;
+  gemm(d);
+  // dK = dS^T Q
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = s; d.N = dh_; d.K = s;
+  d.batch = Z; d.batch_inner = hl_;
+  d.a = operand(w.dp, Z * s, s, s, true, hl_ * s, s);
+  d.b = operand(qkv, Ts, nc, nc, true, s, 0, 0, dh_);
+  d.c = dqkv + hd * es; d.ldc = nc; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
+  d.alpha = 1.f; d.causal = OASES_CAUSAL_K_FROM_M;
+  gemm(d);
+}
+
+// ------------------------------------------------------------------ plan ops
+void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
+  Worker& w = workers_[static_cast<size_t>(wi)];
+  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  void* x = w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)];
+  if (block > 0 && with_bdr) {
+    const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
+    check_cuda(bias_dropout_residual_fwd(dtype(), w.fwd_ar[(block - 1) % 2][static_cast<size_t>(sb)],
+                                         cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr,
+                                         cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr,
+                                         x, Ts, static_cast<int>(h), cfg_.p_hidden, cfg_.seed,
+                                         drop_offset(block - 1, sb, 0), ctx_.compute),
+               "bdr_fwd");
+    ++launches_;
+  }
+  Workspace& ws = ws_for(w, block, sb);
+  const BlockParams& bp = w.params[static_cast<size_t>(block)];
+  const bool att = is_attention(block);
+  const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+  const void* ln = x;
+  if (cfg_.ln) {
+    ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
+    ln = ws.ln;
+  }
+  oases_gemm_desc d{};
+  d.c_dtype = dtype();
+  d.M = Ts; d.N = ncol; d.K = h;
+  d.batch = 1; d.batch_inner = 1;
+  d.a = operand(ln, Ts, h, h, false);
+  d.b = operand(bp.p[OASES_P_W_COL], ncol, h, h, false);
+  d.c = ws.col; d.ldc = ncol;
+  d.alpha = 1.f;
+  d.bias = cfg_.bias ? bp.p[OASES_P_B_COL] : nullptr;
+  if (att) {
+    d.epilogue = OASES_EPI_BIAS;
+    gemm(d);
+    attention_fwd(w, block, sb, ws);
+  } else {
+    d.epilogue = OASES_EPI_BIAS_GELU;
+    d.c2 = ws.act;
+    gemm(d);
+  }
+  if (with_row) {
+    d = oases_gemm_desc{};
+    d.c_dtype = dtype();
+    d.M = Ts; d.N = h; d.K = nrow;
+    d.batch = 1; d.batch_inner = 1;
+    d.a = operand(ws.act, Ts, nrow, nrow, false);
+    d.b = operand(bp.p[OASES_P_W_ROW], h, nrow, nrow, false);
+    d.c = w.fwd_ar[block % 2][static_cast<size_t>(sb)];
+    d.ldc = h;
+    d.alpha = 1.f;
+    gemm(d);
+  }
+}
+
+void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) {
+  Worker& w = workers_[static_cast<size_t>(wi)];
+  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  void* x = w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)];
+  if (rebuild_x && block > 0) {
+    const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
+    check_cuda(bias_dropout_residual_fwd(dtype(), w.rec_ar[(block - 1) % 2][static_cast<size_t>(sb)],
+                                         cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr,
+                                         cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr,
+                                         x, Ts, static_cast<int>(h), cfg_.p_hidden, cfg_.seed,
+                                         drop_offset(block - 1, sb, 0), ctx_.compute),
+               "bdr_fwd (replay)");
+    ++launches_;
+  }
+  // Same kernels as the forward from the stored x_b; the row GEMM only when
+  // this variant replays the block's AllReduce.
+  Workspace& ws = ws_for(w, block, sb);
+  const BlockParams& bp = w.params[static_cast<size_t>(block)];
+  const bool att = is_attention(block);
+  const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+  const void* ln = x;
+  if (cfg_.ln) {
+    ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
+    ln = ws.ln;
+  }
+  oases_gemm_desc d{};
+  d.c_dtype = dtype();
+  d.M = Ts; d.N = ncol; d.K = h;
+  d.batch = 1; d.batch_inner = 1;
+  d.a = operand(ln, Ts, h, h, false);
+  d.b = operand(bp.p[OASES_P_W_COL], ncol, h, h, false);
+  d.c = ws.col; d.ldc = ncol;
+  d.alpha = 1.f;
+  d.bias = cfg_.bias ? bp.p[OASES_P_B_COL] : nullptr;
+  if (att) {
+    d.epilogue = OASES_EPI_BIAS;
+    gemm(d);
+    attention_fwd(w, block, sb, ws);
+  } else {
+    d.epilogue = OASES_EPI_BIAS_GELU;
+    d.c2 = ws.act;
+    gemm(d);
+  }
+  if (with_row) {
+    d = oases_gemm_desc{};
+    d.c_dtype = dtype();
+    d.M = Ts; d.N = h; d.K = nrow;
+    d.batch = 1; d.batch_inner = 1;
+    d.a = operand(ws.act, Ts, nrow, nrow, false);
+    d.b = operand(bp.p[OASES_P_W_ROW], h, nrow, nrow, false);
+    d.c = w.rec_ar[block % 2][static_cast<size_t>(sb)];
+    d.ldc = h;
+    d.alpha = 1.f;
+    gemm(d);
+  }
+}
+
+void Stack::backward(int wi, int block, int sb) {
+  Worker& w = workers_[static_cast<size_t>(wi)];
+  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  const int hi = static_cast<int>(h);
+  void* g = half(w.grad, sb, h);
+  const size_t usb = static_cast<size_t>(sb);
+  // 1. gradient arriving at x_{b+1}
+  if (block == nblocks_ - 1) {
+    const BlockParams& bp = w.params[static_cast<size_t>(block)];
+    check_cuda(bias_dropout_residual_fwd(dtype(), w.fwd_ar[block % 2][usb], cfg_.bias ? bp.p[OASES_P_B_ROW] : nullptr,
+                                         cfg_.residual ? w.xs[static_cast<size_t>(block)][usb] : nullptr, w.y, Ts, hi,
+                                         cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0), ctx_.compute),
+               "bdr_fwd (loss head)");
+    const bool acc = loss_touched_[static_cast<size_t>(wi)];
+    loss_touched_[static_cast<size_t>(wi)] = true;
+    check_cuda(gelu_sq_loss(dtype(), w.y, g, w.loss, acc ? 1 : 0, w.loss_ws, Ts * h, ctx_.compute), "loss head");
+    launches_ += 3;
+  } else {
+    const BlockParams& nxt = w.params[static_cast<size_t>(block + 1)];
+    const void* dln = w.bwd_ar[(block + 1) % 2][usb];
+    if (cfg_.ln) {
+      const bool acc = touch(block + 1, OASES_P_LN_GAMMA);
+      check_cuda(layernorm_bwd(dtype(), w.xs[static_cast<size_t>(block + 1)][usb], nxt.p[OASES_P_LN_GAMMA], dln, g,
+                               cfg_.residual ? 1 : 0, nxt.g[OASES_P_LN_GAMMA], nxt.g[OASES_P_LN_BETA], acc ? 1 : 0,
+                               w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute),
+                 "layernorm_bwd");
+      launches_ += 3;
+    } else {
+      check_cuda(bias_dropout_residual_fwd(dtype(), dln, nullptr, cfg_.residual ? g : nullptr, g, Ts, hi, 0.f, 0, 0,
+                                           ctx_.compute),
+                 "residual grad add");
+      ++launches_;
+    }
+  }
+  // 2. through bias-dropout: g_ar = dropout'(g), dbias_row += colsum(g_ar)
+  BlockParams& bp = w.params[static_cast<size_t>(block)];
+  const void* gar = g;
+  if (cfg_.p_hidden > 0.f || cfg_.bias) {
+    const bool acc = cfg_.bias ? touch(block, OASES_P_B_ROW) : false;
+    check_cuda(col_pass(dtype(), g, cfg_.p_hidden > 0.f ? w.gar : nullptr, cfg_.bias ? bp.g[OASES_P_B_ROW] : nullptr,
+                        acc ? 1 : 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0), ctx_.compute),
+               "bdr_bwd");
+    launches_ += 2;
+    if (cfg_.p_hidden > 0.f) gar = w.gar;
+  }
+  Workspace& ws = ws_for(w, block, sb);
+  const bool att = is_attention(block);
+  const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+  // 3. row-parallel GEMM: dW_row += g_ar^T act ; d(act) = g_ar W_row
+  oases_gemm_desc d{};
+  d.c_dtype = OASES_F32;
+  d.M = h; d.N = nrow; d.K = Ts;
+  d.batch = 1; d.batch_inner = 1;
+  d.a = operand(gar, Ts, h, h, true);
+  d.b = operand(ws.act, Ts, nrow, nrow, true);
+  d.c = bp.g[OASES_P_W_ROW]; d.ldc = nrow;
+  d.alpha = 1.f; d.accumulate = touch(block, OASES_P_W_ROW) ? 1 : 0;
+  gemm(d);
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = Ts; d.N = nrow; d.K = h;
+  d.batch = 1; d.batch_inner = 1;
+  d.a = operand(gar, Ts, h, h, false);
+  d.b = operand(bp.p[OASES_P_W_ROW], h, nrow, nrow, true);
+  d.alpha = 1.f;
+  if (att) {
+    d.c = w.du; d.ldc = nrow;
+    gemm(d);
+    attention_bwd(w, block, sb, ws);
+  } else {
+    // dpre = (g_ar W_row) o gelu'(pre)   (hadamard + gelu_grad fused, numerics.cpp:203-204)
+    d.c = w.dcol; d.ldc = ncol;
+    d.epilogue = OASES_EPI_DGELU;
+    d.aux = ws.col;
+    gemm(d);
+  }
+  // 4. column bias
+  if (cfg_.bias) {
+    const bool acc = touch(block, OASES_P_B_COL);
+    check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws, Ts,
+                        static_cast<int>(ncol), 0.f, 0, 0, ctx_.compute),
+               "colsum");
+    launches_ += 2;
+  }
+  // 5. column-parallel GEMM: dW_col += dcol^T ln ; d_ln partial = dcol W_col -> AR_b (backward f)
+  const void* ln = cfg_.ln ? ws.ln : w.xs[static_cast<size_t>(block)][usb];
+  d = oases_gemm_desc{};
+  d.c_dtype = OASES_F32;
+  d.M = ncol; d.N = h; d.K = Ts;
+  d.batch = 1; d.batch_inner = 1;
+  d.a = operand(w.dcol, Ts, ncol, ncol, true);
+  d.b = operand(ln, Ts, h, h, true);
+  d.c = bp.g[OASES_P_W_COL]; d.ldc = h;
+  d.alpha = 1.f; d.accumulate = touch(block, OASES_P_W_COL) ? 1 : 0;
+  gemm(d);
+  d = oases_gemm_desc{};
+  d.c_dtype = dtype();
+  d.M = Ts; d.N = h; d.K = ncol;
+  d.batch = 1; d.batch_inner = 1;
+  d.a = operand(w.dcol, Ts, ncol, ncol, false);
+  d.b = operand(bp.p[OASES_P_W_COL], ncol, h, h, true);
+  d.c = w.bwd_ar[block % 2][usb]; d.ldc = h;
+  d.alpha = 1.f;
+  gemm(d);
+}
+
+void Stack::tail(int wi, int sb) {
+  Worker& w = workers_[static_cast<size_t>(wi)];
+  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  void* g = half(w.grad, sb, h);
+  const size_t usb = static_cast<size_t>(sb);
+  const void* dln = w.bwd_ar[0][usb];
+  if (cfg_.ln) {
+    const BlockParams& bp = w.params[0];
+    const bool acc = touch(0, OASES_P_LN_GAMMA);
+    check_cuda(layernorm_bwd(dtype(), w.xs[0][usb], bp.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0,
+                             bp.g[OASES_P_LN_GAMMA], bp.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, Ts,
+                             static_cast<int>(h), cfg_.eps, ctx_.compute),
+               "layernorm_bwd (tail)");
+    launches_ += 3;
+  } else {
+    check_cuda(bias_dropout_residual_fwd(dtype(), dln, nullptr, cfg_.residual ? g : nullptr, g, Ts,
+                                         static_cast<int>(h), 0.f, 0, 0, ctx_.compute),
+               "residual grad add (tail)");
+    ++launches_;
+  }
+}
+
+void Stack::allreduce(tmpsim::Pass pass, int block, int sb, bool both) {
+  if (ctx_.tp == 1) return;
+  const int par = block % 2;
+  auto pick = [&](Worker& w) -> void* {
+    auto& arr = pass == tmpsim::Pass::Forward ? w.fwd_ar[par] : pass == tmpsim::Pass::Recompute ? w.rec_ar[par] : w.bwd_ar[par];
+    return arr[both ? 0 : static_cast<size_t>(sb)];
+  };
+  const int64_t count = tokens_sub() * cfg_.h * (both ? 2 : 1);
+  if (ctx_.local_workers > 1) {
+    std::vector<void*> bufs;
+    for (Worker& w : workers_) bufs.push_back(pick(w));
+    check_cuda(local_allreduce(dtype(), bufs.data(), static_cast<int>(bufs.size()), count, ctx_.comm),
+               "local allreduce");
+    ++launches_;
+    return;
+  }
+  void* p = pick(workers_[0]);
+  check_nccl(ncclAllReduce(p, p, static_cast<size_t>(count), dtype() == OASES_BF16 ? ncclBfloat16 : ncclFloat32,
+                           ncclSum, ctx_.nccl, ctx_.comm),
+             "ncclAllReduce");
+  ++launches_;
+}
+
+}  // namespace oases

@@ -1,0 +1,191 @@
+// Runtime objects behind the C-ABI: the device/stream/NCCL context, the TMP
+// layer stack (weights, saved boundary tensors, workspaces) and the plan
+// executor that turns a tmpsim::SchedulePlan into kernels on a compute stream
+// and AllReduces on a dedicated comm stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/oases.h"
+#include "../../../include/oases/tmpsim.hpp"
+
+namespace oases {
+
+// ------------------------------------------------------------------ context
+struct Context {
+  int tp = 1;
+  int rank = 0;
+  int device = 0;
+  int local_workers = 1;  // >1: all TMP ranks emulated in-process on `device`
+  int gemm_max_ctas = 0;
+  int nccl_max_ctas = 0;
+  cudaStream_t compute = nullptr;
+  cudaStream_t comm = nullptr;
+  ncclComm_t nccl = nullptr;
+  ~Context();
+};
+
+std::unique_ptr<Context> make_context(const oases_ctx_desc& d);
+
+// ------------------------------------------------------------------ memory
+class DeviceArena {
+ public:
+  ~DeviceArena();
+  void* alloc(size_t bytes);  // 256-byte aligned, zero-initialised
+  size_t bytes() const { return total_; }
+
+ private:
+  std::vector<void*> blocks_;
+  size_t total_ = 0;
+};
+
+// ------------------------------------------------------------------ stack
+struct ModelCfg {
+  int h = 0, f = 0, heads = 0, s = 0, b = 0, layers = 0;
+  int bytes = 2;
+  bool recompute = true, attention = true, ln = true, bias = true, residual = true;
+  float p_hidden = 0.f, p_attn = 0.f, eps = 1e-5f;
+  uint64_t seed = 0;
+};
+
+// Per-block parameters of one TMP worker (device layout [out, in]).
+struct BlockParams {
+  void* p[OASES_P_COUNT] = {};   // activation dtype
+  float* g[OASES_P_COUNT] = {};  // f32 gradients
+  int64_t numel[OASES_P_COUNT] = {};
+  int rows[OASES_P_COUNT] = {};  // device layout rows (out features) for 2-D weights
+};
+
+// Activations of one (block, sub-batch) forward/recompute instance.
+struct Workspace {
+  void* ln = nullptr;   // [T_sub, h]  (aliases x when LN is off)
+  void* col = nullptr;  // [T_sub, ncol]  qkv | pre
+  void* act = nullptr;  // [T_sub, nrow]  ctx | gelu(pre)
+  void* p = nullptr;    // [bh*Hl*s, s]   S then P (in place)
+  void* pd = nullptr;   // dropped P (== p when attention dropout is 0)
+};
+
+struct Worker {
+  int rank = 0;
+  std::vector<BlockParams> params;
+  // saved residual stream x_b per sub-batch (b = 0..nblocks-1), x_0 aliases input
+  std::vector<std::array<void*, 2>> xs;
+  std::array<void*, 2> fwd_ar[2] = {}, rec_ar[2] = {}, bwd_ar[2] = {};  // [block parity][sb]
+  std::vector<std::array<Workspace, 2>> ws;  // [slot][sb]
+  void* input = nullptr;                     // [T, h]
+  void* grad = nullptr;                      // [T, h] residual gradient g (halves per sb) == dX at the end
+  // backward scratch (the compute stream serialises all B_b)
+  void* gar = nullptr;   // [T_sub, h]  dropout'(g)
+  void* du = nullptr;    // [T_sub, nmax] d(row GEMM input)
+  void* dcol = nullptr;  // [T_sub, ncol_max]
+  void* dp = nullptr;    // [bh*Hl*s, s]  dP_drop then dS
+  void* y = nullptr;     // [T_sub, h] final output for the loss head
+  void* ln_ws = nullptr;
+  void* col_ws = nullptr;
+  double* loss = nullptr;     // device scalar (f64)
+  double* loss_ws = nullptr;  // partials
+};
+
+class Stack {
+ public:
+  Stack(Context& ctx, const ModelCfg& cfg);
+  ~Stack();
+
+  const ModelCfg& cfg() const { return cfg_; }
+  Context& ctx() { return ctx_; }
+  int num_blocks() const { return nblocks_; }
+  int num_workers() const { return static_cast<int>(workers_.size()); }
+  bool is_attention(int b) const { return cfg_.attention && (b % 2 == 0); }
+  int dtype() const { return cfg_.bytes == 2 ? OASES_BF16 : OASES_F32; }
+  size_t esize() const { return static_cast<size_t>(cfg_.bytes); }
+  int64_t tokens_sub() const { return static_cast<int64_t>(cfg_.b / 2) * cfg_.s; }
+  int64_t param_numel(int block, int p) const;
+  size_t device_bytes() const { return arena_.bytes(); }
+
+  void set_param(int worker, int block, int p, const double* host);
+  void get_grad(int worker, int block, int p, double* host);
+  void init_random(uint64_t seed);
+  void set_input(const void* host, int host_dtype, cudaStream_t st);
+  void get_input_grad(double* host);
+  void get_activation(int worker, int block, int sb, double* host);
+
+  // ---- per-op kernel lists (issued on ctx.compute for every worker) ----
+  void forward(int worker, int block, int sb, bool with_bdr, bool with_row);
+  // recompute: replay_input: -1 = saved x_b; else rebuild x_b from rec_ar of block-1
+  void recompute(int worker, int block, int sb, bool rebuild_x, bool with_row);
+  void backward(int worker, int block, int sb);
+  void tail(int worker, int sb);  // LN_0 backward after the last backward AR
+  // ---- communication (issued on ctx.comm) ----
+  void allreduce(tmpsim::Pass pass, int block, int sb, bool both_halves);
+
+  void begin_step();  // resets first-touch flags of gradient accumulation
+  double read_loss();
+
+  int64_t kernel_launches() const { return launches_; }
+
+ private:
+  void alloc_all();
+  void gemm(const oases_gemm_desc& d);
+  void ln_fwd(const void* x, const void* g, const void* b, void* y);
+  void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);
+  void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
+  Workspace& ws_for(Worker& w, int block, int sb);
+  bool touch(int block, int p);  // true if the gradient must accumulate (already written this step)
+  void* half(void* base, int sb, int64_t cols) const;
+
+  Context& ctx_;
+  ModelCfg cfg_;
+  DeviceArena arena_;
+  std::vector<Worker> workers_;
+  int nblocks_ = 0;
+  int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
+  std::vector<std::array<bool, OASES_P_COUNT>> touched_;
+  std::vector<bool> loss_touched_;
+  int64_t launches_ = 0;
+};
+
+// ------------------------------------------------------------------ executor
+struct ExecOp {
+  int id = 0;
+  tmpsim::OpKind kind = tmpsim::OpKind::ForwardCompute;
+  tmpsim::Pass pass = tmpsim::Pass::Forward;
+  int stream = 0;  // 0 compute, 1 comm
+  int block = 0;
+  int sb = 0;
+  bool both_halves = false;  // unsplit (Default) plans: one op covers both sub-batches
+  bool rebuild_x = false;    // recompute restarts from a replayed comm (CrossPass inside a unit)
+  bool with_row = false;     // recompute also runs the row-parallel GEMM (its AR is replayed)
+  std::vector<int> waits;    // cross-stream deps (op ids)
+};
+
+class Executor {
+ public:
+  Executor(Stack& stack, const tmpsim::SchedulePlan& plan);
+  ~Executor();
+  // One step; returns measured SimResult (trace when `trace`).
+  tmpsim::SimResult step(bool trace);
+  bool capture_graph();
+  const tmpsim::SchedulePlan& plan() const { return plan_; }
+  const std::vector<oases_trace_event>& events() const { return events_; }
+
+ private:
+  void issue(bool trace);
+  Stack& stack_;
+  tmpsim::SchedulePlan plan_;
+  std::vector<ExecOp> ops_;
+  std::vector<cudaEvent_t> done_;   // per op (+ tails) completion, sync-only
+  std::vector<cudaEvent_t> t0_, t1_;  // per op timing
+  cudaEvent_t begin_ = nullptr, end_ = nullptr, fork_ = nullptr;
+  std::array<int, 2> tail_wait_ = {-1, -1};  // last backward AR (per sb) the LN_0 tail waits for
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  std::vector<oases_trace_event> events_;
+};
+
+}  // namespace oases

@@ -86,14 +86,16 @@ def layernorm_bwd(x, gamma, dy, dx, dgamma, dbeta, accumulate_dx=False, acc_para
                                          _stream(stream)))
 
 
-def softmax_fwd(s, p, p_drop, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, stream=None):
+def softmax_fwd(s, p, p_drop, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, heads_local=1, heads_total=1,
+                head_offset=0, stream=None):
     check(capi.lib().oases_softmax_fwd(_dtype(s), _ptr(s), _ptr(p), _ptr(p_drop), batch, seq, scale, dropout_p, seed,
-                                       offset, _stream(stream)))
+                                       offset, heads_local, heads_total, head_offset, _stream(stream)))
 
 
-def softmax_bwd(p, dp_drop, ds, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, stream=None):
+def softmax_bwd(p, dp_drop, ds, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, heads_local=1, heads_total=1,
+                head_offset=0, stream=None):
     check(capi.lib().oases_softmax_bwd(_dtype(p), _ptr(p), _ptr(dp_drop), _ptr(ds), batch, seq, scale, dropout_p,
-                                       seed, offset, _stream(stream)))
+                                       seed, offset, heads_local, heads_total, head_offset, _stream(stream)))
 
 
 def bias_dropout_residual_fwd(x, bias, residual, out, dropout_p=0.0, seed=0, offset=0, stream=None):
