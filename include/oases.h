@@ -289,8 +289,19 @@ oases_status oases_stack_get_activation(oases_stack* s, int worker, int block, i
 /* Capture the bound plan's step as a CUDA graph (trace off). */
 oases_status oases_stack_capture_graph(oases_stack* s);
 oases_status oases_stack_sync(oases_stack* s);
-/* Per-kernel-class device time of the last traced step (name, ms) */
+/* Number of kernels this stack has launched (all steps so far). */
 int oases_stack_kernel_launches(const oases_stack* s);
+/* Live cudaEvent timing of every linear-layer GEMM launch (QKV/proj/FC1/FC2
+ * forward, dgrad, wgrad) on the compute stream, for the roofline in bench.py.
+ * Stats accumulate over steps since the last read; reading resets them. */
+typedef struct {
+  double gemm_ms;     /* summed launch durations */
+  double gemm_flops;  /* summed algorithmic 2*M*N*K */
+  int32_t gemm_launches;
+  int32_t pad_;
+} oases_kernel_stats;
+oases_status oases_stack_set_kernel_timing(oases_stack* s, int on);
+oases_status oases_stack_kernel_stats(oases_stack* s, oases_kernel_stats* out);
 
 #ifdef __cplusplus
 }

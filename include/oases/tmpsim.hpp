@@ -80,6 +80,9 @@ struct ModelGraph {
 };
 
 std::vector<Operator> build_operator_sequence(const ModelSpec& spec);
+// Extension: FFN-only layers (compute + AllReduce per layer) -- the shape of the
+// reference's toy checker (numerics.hpp:37-44) as a block chain.
+std::vector<Operator> build_ffn_sequence(const ModelSpec& spec);
 ModelGraph build_block_graph(const std::vector<Operator>& ops);
 ModelGraph build_block_graph(const std::vector<Operator>& ops, const ModelSpec& spec);
 std::vector<Operator> flatten(const ModelGraph& graph);

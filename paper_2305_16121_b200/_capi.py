@@ -130,6 +130,11 @@ class TraceEventC(C.Structure):
     _fields_ = [("op_id", C.c_int32), ("stream", C.c_int32), ("start", C.c_double), ("end", C.c_double)]
 
 
+class KernelStats(C.Structure):
+    _fields_ = [("gemm_ms", C.c_double), ("gemm_flops", C.c_double), ("gemm_launches", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
 class StepResult(C.Structure):
     _fields_ = [
         ("makespan", C.c_double),
@@ -190,6 +195,8 @@ _SIGNATURES = [
     ("oases_stack_capture_graph", C.c_int, [C.c_void_p]),
     ("oases_stack_sync", C.c_int, [C.c_void_p]),
     ("oases_stack_kernel_launches", C.c_int, [C.c_void_p]),
+    ("oases_stack_set_kernel_timing", C.c_int, [C.c_void_p, C.c_int]),
+    ("oases_stack_kernel_stats", C.c_int, [C.c_void_p, C.POINTER(KernelStats)]),
 ]
 
 SYMBOLS = [name for name, _, _ in _SIGNATURES]

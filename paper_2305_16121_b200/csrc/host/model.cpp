@@ -67,6 +67,25 @@ std::vector<Operator> build_operator_sequence(const ModelSpec& spec) {
   return seq;
 }
 
+std::vector<Operator> build_ffn_sequence(const ModelSpec& spec) {
+  spec.validate();
+  std::vector<Operator> seq;
+  const std::int64_t h = spec.hidden_size;
+  for (int layer = 0; layer < spec.num_layers; ++layer) {
+    for (OpKind kind : {OpKind::ForwardCompute, OpKind::AllReduce}) {
+      Operator op;
+      op.id = static_cast<int>(seq.size());
+      op.kind = kind;
+      op.layer = layer;
+      op.sublayer = Sublayer::Ffn;
+      op.param_count = kind == OpKind::ForwardCompute ? 8 * h * h : 0;
+      op.tensor_elements = static_cast<std::int64_t>(spec.seq_len) * h;
+      seq.push_back(op);
+    }
+  }
+  return seq;
+}
+
 ModelGraph build_block_graph(const std::vector<Operator>& ops) {
   ModelGraph g;
   std::vector<Operator> pending;

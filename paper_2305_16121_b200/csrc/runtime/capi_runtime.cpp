@@ -201,6 +201,24 @@ oases_status oases_stack_sync(oases_stack* s) {
   return guarded([&] { oases::check_cuda(cudaDeviceSynchronize(), "sync"); (void)S(s); });
 }
 
+oases_status oases_stack_set_kernel_timing(oases_stack* s, int on) {
+  return guarded([&] {
+    S(s).set_kernel_timing(on != 0);
+    S(s).reset_kernel_stats();
+  });
+}
+
+oases_status oases_stack_kernel_stats(oases_stack* s, oases_kernel_stats* out) {
+  return guarded([&] {
+    if (!out) throw ConfigError("null output");
+    std::memset(out, 0, sizeof(*out));
+    int n = 0;
+    S(s).kernel_stats(&out->gemm_ms, &out->gemm_flops, &n);
+    out->gemm_launches = n;
+    S(s).reset_kernel_stats();
+  });
+}
+
 int oases_stack_kernel_launches(const oases_stack* s) {
   return (s && s->stack) ? static_cast<int>(s->stack->kernel_launches()) : 0;
 }

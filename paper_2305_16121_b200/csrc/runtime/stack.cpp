@@ -127,7 +127,9 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
     if (cfg.heads < 1 || cfg.h % cfg.heads || cfg.heads % t)
       throw ConfigError("stack: hidden % heads and heads % tp must be 0");
   }
-  if (cfg.h % 8 || (cfg.attention && cfg.s % 8)) throw ConfigError("stack: hidden and seq must be multiples of 8");
+  // 16-byte vector loads in LayerNorm / softmax rows
+  if ((cfg.ln && cfg.h % 8) || (cfg.attention && (cfg.s % 8 || cfg.h % 8)))
+    throw ConfigError("stack: hidden (with LayerNorm/attention) and seq must be multiples of 8");
   nblocks_ = cfg.layers * (cfg.attention ? 2 : 1);
   hl_ = cfg.attention ? cfg.heads / t : 0;
   dh_ = cfg.attention ? cfg.h / cfg.heads : 0;
@@ -148,11 +150,27 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
   workers_.resize(static_cast<size_t>(W));
   for (int w = 0; w < W; ++w) workers_[static_cast<size_t>(w)].rank = W > 1 ? w : ctx.rank;
   alloc_all();
-  touched_.assign(static_cast<size_t>(nblocks_), {});
+  touched_.assign(static_cast<size_t>(W), std::vector<std::array<bool, OASES_P_COUNT>>(static_cast<size_t>(nblocks_)));
   loss_touched_.assign(static_cast<size_t>(W), false);
 }
 
-Stack::~Stack() = default;
+Stack::~Stack() {
+  for (cudaEvent_t e : tev_) cudaEventDestroy(e);
+}
+
+void Stack::kernel_stats(double* gemm_ms, double* gemm_flops, int* launches) {
+  double ms = 0.0, fl = 0.0;
+  if (timed_) check_cuda(cudaEventSynchronize(tev_[2 * timed_ - 1]), "kernel stats sync");
+  for (size_t i = 0; i < timed_; ++i) {
+    float t = 0.f;
+    check_cuda(cudaEventElapsedTime(&t, tev_[2 * i], tev_[2 * i + 1]), "elapsed");
+    ms += t;
+    fl += tflops_[i];
+  }
+  *gemm_ms = ms;
+  *gemm_flops = fl;
+  *launches = static_cast<int>(timed_);
+}
 
 int64_t Stack::param_numel(int block, int p) const {
   if (block < 0 || block >= nblocks_ || p < 0 || p >= OASES_P_COUNT) return 0;
@@ -241,15 +259,17 @@ Workspace& Stack::ws_for(Worker& w, int block, int sb) {
   return w.ws[std::min(slot, w.ws.size() - 1)][static_cast<size_t>(sb)];
 }
 
-bool Stack::touch(int block, int p) {
-  bool& t = touched_[static_cast<size_t>(block)][static_cast<size_t>(p)];
+bool Stack::touch(const Worker& w, int block, int p) {
+  const size_t wi = static_cast<size_t>(&w - workers_.data());
+  bool& t = touched_[wi][static_cast<size_t>(block)][static_cast<size_t>(p)];
   const bool was = t;
   t = true;
   return was;
 }
 
 void Stack::begin_step() {
-  for (auto& a : touched_) a.fill(false);
+  for (auto& per_worker : touched_)
+    for (auto& a : per_worker) a.fill(false);
   std::fill(loss_touched_.begin(), loss_touched_.end(), false);
 }
 
@@ -257,10 +277,25 @@ void Stack::gemm(const oases_gemm_desc& d0) {
   oases_gemm_desc d = d0;
   d.dtype = dtype();
   d.max_ctas = ctx_.gemm_max_ctas;
+  const bool timed = timing_ && d.causal == OASES_CAUSAL_NONE && d.batch == 1;
+  if (timed) {
+    while (tev_.size() < 2 * (timed_ + 1)) {
+      cudaEvent_t e;
+      check_cuda(cudaEventCreate(&e), "event");
+      tev_.push_back(e);
+    }
+    if (tflops_.size() < timed_ + 1) tflops_.resize(timed_ + 1);
+    tflops_[timed_] = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);
+    check_cuda(cudaEventRecord(tev_[2 * timed_], ctx_.compute), "record");
+  }
   GemmStatus st = d.dtype == OASES_BF16 ? gemm_tc(d, ctx_.compute) : gemm_simt(d, ctx_.compute);
   if (!st.ok) {
     if (st.cuda) throw CudaError(st.err);
     throw ConfigError(st.err);
+  }
+  if (timed) {
+    check_cuda(cudaEventRecord(tev_[2 * timed_ + 1], ctx_.compute), "record");
+    ++timed_;
   }
   ++launches_;
 }
@@ -633,7 +668,7 @@ void Stack::backward(int wi, int block, int sb) {
     const BlockParams& nxt = w.params[static_cast<size_t>(block + 1)];
     const void* dln = w.bwd_ar[(block + 1) % 2][usb];
     if (cfg_.ln) {
-      const bool acc = touch(block + 1, OASES_P_LN_GAMMA);
+      const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
       check_cuda(layernorm_bwd(dtype(), w.xs[static_cast<size_t>(block + 1)][usb], nxt.p[OASES_P_LN_GAMMA], dln, g,
                                cfg_.residual ? 1 : 0, nxt.g[OASES_P_LN_GAMMA], nxt.g[OASES_P_LN_BETA], acc ? 1 : 0,
                                w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute),
@@ -650,7 +685,7 @@ void Stack::backward(int wi, int block, int sb) {
   BlockParams& bp = w.params[static_cast<size_t>(block)];
   const void* gar = g;
   if (cfg_.p_hidden > 0.f || cfg_.bias) {
-    const bool acc = cfg_.bias ? touch(block, OASES_P_B_ROW) : false;
+    const bool acc = cfg_.bias ? touch(w, block, OASES_P_B_ROW) : false;
     check_cuda(col_pass(dtype(), g, cfg_.p_hidden > 0.f ? w.gar : nullptr, cfg_.bias ? bp.g[OASES_P_B_ROW] : nullptr,
                         acc ? 1 : 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0), ctx_.compute),
                "bdr_bwd");
@@ -668,7 +703,7 @@ void Stack::backward(int wi, int block, int sb) {
   d.a = operand(gar, Ts, h, h, true);
   d.b = operand(ws.act, Ts, nrow, nrow, true);
   d.c = bp.g[OASES_P_W_ROW]; d.ldc = nrow;
-  d.alpha = 1.f; d.accumulate = touch(block, OASES_P_W_ROW) ? 1 : 0;
+  d.alpha = 1.f; d.accumulate = touch(w, block, OASES_P_W_ROW) ? 1 : 0;
   gemm(d);
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
@@ -690,7 +725,7 @@ void Stack::backward(int wi, int block, int sb) {
   }
   // 4. column bias
   if (cfg_.bias) {
-    const bool acc = touch(block, OASES_P_B_COL);
+    const bool acc = touch(w, block, OASES_P_B_COL);
     check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws, Ts,
                         static_cast<int>(ncol), 0.f, 0, 0, ctx_.compute),
                "colsum");
@@ -705,7 +740,7 @@ void Stack::backward(int wi, int block, int sb) {
   d.a = operand(w.dcol, Ts, ncol, ncol, true);
   d.b = operand(ln, Ts, h, h, true);
   d.c = bp.g[OASES_P_W_COL]; d.ldc = h;
-  d.alpha = 1.f; d.accumulate = touch(block, OASES_P_W_COL) ? 1 : 0;
+  d.alpha = 1.f; d.accumulate = touch(w, block, OASES_P_W_COL) ? 1 : 0;
   gemm(d);
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
@@ -726,7 +761,7 @@ void Stack::tail(int wi, int sb) {
   const void* dln = w.bwd_ar[0][usb];
   if (cfg_.ln) {
     const BlockParams& bp = w.params[0];
-    const bool acc = touch(0, OASES_P_LN_GAMMA);
+    const bool acc = touch(w, 0, OASES_P_LN_GAMMA);
     check_cuda(layernorm_bwd(dtype(), w.xs[0][usb], bp.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0,
                              bp.g[OASES_P_LN_GAMMA], bp.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, Ts,
                              static_cast<int>(h), cfg_.eps, ctx_.compute),

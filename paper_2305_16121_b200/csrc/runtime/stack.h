@@ -128,6 +128,11 @@ class Stack {
   double read_loss();
 
   int64_t kernel_launches() const { return launches_; }
+  // Live per-launch timing of the linear-layer GEMMs (QKV/proj/FC1/FC2 and their
+  // dgrad/wgrad) with cudaEvents on the compute stream, for the roofline.
+  void set_kernel_timing(bool on) { timing_ = on; }
+  void reset_kernel_stats() { timed_ = 0; }
+  void kernel_stats(double* gemm_ms, double* gemm_flops, int* launches);
 
  private:
   void alloc_all();
@@ -136,7 +141,7 @@ class Stack {
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);
   void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
   Workspace& ws_for(Worker& w, int block, int sb);
-  bool touch(int block, int p);  // true if the gradient must accumulate (already written this step)
+  bool touch(const Worker& w, int block, int p);  // true if the gradient must accumulate (written this step)
   void* half(void* base, int sb, int64_t cols) const;
 
   Context& ctx_;
@@ -145,9 +150,13 @@ class Stack {
   std::vector<Worker> workers_;
   int nblocks_ = 0;
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
-  std::vector<std::array<bool, OASES_P_COUNT>> touched_;
+  std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;
   int64_t launches_ = 0;
+  bool timing_ = false;
+  size_t timed_ = 0;
+  std::vector<cudaEvent_t> tev_;
+  std::vector<double> tflops_;
 };
 
 // ------------------------------------------------------------------ executor
