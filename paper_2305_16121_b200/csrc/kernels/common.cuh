@@ -55,6 +55,49 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// ---------------------------------------------------------------- 16-byte vectors
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  using raw = float4;
+  __device__ static void unpack(const raw& r, float (&v)[4]) { v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w; }
+  __device__ static raw pack(const float (&v)[4]) { return make_float4(v[0], v[1], v[2], v[3]); }
+};
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  using raw = uint4;
+  __device__ static void unpack(const raw& r, float (&v)[8]) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
+  }
+  __device__ static raw pack(const float (&v)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      w[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void vload(const T* p, float (&v)[Vec<T>::N]) {
+  Vec<T>::unpack(*reinterpret_cast<const typename Vec<T>::raw*>(p), v);
+}
+template <typename T>
+__device__ __forceinline__ void vstore(T* p, const float (&v)[Vec<T>::N]) {
+  *reinterpret_cast<typename Vec<T>::raw*>(p) = Vec<T>::pack(v);
+}
+
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based RNG: the dropout mask of element i under key (seed, offset) is a
 // pure function, so forward, recompute and backward regenerate it bit-exactly.

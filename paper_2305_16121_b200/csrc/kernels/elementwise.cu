@@ -1,6 +1,11 @@
 // Elementwise / column-reduction HBM-bound kernels: bias-dropout-residual,
-// column sums (bias gradients), exact-erf GeLU, the checker's loss head, and
-// the in-process AllReduce used to emulate TMP ranks on one device.
+// column sums (bias gradients), exact-erf GeLU, the checker's loss head, the
+// in-process AllReduce used to emulate TMP ranks on one device, and fills.
+//
+// All bulk paths move 16-byte vectors (8 bf16 / 4 f32) per thread; dropout
+// masks come from Philox (one call per 4 consecutive elements), so forward,
+// recompute and backward regenerate them bit-exactly. Column reductions are
+// two-stage with a fixed summation order (deterministic, no float atomics).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -16,7 +21,49 @@ unsigned grid_for(long long work_items, int per_block) {
   return static_cast<unsigned>(g < 1 ? 1 : g);
 }
 
-// out = residual + dropout(x + bias[col])   (8 elements per thread-iteration)
+// Applies the keep-mask of elements [e, e+V) (e % 4 == 0) to v.
+template <int V>
+__device__ __forceinline__ void apply_dropout(float (&v)[V], unsigned long long e, uint64_t seed, uint64_t offset,
+                                              uint32_t thr, float ks) {
+#pragma unroll
+  for (int q = 0; q < V; q += 4) {
+    uint32_t u[4];
+    Philox::gen(seed, offset, (e + q) >> 2, u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[q + j] = (u[j] >= thr) ? v[q + j] * ks : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------- bias-dropout-residual
+// out = residual + dropout(x + bias[col]); vector path (n % V == 0, cols % V == 0).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bdr_fwd_vec_kernel(const T* __restrict__ x, const T* __restrict__ bias,
+                                                               const T* __restrict__ res, T* __restrict__ out,
+                                                               long long n, int cols, uint32_t thr, float ks, int drop,
+                                                               uint64_t seed, uint64_t offset) {
+  constexpr int V = Vec<T>::N;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * V;
+  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * V; i < n; i += stride) {
+    float v[V];
+    vload(x + i, v);
+    if (bias) {
+      float b[V];
+      vload(bias + (i % cols), b);
+#pragma unroll
+      for (int q = 0; q < V; ++q) v[q] += b[q];
+    }
+    if (drop) apply_dropout<V>(v, static_cast<unsigned long long>(i), seed, offset, thr, ks);
+    if (res) {
+      float r[V];
+      vload(res + i, r);
+#pragma unroll
+      for (int q = 0; q < V; ++q) v[q] += r[q];
+    }
+    vstore(out + i, v);
+  }
+}
+
+// scalar fallback for shapes that are not 16-byte multiples (toy checker sizes)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bdr_fwd_kernel(const T* __restrict__ x, const T* __restrict__ bias,
                                                            const T* __restrict__ res, T* __restrict__ out, long long n,
@@ -39,8 +86,36 @@ __global__ void __launch_bounds__(kThreads) bdr_fwd_kernel(const T* __restrict__
   }
 }
 
-// Column pass: dx = dropout'(dout) (optional, written if dx != null), and
-// partial column sums of dx over a chunk of rows (deterministic).
+// ---------------------------------------------------------------- column pass
+// dx = dropout'(in) (written if dx), partial column sums of dx over a chunk of
+// rows (written if part). Each thread owns V consecutive columns.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) col_pass_vec_kernel(const T* __restrict__ in, T* __restrict__ dx,
+                                                                float* __restrict__ part, long long rows, int cols,
+                                                                int rows_per_chunk, uint32_t thr, float ks, int drop,
+                                                                uint64_t seed, uint64_t offset) {
+  constexpr int V = Vec<T>::N;
+  const int c = (blockIdx.x * kThreads + threadIdx.x) * V;
+  if (c >= cols) return;
+  const long long r0 = static_cast<long long>(blockIdx.y) * rows_per_chunk;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  float s[V] = {};
+  for (long long r = r0; r < r1; ++r) {
+    const long long e = r * cols + c;
+    float v[V];
+    vload(in + e, v);
+    if (drop) apply_dropout<V>(v, static_cast<unsigned long long>(e), seed, offset, thr, ks);
+    if (dx) vstore(dx + e, v);
+#pragma unroll
+    for (int q = 0; q < V; ++q) s[q] += v[q];
+  }
+  if (part) {
+    float* p = part + static_cast<long long>(blockIdx.y) * cols + c;
+#pragma unroll
+    for (int q = 0; q < V; ++q) p[q] = s[q];
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) col_pass_kernel(const T* __restrict__ in, T* __restrict__ dx,
                                                             float* __restrict__ part, long long rows, int cols,
@@ -66,15 +141,27 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(const T* __restrict_
   if (part) part[static_cast<long long>(blockIdx.y) * cols + c] = s;
 }
 
-__global__ void col_finalize_kernel(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out,
-                                    int acc) {
-  const int c = blockIdx.x * kThreads + threadIdx.x;
-  if (c >= cols) return;
+// out[c] (+)= sum_k part[k][c], fixed order: 8 interleaved partial sums per
+// column, combined in index order.
+__global__ void __launch_bounds__(kThreads) col_finalize_kernel(const float* __restrict__ part, int chunks, int cols,
+                                                                float* __restrict__ out, int acc) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int k = 0; k < chunks; ++k) s += part[static_cast<long long>(k) * cols + c];
-  out[c] = acc ? out[c] + s : s;
+  if (c < cols)
+    for (int k = g; k < chunks; k += 8) s += part[static_cast<long long>(k) * cols + c];
+  sm[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += sm[j][lane];
+    out[c] = acc ? out[c] + t : t;
+  }
 }
 
+// ---------------------------------------------------------------- GeLU / loss
 template <typename T>
 __global__ void __launch_bounds__(kThreads) gelu_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, long long n) {
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -111,13 +198,23 @@ __global__ void __launch_bounds__(kThreads) gelu_sq_loss_kernel(const T* __restr
     part[blockIdx.x] = s;
   }
 }
-__global__ void loss_finalize_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out, int acc) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+
+// Deterministic tree over the block partials (fixed order).
+__global__ void __launch_bounds__(kThreads) loss_finalize_kernel(const double* __restrict__ part, int nparts,
+                                                                 double* __restrict__ out, int acc) {
+  __shared__ double sm[kThreads];
   double s = 0.0;
-  for (int i = 0; i < nparts; ++i) s += part[i];
-  *out = acc ? *out + s : s;
+  for (int i = threadIdx.x; i < nparts; i += kThreads) s += part[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = acc ? *out + sm[0] : sm[0];
 }
 
+// ---------------------------------------------------------------- in-process AllReduce
 struct BufList {
   void* p[8];
 };
@@ -132,54 +229,133 @@ __global__ void __launch_bounds__(kThreads) local_allreduce_kernel(BufList b, in
   }
 }
 
-int chunks_for(long long rows) {
-  long long c = (rows + 31) / 32;
-  if (c > 512) c = 512;
-  return static_cast<int>(c < 1 ? 1 : c);
+// ---------------------------------------------------------------- fills
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fill_uniform_kernel(T* p, long long n, float scale, uint64_t seed,
+                                                                uint64_t offset) {
+  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x * 4) {
+    uint32_t u[4];
+    Philox::gen(seed, offset, static_cast<unsigned long long>(i) >> 2, u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i + q >= n) break;
+      const float r = (static_cast<float>(u[q] >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0,1)
+      p[i + q] = from_f<T>((2.f * r - 1.f) * scale);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fill_const_kernel(T* p, long long n, float v) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = from_f<T>(v);
+}
+
+template <typename S, typename D>
+__global__ void __launch_bounds__(kThreads) convert_kernel(const S* src, D* dst, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = from_f<D>(to_f(src[i]));
+}
+
+struct ColSplit {
+  int chunks, rows_per_chunk;
+};
+// ~4 CTAs per SM over (column blocks x row chunks)
+ColSplit col_split(long long rows, int col_blocks) {
+  long long chunks = (4LL * 148 + col_blocks - 1) / col_blocks;
+  if (chunks > rows) chunks = rows;
+  if (chunks < 1) chunks = 1;
+  const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
+  return {static_cast<int>((rows + rpc - 1) / rpc), rpc};
+}
+
+template <typename T>
+bool vec_ok(const void* a, const void* b, long long n, int cols) {
+  constexpr int V = 16 / sizeof(T);
+  auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+  return n % V == 0 && cols % V == 0 && al(a) && al(b);
 }
 
 }  // namespace
 
 size_t colsum_workspace(long long rows, int cols) {
-  return static_cast<size_t>(chunks_for(rows)) * cols * sizeof(float) + 256;
+  // upper bound over both the vector (V columns per thread) and scalar layouts
+  const ColSplit s = col_split(rows, (cols + kThreads - 1) / kThreads);
+  const ColSplit v = col_split(rows, (cols + kThreads * 4 - 1) / (kThreads * 4));
+  return static_cast<size_t>(s.chunks > v.chunks ? s.chunks : v.chunks) * cols * sizeof(float) + 256;
 }
 
 cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias, const void* res, void* out,
                                       long long rows, int cols, float p, uint64_t seed, uint64_t offset,
                                       cudaStream_t st) {
   const long long n = rows * cols;
-  const unsigned g = grid_for(n, kThreads * 4);
   const int drop = p > 0.f;
   const uint32_t thr = dropout_threshold(p);
   const float ks = drop ? 1.f / (1.f - p) : 1.f;
-  if (dtype == OASES_BF16)
-    bdr_fwd_kernel<__nv_bfloat16><<<g, kThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(bias),
-        static_cast<const __nv_bfloat16*>(res), static_cast<__nv_bfloat16*>(out), n, cols, thr, ks, drop, seed, offset);
-  else
-    bdr_fwd_kernel<float><<<g, kThreads, 0, st>>>(static_cast<const float*>(x), static_cast<const float*>(bias),
-                                                  static_cast<const float*>(res), static_cast<float*>(out), n, cols, thr,
-                                                  ks, drop, seed, offset);
+  if (dtype == OASES_BF16) {
+    using T = __nv_bfloat16;
+    auto X = static_cast<const T*>(x);
+    auto B = static_cast<const T*>(bias);
+    auto R = static_cast<const T*>(res);
+    auto O = static_cast<T*>(out);
+    if (vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
+      bdr_fwd_vec_kernel<T><<<grid_for(n, kThreads * 8), kThreads, 0, st>>>(X, B, R, O, n, cols, thr, ks, drop, seed,
+                                                                          offset);
+    else
+      bdr_fwd_kernel<T><<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(X, B, R, O, n, cols, thr, ks, drop, seed,
+                                                                      offset);
+  } else {
+    using T = float;
+    auto X = static_cast<const T*>(x);
+    auto B = static_cast<const T*>(bias);
+    auto R = static_cast<const T*>(res);
+    auto O = static_cast<T*>(out);
+    if (vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
+      bdr_fwd_vec_kernel<T><<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(X, B, R, O, n, cols, thr, ks, drop, seed,
+                                                                          offset);
+    else
+      bdr_fwd_kernel<T><<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(X, B, R, O, n, cols, thr, ks, drop, seed,
+                                                                      offset);
+  }
   return cudaGetLastError();
+}
+
+template <typename T>
+static void col_pass_t(const void* in, void* dx, float* part, long long rows, int cols, uint32_t thr, float ks,
+                       int drop, uint64_t seed, uint64_t offset, int* chunks_out, cudaStream_t st) {
+  constexpr int V = 16 / sizeof(T);
+  if (vec_ok<T>(in, dx, rows * cols, cols)) {
+    const int cb = (cols + kThreads * V - 1) / (kThreads * V);
+    const ColSplit sp = col_split(rows, cb);
+    col_pass_vec_kernel<T><<<dim3(cb, sp.chunks), kThreads, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(dx),
+                                                                      part, rows, cols, sp.rows_per_chunk, thr, ks,
+                                                                      drop, seed, offset);
+    *chunks_out = sp.chunks;
+  } else {
+    const int cb = (cols + kThreads - 1) / kThreads;
+    const ColSplit sp = col_split(rows, cb);
+    col_pass_kernel<T><<<dim3(cb, sp.chunks), kThreads, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(dx), part,
+                                                                  rows, cols, sp.rows_per_chunk, thr, ks, drop, seed,
+                                                                  offset);
+    *chunks_out = sp.chunks;
+  }
 }
 
 cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, void* ws, long long rows, int cols,
                      float p, uint64_t seed, uint64_t offset, cudaStream_t st) {
-  const int chunks = chunks_for(rows);
-  const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
   float* part = out ? static_cast<float*>(ws) : nullptr;
-  dim3 grid((cols + kThreads - 1) / kThreads, chunks);
   const int drop = p > 0.f;
   const uint32_t thr = dropout_threshold(p);
   const float ks = drop ? 1.f / (1.f - p) : 1.f;
+  int chunks = 0;
   if (dtype == OASES_BF16)
-    col_pass_kernel<__nv_bfloat16><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in),
-                                                              static_cast<__nv_bfloat16*>(dx), part, rows, cols, rpc,
-                                                              thr, ks, drop, seed, offset);
+    col_pass_t<__nv_bfloat16>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
   else
-    col_pass_kernel<float><<<grid, kThreads, 0, st>>>(static_cast<const float*>(in), static_cast<float*>(dx), part,
-                                                      rows, cols, rpc, thr, ks, drop, seed, offset);
-  if (out) col_finalize_kernel<<<(cols + kThreads - 1) / kThreads, kThreads, 0, st>>>(part, chunks, cols, out, acc);
+    col_pass_t<float>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
+  if (out) col_finalize_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
   return cudaGetLastError();
 }
 
@@ -214,7 +390,7 @@ cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int a
                                                 ws, n);
   else
     gelu_sq_loss_kernel<<<g, kThreads, 0, st>>>(static_cast<const float*>(z), static_cast<float*>(dz), ws, n);
-  loss_finalize_kernel<<<1, 32, 0, st>>>(ws, static_cast<int>(g), loss, acc);
+  loss_finalize_kernel<<<1, kThreads, 0, st>>>(ws, static_cast<int>(g), loss, acc);
   return cudaGetLastError();
 }
 
@@ -227,43 +403,6 @@ cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cu
   else local_allreduce_kernel<float><<<g, kThreads, 0, st>>>(b, w, n);
   return cudaGetLastError();
 }
-
-}  // namespace oases
-
-namespace oases {
-namespace {
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads) fill_uniform_kernel(T* p, long long n, float scale, uint64_t seed,
-                                                                uint64_t offset) {
-  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x * 4) {
-    uint32_t u[4];
-    Philox::gen(seed, offset, static_cast<unsigned long long>(i) >> 2, u);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (i + q >= n) break;
-      const float r = (static_cast<float>(u[q] >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0,1)
-      p[i + q] = from_f<T>((2.f * r - 1.f) * scale);
-    }
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads) fill_const_kernel(T* p, long long n, float v) {
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    p[i] = from_f<T>(v);
-}
-
-template <typename S, typename D>
-__global__ void __launch_bounds__(kThreads) convert_kernel(const S* src, D* dst, long long n) {
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    dst[i] = from_f<D>(to_f(src[i]));
-}
-
-}  // namespace
 
 cudaError_t fill_uniform(int dtype, void* p, long long n, float scale, uint64_t seed, uint64_t offset,
                          cudaStream_t st) {

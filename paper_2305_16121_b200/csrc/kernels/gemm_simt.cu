@@ -40,14 +40,20 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
   const float* A = p.a + (p.a_row[0] * zo + p.a_row[1] * zi) * p.lda + (p.a_col[0] * zo + p.a_col[1] * zi);
   const float* B = p.b + (p.b_row[0] * zo + p.b_row[1] * zi) * p.ldb + (p.b_col[0] * zo + p.b_col[1] * zi);
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < p.K; k0 += TK) {
+  // Causal K ranges at the tcgen05 kernel's 128-row tile granularity: the
+  // softmax only writes the band the tensor-core kernel reads.
+  const int base = (m0 / 128) * 128;
+  int kbeg = 0, kend = p.K;
+  if (p.causal == OASES_CAUSAL_K_UPTO_M) kend = min(p.K, base + 128);
+  if (p.causal == OASES_CAUSAL_K_FROM_M) kbeg = base;
+  for (int k0 = kbeg; k0 < kend; k0 += TK) {
     // 64x16 tile of A and of B: 1024 elements, 4 per thread.
     for (int i = threadIdx.x; i < TM * TK; i += 256) {
       int mm, kk;
       if (p.a_mn) { mm = i % TM; kk = i / TM; } else { kk = i % TK; mm = i / TK; }
       const int m = m0 + mm, k = k0 + kk;
       float v = 0.f;
-      if (m < p.M && k < p.K) v = p.a_mn ? A[static_cast<long long>(k) * p.lda + m] : A[static_cast<long long>(m) * p.lda + k];
+      if (m < p.M && k < kend) v = p.a_mn ? A[static_cast<long long>(k) * p.lda + m] : A[static_cast<long long>(m) * p.lda + k];
       As[kk][mm] = v;
     }
     for (int i = threadIdx.x; i < TN * TK; i += 256) {
@@ -55,7 +61,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
       if (p.b_mn) { nn = i % TN; kk = i / TN; } else { kk = i % TK; nn = i / TK; }
       const int n = n0 + nn, k = k0 + kk;
       float v = 0.f;
-      if (n < p.N && k < p.K) v = p.b_mn ? B[static_cast<long long>(k) * p.ldb + n] : B[static_cast<long long>(n) * p.ldb + k];
+      if (n < p.N && k < kend) v = p.b_mn ? B[static_cast<long long>(k) * p.ldb + n] : B[static_cast<long long>(n) * p.ldb + k];
       Bs[kk][nn] = v;
     }
     __syncthreads();

@@ -10,48 +10,6 @@
 namespace oases {
 namespace {
 
-template <typename T>
-struct Vec;
-template <>
-struct Vec<float> {
-  static constexpr int N = 4;
-  using raw = float4;
-  __device__ static void unpack(const raw& r, float (&v)[4]) { v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w; }
-  __device__ static raw pack(const float (&v)[4]) { return make_float4(v[0], v[1], v[2], v[3]); }
-};
-template <>
-struct Vec<__nv_bfloat16> {
-  static constexpr int N = 8;
-  using raw = uint4;
-  __device__ static void unpack(const raw& r, float (&v)[8]) {
-    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
-      v[2 * j] = f.x;
-      v[2 * j + 1] = f.y;
-    }
-  }
-  __device__ static raw pack(const float (&v)[8]) {
-    uint32_t w[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-      w[j] = *reinterpret_cast<uint32_t*>(&h);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
-  }
-};
-
-template <typename T>
-__device__ __forceinline__ void vload(const T* p, float (&v)[Vec<T>::N]) {
-  Vec<T>::unpack(*reinterpret_cast<const typename Vec<T>::raw*>(p), v);
-}
-template <typename T>
-__device__ __forceinline__ void vstore(T* p, const float (&v)[Vec<T>::N]) {
-  *reinterpret_cast<typename Vec<T>::raw*>(p) = Vec<T>::pack(v);
-}
-
 // Chan/Welford merge of (n, mean, M2) across a warp.
 __device__ __forceinline__ void welford_warp(float& n, float& mean, float& m2) {
 #pragma unroll
@@ -160,39 +118,175 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ x, co
   }
 }
 
+// Register-cached variants: the row lives in NV 16-byte vectors per lane, so
+// x (and dy) are read from HBM exactly once and the statistics are exact
+// two-pass (mean, then centred variance) in f32.
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) ln_fwd_cached_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
+                                                            const T* __restrict__ beta, T* __restrict__ y,
+                                                            long long rows, int cols, float eps) {
+  constexpr int V = Vec<T>::N;
+  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const T* xr = x + row * cols;
+  float v[NV][V];
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = (t * 32 + lane) * V;
+    if (c < cols) {
+      vload(xr + c, v[t]);
+#pragma unroll
+      for (int e = 0; e < V; ++e) sum += v[t][e];
+    }
+  }
+  const float mean = warp_sum(sum) / static_cast<float>(cols);
+  float var = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t)
+    if ((t * 32 + lane) * V < cols)
+#pragma unroll
+      for (int e = 0; e < V; ++e) var += (v[t][e] - mean) * (v[t][e] - mean);
+  const float rstd = rsqrtf(warp_sum(var) / static_cast<float>(cols) + eps);
+  T* yr = y + row * cols;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = (t * 32 + lane) * V;
+    if (c >= cols) continue;
+    float g[V], b[V];
+    vload(gamma + c, g);
+    vload(beta + c, b);
+#pragma unroll
+    for (int e = 0; e < V; ++e) v[t][e] = (v[t][e] - mean) * rstd * g[e] + b[e];
+    vstore(yr + c, v[t]);
+  }
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) ln_bwd_cached_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
+                                                            const T* __restrict__ dy, T* __restrict__ dx, int acc,
+                                                            float2* __restrict__ stats, long long rows, int cols,
+                                                            float eps) {
+  constexpr int V = Vec<T>::N;
+  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const T* xr = x + row * cols;
+  const T* dyr = dy + row * cols;
+  float xv[NV][V], gv[NV][V];
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = (t * 32 + lane) * V;
+    if (c < cols) {
+      vload(xr + c, xv[t]);
+      float d[V], g[V];
+      vload(dyr + c, d);
+      vload(gamma + c, g);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        sum += xv[t][e];
+        gv[t][e] = d[e] * g[e];
+      }
+    }
+  }
+  const float mean = warp_sum(sum) / static_cast<float>(cols);
+  float var = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t)
+    if ((t * 32 + lane) * V < cols)
+#pragma unroll
+      for (int e = 0; e < V; ++e) var += (xv[t][e] - mean) * (xv[t][e] - mean);
+  const float rstd = rsqrtf(warp_sum(var) / static_cast<float>(cols) + eps);
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t)
+    if ((t * 32 + lane) * V < cols)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        xv[t][e] = (xv[t][e] - mean) * rstd;  // xhat
+        s1 += gv[t][e];
+        s2 += gv[t][e] * xv[t][e];
+      }
+  s1 = warp_sum(s1) / static_cast<float>(cols);
+  s2 = warp_sum(s2) / static_cast<float>(cols);
+  if (lane == 0) stats[row] = make_float2(mean, rstd);
+  T* dxr = dx + row * cols;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = (t * 32 + lane) * V;
+    if (c >= cols) continue;
+    float o[V];
+    if (acc) vload(dxr + c, o);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const float r = rstd * (gv[t][e] - s1 - xv[t][e] * s2);
+      o[e] = acc ? o[e] + r : r;
+    }
+    vstore(dxr + c, o);
+  }
+}
+
 // Column partial sums over a chunk of rows: part[chunk][0][c] = sum dy*xhat,
-// part[chunk][1][c] = sum dy. Threads own columns -> coalesced, deterministic.
+// part[chunk][1][c] = sum dy. Each thread owns V consecutive columns.
 template <typename T>
 __global__ void __launch_bounds__(256) ln_param_partial_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                                                                const float2* __restrict__ stats, float* __restrict__ part,
                                                                long long rows, int cols, int rows_per_chunk) {
-  const int c = blockIdx.x * 256 + threadIdx.x;
+  constexpr int V = Vec<T>::N;
+  const int c = (blockIdx.x * 256 + threadIdx.x) * V;
   if (c >= cols) return;
   const long long r0 = static_cast<long long>(blockIdx.y) * rows_per_chunk;
-  long long r1 = r0 + rows_per_chunk;
-  if (r1 > rows) r1 = rows;
-  float sg = 0.f, sb = 0.f;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  float sg[V] = {}, sb[V] = {};
   for (long long r = r0; r < r1; ++r) {
     const float2 st = stats[r];
-    const float d = to_f(dy[r * cols + c]);
-    sg += d * (to_f(x[r * cols + c]) - st.x) * st.y;
-    sb += d;
+    float d[V], xv[V];
+    vload(dy + r * cols + c, d);
+    vload(x + r * cols + c, xv);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      sg[e] += d[e] * (xv[e] - st.x) * st.y;
+      sb[e] += d[e];
+    }
   }
-  part[(static_cast<long long>(blockIdx.y) * 2 + 0) * cols + c] = sg;
-  part[(static_cast<long long>(blockIdx.y) * 2 + 1) * cols + c] = sb;
+  float* p0 = part + (static_cast<long long>(blockIdx.y) * 2 + 0) * cols + c;
+  float* p1 = part + (static_cast<long long>(blockIdx.y) * 2 + 1) * cols + c;
+#pragma unroll
+  for (int e = 0; e < V; ++e) {
+    p0[e] = sg[e];
+    p1[e] = sb[e];
+  }
 }
 
-__global__ void colpair_finalize_kernel(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out0,
-                                        float* __restrict__ out1, int acc) {
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  if (c >= cols) return;
+// out0/out1[c] (+)= sum_k part[k][0/1][c] in a fixed order (8 interleaved
+// partial sums per column combined in index order).
+__global__ void __launch_bounds__(256) colpair_finalize_kernel(const float* __restrict__ part, int chunks, int cols,
+                                                               float* __restrict__ out0, float* __restrict__ out1,
+                                                               int acc) {
+  __shared__ float sm[2][8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
-  for (int k = 0; k < chunks; ++k) {
-    a += part[(static_cast<long long>(k) * 2 + 0) * cols + c];
-    b += part[(static_cast<long long>(k) * 2 + 1) * cols + c];
+  if (c < cols)
+    for (int k = g; k < chunks; k += 8) {
+      a += part[(static_cast<long long>(k) * 2 + 0) * cols + c];
+      b += part[(static_cast<long long>(k) * 2 + 1) * cols + c];
+    }
+  sm[0][g][lane] = a;
+  sm[1][g][lane] = b;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float ta = 0.f, tb = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ta += sm[0][j][lane];
+      tb += sm[1][j][lane];
+    }
+    if (out0) out0[c] = acc ? out0[c] + ta : ta;
+    if (out1) out1[c] = acc ? out1[c] + tb : tb;
   }
-  if (out0) out0[c] = acc ? out0[c] + a : a;
-  if (out1) out1[c] = acc ? out1[c] + b : b;
 }
 
 // ------------------------------------------------------------------ softmax
@@ -251,14 +345,20 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const T* __restrict__ 
   const float inv = 1.f / sum;
   T* pr = p + row * seq;
   T* pdr = pd ? pd + row * seq : nullptr;
+  // Only the band [0, round_up(i+1, 128)) is ever read by the causal P.V /
+  // P^T.dO GEMMs (their K ranges stop at the 128-row tile edge), so the zero
+  // tail beyond it is never written.
+  const int band = min(seq, ((i + 128) / 128) * 128);
 #pragma unroll
   for (int t = 0; t < NV; ++t) {
     const int c = (t * 32 + lane) * V;
-    if (c >= seq) continue;
+    if (c >= band) continue;
 #pragma unroll
     for (int e = 0; e < V; ++e) v[t][e] *= inv;
     vstore(pr + c, v[t]);
-    if (pdr) {
+    if (pdr && c > i) {
+      vstore(pdr + c, v[t]);  // all zeros: no mask needed
+    } else if (pdr) {
       const unsigned long long base = global_row(row, seq, hl, hg, hoff) * seq + c;
 #pragma unroll
       for (int e = 0; e < V; e += 4) {
@@ -312,10 +412,11 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ 
     }
   }
   dot = warp_sum(dot);
+  const int band = min(seq, ((i + 128) / 128) * 128);  // see softmax_fwd_kernel
 #pragma unroll
   for (int t = 0; t < NV; ++t) {
     const int c = (t * 32 + lane) * V;
-    if (c >= seq) continue;
+    if (c >= band) continue;
 #pragma unroll
     for (int e = 0; e < V; ++e) pv[t][e] = scale * pv[t][e] * (dv[t][e] - dot);
     vstore(ds + row * seq + c, pv[t]);
@@ -351,59 +452,96 @@ struct SoftmaxBwdL {
   }
 };
 
-int param_chunks(long long rows) {
-  long long c = (rows + 63) / 64;
-  if (c > 256) c = 256;
-  return static_cast<int>(c < 1 ? 1 : c);
+template <typename T, int NV>
+struct LnFwdL {
+  template <typename... A>
+  static void launch(unsigned grid, cudaStream_t st, A... a) {
+    ln_fwd_cached_kernel<T, NV><<<grid, 256, 0, st>>>(a...);
+  }
+};
+template <typename T, int NV>
+struct LnBwdL {
+  template <typename... A>
+  static void launch(unsigned grid, cudaStream_t st, A... a) {
+    ln_bwd_cached_kernel<T, NV><<<grid, 256, 0, st>>>(a...);
+  }
+};
+
+// (column blocks) x (row chunks) ~ 4 CTAs per SM
+struct ParamSplit {
+  int col_blocks, chunks, rows_per_chunk;
+};
+template <typename T>
+ParamSplit param_split(long long rows, int cols) {
+  constexpr int V = Vec<T>::N;
+  const int cb = (cols + 256 * V - 1) / (256 * V);
+  long long chunks = (4LL * 148 + cb - 1) / cb;
+  if (chunks > rows) chunks = rows;
+  if (chunks < 1) chunks = 1;
+  const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
+  return {cb, static_cast<int>((rows + rpc - 1) / rpc), rpc};
+}
+
+template <typename T>
+cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx, int acc_dx, float* dgamma,
+                     float* dbeta, int acc_params, void* workspace, long long rows, int cols, float eps,
+                     cudaStream_t st) {
+  float2* stats = static_cast<float2*>(workspace);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) +
+                                         ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)));
+  auto X = static_cast<const T*>(x);
+  auto DY = static_cast<const T*>(dy);
+  auto G = static_cast<const T*>(gamma);
+  auto DX = static_cast<T*>(dx);
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  if (cols <= 16 * 32 * Vec<T>::N) {
+    const cudaError_t e = launch_rows_nv<T, LnBwdL>(cols, rows, st, X, G, DY, DX, acc_dx, stats, rows, cols, eps);
+    if (e != cudaSuccess) return e;
+  } else {
+    ln_bwd_kernel<T><<<grid, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows, cols, eps);
+  }
+  if (dgamma || dbeta) {
+    const ParamSplit sp = param_split<T>(rows, cols);
+    ln_param_partial_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
+                                                                               sp.rows_per_chunk);
+    colpair_finalize_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta, acc_params);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y, long long rows, int cols, float eps,
+                     cudaStream_t st) {
+  auto X = static_cast<const T*>(x);
+  auto G = static_cast<const T*>(gamma);
+  auto B = static_cast<const T*>(beta);
+  auto Y = static_cast<T*>(y);
+  if (cols <= 16 * 32 * Vec<T>::N) return launch_rows_nv<T, LnFwdL>(cols, rows, st, X, G, B, Y, rows, cols, eps);
+  ln_fwd_kernel<T><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(X, G, B, Y, rows, cols, eps);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 size_t layernorm_bwd_workspace(long long rows, int cols) {
-  const int chunks = param_chunks(rows);
-  return static_cast<size_t>(rows) * sizeof(float2) + static_cast<size_t>(chunks) * 2 * cols * sizeof(float) + 256;
+  const ParamSplit a = param_split<float>(rows, cols), b = param_split<__nv_bfloat16>(rows, cols);
+  const int chunks = a.chunks > b.chunks ? a.chunks : b.chunks;
+  return ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)) +
+         static_cast<size_t>(chunks) * 2 * cols * sizeof(float) + 256;
 }
 
 cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, long long rows,
                           int cols, float eps, cudaStream_t st) {
-  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
-  if (dtype == OASES_BF16)
-    ln_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(gamma),
-        static_cast<const __nv_bfloat16*>(beta), static_cast<__nv_bfloat16*>(y), rows, cols, eps);
-  else
-    ln_fwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), static_cast<const float*>(gamma),
-                                               static_cast<const float*>(beta), static_cast<float*>(y), rows, cols,
-                                               eps);
-  return cudaGetLastError();
+  if (dtype == OASES_BF16) return ln_fwd_t<__nv_bfloat16>(x, gamma, beta, y, rows, cols, eps, st);
+  return ln_fwd_t<float>(x, gamma, beta, y, rows, cols, eps, st);
 }
 
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,
                           float* dgamma, float* dbeta, int acc_params, void* workspace, long long rows, int cols,
                           float eps, cudaStream_t st) {
-  float2* stats = static_cast<float2*>(workspace);
-  float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) +
-                                         ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)));
-  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
-  const int chunks = param_chunks(rows);
-  const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
-  dim3 pgrid((cols + 255) / 256, chunks);
-  if (dtype == OASES_BF16) {
-    auto X = static_cast<const __nv_bfloat16*>(x);
-    auto DY = static_cast<const __nv_bfloat16*>(dy);
-    ln_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(X, static_cast<const __nv_bfloat16*>(gamma), DY,
-                                                       static_cast<__nv_bfloat16*>(dx), acc_dx, stats, rows, cols, eps);
-    if (dgamma || dbeta) ln_param_partial_kernel<__nv_bfloat16><<<pgrid, 256, 0, st>>>(X, DY, stats, part, rows, cols, rpc);
-  } else {
-    auto X = static_cast<const float*>(x);
-    auto DY = static_cast<const float*>(dy);
-    ln_bwd_kernel<float><<<grid, 256, 0, st>>>(X, static_cast<const float*>(gamma), DY, static_cast<float*>(dx),
-                                               acc_dx, stats, rows, cols, eps);
-    if (dgamma || dbeta) ln_param_partial_kernel<float><<<pgrid, 256, 0, st>>>(X, DY, stats, part, rows, cols, rpc);
-  }
-  if (dgamma || dbeta)
-    colpair_finalize_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, chunks, cols, dgamma, dbeta, acc_params);
-  return cudaGetLastError();
+  if (dtype == OASES_BF16)
+    return ln_bwd_t<__nv_bfloat16>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st);
+  return ln_bwd_t<float>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st);
 }
 
 cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,

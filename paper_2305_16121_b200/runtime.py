@@ -11,6 +11,7 @@ operator API for this path, over the C-ABI of include/oases.h).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 from dataclasses import dataclass, field
 
@@ -21,6 +22,15 @@ from . import tmpsim as t
 from ._capi import check
 
 LN_GAMMA, LN_BETA, W_COL, B_COL, W_ROW, B_ROW = range(6)
+
+_SHUTTING_DOWN = [False]
+
+
+@atexit.register
+def _mark_shutdown():
+    # Native handles still alive at interpreter exit are leaked on purpose: the
+    # CUDA runtime may already be tearing down when their finalisers run.
+    _SHUTTING_DOWN[0] = True
 
 VARIANTS = {"Default": t.ScheduleVariant.Default, "IntraPass": t.ScheduleVariant.IntraPass,
             "CrossPass": t.ScheduleVariant.CrossPass, "Oases": t.ScheduleVariant.Oases}
@@ -121,6 +131,8 @@ class Context:
             self._h = C.c_void_p()
 
     def __del__(self):
+        if _SHUTTING_DOWN[0]:
+            return
         try:
             self.close()
         except Exception:
@@ -167,6 +179,8 @@ class LayerStack:
             self._h = C.c_void_p()
 
     def __del__(self):
+        if _SHUTTING_DOWN[0]:
+            return
         try:
             self.close()
         except Exception:
