@@ -17,6 +17,7 @@
 //               vectorised global stores
 // Tile 128 x BN x 64, BN in {128, 256}, SWIZZLE_128B operand tiles.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <cudaTypedefs.h>
 
@@ -37,7 +38,8 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr int STG_BYTES = 4 * 32 * 128;  // epilogue staging, 4 KB per epilogue warp
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STG_BYTES + BAR_BYTES + 1024;
   static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
 };
 
@@ -155,39 +157,110 @@ __device__ __forceinline__ void load32<__nv_bfloat16>(const __nv_bfloat16* src, 
   }
 }
 
+template <typename T>
+__device__ __forceinline__ void load4(const T* src, float (&v)[4]);
+template <>
+__device__ __forceinline__ void load4<float>(const float* src, float (&v)[4]) {
+  const float4 f = *reinterpret_cast<const float4*>(src);
+  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+template <>
+__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* src, float (&v)[4]) {
+  const uint2 u = *reinterpret_cast<const uint2*>(src);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <typename T>
+__device__ __forceinline__ void store4(T* dst, const float (&v)[4]);
+template <>
+__device__ __forceinline__ void store4<float>(float* dst, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[4]) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(dst) = u;
+}
+
+// Fused epilogue math for 4 consecutive output columns of one row (global
+// offsets already resolved): alpha, bias, dGeLU(aux), accumulate, store, GeLU.
 template <typename OutT>
-__device__ __forceinline__ void epilogue_chunk(const TcParams& p, int z, int m, int n, float (&v)[32]) {
-  const int valid = p.N - n < 32 ? p.N - n : 32;
-  const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
-  const long long row = p.c_row_off[0] * zo + p.c_row_off[1] * zi + m;
-  const long long col = p.c_col_off[0] * zo + p.c_col_off[1] * zi + n;
-  const long long off = row * p.ldc + col;
+__device__ __forceinline__ void epilogue4(const TcParams& p, long long off, int n, const float4 a) {
+  float v[4] = {a.x * p.alpha, a.y * p.alpha, a.z * p.alpha, a.w * p.alpha};
+  const int valid = p.N - n < 4 ? p.N - n : 4;
   OutT* c = reinterpret_cast<OutT*>(p.c) + off;
+  if (valid == 4) {
+    if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias) {
+      const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p.bias) + n);
+      const float2 b0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 b1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      v[0] += b0.x; v[1] += b0.y; v[2] += b1.x; v[3] += b1.y;
+    }
+    if (p.epilogue == OASES_EPI_DGELU) {
+      float x[4];
+      load4<OutT>(reinterpret_cast<const OutT*>(p.aux) + off, x);
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
-  if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias) {
-    float b[32];
-    load32<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(p.bias) + n, b, valid);
+      for (int i = 0; i < 4; ++i) v[i] *= gelu_grad_f(x[i]);
+    }
+    if (p.accumulate) {
+      float o[4];
+      load4<OutT>(c, o);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += b[i];
+      for (int i = 0; i < 4; ++i) v[i] += o[i];
+    }
+    store4<OutT>(c, v);
+    if (p.epilogue == OASES_EPI_BIAS_GELU) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = gelu_f(v[i]);
+      store4<OutT>(reinterpret_cast<OutT*>(p.c2) + off, v);
+    }
+    return;
   }
-  if (p.epilogue == OASES_EPI_DGELU) {
-    float a[32];
-    load32<OutT>(reinterpret_cast<const OutT*>(p.aux) + off, a, valid);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(a[i]);
+  for (int i = 0; i < valid; ++i) {
+    float x = v[i];
+    if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias)
+      x += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n + i]);
+    if (p.epilogue == OASES_EPI_DGELU) x *= gelu_grad_f(to_f(reinterpret_cast<const OutT*>(p.aux)[off + i]));
+    if (p.accumulate) x += to_f(c[i]);
+    c[i] = from_f<OutT>(x);
+    if (p.epilogue == OASES_EPI_BIAS_GELU) reinterpret_cast<OutT*>(p.c2)[off + i] = from_f<OutT>(gelu_f(x));
   }
-  if (p.accumulate) {
-    float o[32];
-    load32<OutT>(c, o, valid);
+}
+
+// One warp's 32-row stripe of an accumulator tile. TMEM -> registers (thread =
+// row) -> 128B-swizzled smem staging -> read back as 4-wide row segments so
+// every global access of the warp covers 4 contiguous rows (8 lanes per row)
+// instead of 32 scattered rows -> fused epilogue -> global.
+template <typename OutT>
+__device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_base, int n0, int ncols,
+                                                uint32_t taddr, float4* stg, int lane) {
+  const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
+  const long long row0 = p.c_row_off[0] * zo + p.c_row_off[1] * zi;
+  const long long col0 = p.c_col_off[0] * zo + p.c_col_off[1] * zi;
+#pragma unroll 1
+  for (int c = 0; c < ncols / 32; ++c) {
+    const int nc = n0 + c * 32;
+    uint32_t r[32];
+    tmem_ld32(taddr + static_cast<uint32_t>(c * 32), r);
+    tmem_wait_ld();
+    if (nc >= p.N) continue;  // warp-uniform
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += o[i];
-  }
-  store32<OutT>(c, v, valid);
-  if (p.epilogue == OASES_EPI_BIAS_GELU) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
-    store32<OutT>(reinterpret_cast<OutT*>(p.c2) + off, v, valid);
+    for (int j = 0; j < 8; ++j)
+      stg[lane * 8 + (j ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+    __syncwarp();
+#pragma unroll 2
+    for (int it = 0; it < 8; ++it) {
+      const int row = it * 4 + (lane >> 3), ch = lane & 7;
+      const float4 a = stg[row * 8 + (ch ^ (row & 7))];
+      const int m = m_base + row, n = nc + ch * 4;
+      if (m < p.M && n < p.N) epilogue4<OutT>(p, (row0 + m) * p.ldc + col0 + n, n, a);
+    }
+    __syncwarp();
   }
 }
 
@@ -199,7 +272,8 @@ __global__ void __launch_bounds__(192, 1)
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  float4* stg_all = reinterpret_cast<float4*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STG_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -308,21 +382,10 @@ __global__ void __launch_bounds__(192, 1)
       if (!decode_tile<BN>(p, t, ti)) continue;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int m = ti.m0 + q * 32 + lane;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
-        tmem_wait_ld();
-        const int n = ti.n0 + c * 32;
-        if (m < p.M && n < p.N) {
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (p.c_f32) epilogue_chunk<float>(p, ti.z, m, n, v);
-          else epilogue_chunk<__nv_bfloat16>(p, ti.z, m, n, v);
-        }
-      }
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      float4* stg = stg_all + (warp - 2) * 256;
+      if (p.c_f32) epilogue_stripe<float>(p, ti.z, ti.m0 + q * 32, ti.n0, BN, taddr, stg, lane);
+      else epilogue_stripe<__nv_bfloat16>(p, ti.z, ti.m0 + q * 32, ti.n0, BN, taddr, stg, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -335,6 +398,162 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ----------------------------------------------------------------- CTA-pair kernel
+// cta_group::2 variant for large non-causal GEMMs: a cluster of 2 CTAs on one
+// TPC computes a 256 x 256 tile. Each CTA stages its own 128-row half of A and
+// 128-row half of B (TMA completion counted on the leader's barrier); the
+// leader's single thread issues tcgen05.mma.cta_group::2 (M = 256) reading
+// both CTAs' smem, so per SM the operand traffic per MAC halves relative to
+// the 128 x 256 single-CTA tile. Accumulators: 2 x 256 TMEM columns per CTA.
+constexpr int PAIR_BM = 256, PAIR_BN = 256, PAIR_STAGES = 6;
+constexpr int PAIR_HALF_BYTES = 128 * BK * 2;               // 16 KB
+constexpr int PAIR_STAGE_BYTES = 2 * PAIR_HALF_BYTES;       // A half + B half
+constexpr int PAIR_STG_BYTES = 4 * 32 * 128;
+constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + PAIR_STG_BYTES + 256 + 1024;
+constexpr uint32_t PAIR_TMEM_COLS = 512;
+
+template <int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                    const TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float4* stg_all = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + PAIR_STG_BYTES);
+  uint64_t* empty = full + PAIR_STAGES;
+  uint64_t* tfull = empty + PAIR_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int total_tiles = p.batch * p.tiles_m * p.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma_a);
+    tma_prefetch(&tma_b);
+    for (int s = 0; s < PAIR_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader's arrive.expect_tx; both CTAs' TMA bytes
+      mbar_init(&empty[s], 1);  // multicast commit from the leader's MMA
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, PAIR_TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int t, int& z, int& m0, int& n0) {
+    const int per_z = p.tiles_m * p.tiles_n;
+    z = t / per_z;
+    const int r = t - z * per_z;
+    const int mt = r / p.tiles_n;
+    m0 = mt * PAIR_BM;
+    n0 = (r - mt * p.tiles_n) * PAIR_BN;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total_tiles; t += npairs) {
+        int z, m0, n0;
+        decode(t, z, m0, n0);
+        const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
+        const int ax = p.a_x_off[0] * zo + p.a_x_off[1] * zi, ay = p.a_y_off[0] * zo + p.a_y_off[1] * zi;
+        const int bx = p.b_x_off[0] * zo + p.b_x_off[1] * zi, by = p.b_y_off[0] * zo + p.b_y_off[1] * zi;
+        const int am = m0 + static_cast<int>(rank) * 128, bn = n0 + static_cast<int>(rank) * 128;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PAIR_STAGE_BYTES);
+          uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
+          uint8_t* sb = sa + PAIR_HALF_BYTES;
+          const int k0 = kb * BK;
+          if (A_MN) {
+            tma_load_2d_pair(sa, &tma_a, &full[stage], ax + am, ay + k0);
+            tma_load_2d_pair(sa + 8192, &tma_a, &full[stage], ax + am + 64, ay + k0);
+          } else {
+            tma_load_2d_pair(sa, &tma_a, &full[stage], ax + k0, ay + am);
+          }
+          if (B_MN) {
+            tma_load_2d_pair(sb, &tma_b, &full[stage], bx + bn, by + k0);
+            tma_load_2d_pair(sb + 8192, &tma_b, &full[stage], bx + bn + 64, by + k0);
+          } else {
+            tma_load_2d_pair(sb, &tma_b, &full[stage], bx + k0, by + bn);
+          }
+          if (++stage == PAIR_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(PAIR_BM, PAIR_BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t smem_base = smem_u32(smem);
+      for (int t = pair; t < total_tiles; t += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * PAIR_BN);
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_base + stage * PAIR_STAGE_BYTES;
+          const uint32_t sb = sa + PAIR_HALF_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                        : umma_desc_sw128(sb + kk * 32, 16, 1024);
+            umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit_pair(&empty[stage], 0x3);
+          if (++stage == PAIR_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < total_tiles; t += npairs) {
+      int z, m0, n0;
+      decode(t, z, m0, n0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * PAIR_BN);
+      float4* stg = stg_all + (warp - 2) * 256;
+      const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
+      if (p.c_f32) epilogue_stripe<float>(p, z, mb, n0, PAIR_BN, taddr, stg, lane);
+      else epilogue_stripe<__nv_bfloat16>(p, z, mb, n0, PAIR_BN, taddr, stg, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, PAIR_TMEM_COLS);
   }
 }
 
@@ -389,6 +608,28 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcPara
   return cudaGetLastError();
 }
 
+template <int A_MN, int B_MN>
+cudaError_t launch_tc2(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p, int grid,
+                       cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PAIR_SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gemm_tc2_kernel<A_MN, B_MN><<<grid, 192, PAIR_SMEM, stream>>>(ma, mb, p);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_pair(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
+                          int grid, cudaStream_t s) {
+  if (!a_mn && !b_mn) return launch_tc2<0, 0>(ma, mb, p, grid, s);
+  if (!a_mn && b_mn) return launch_tc2<0, 1>(ma, mb, p, grid, s);
+  if (a_mn && !b_mn) return launch_tc2<1, 0>(ma, mb, p, grid, s);
+  return launch_tc2<1, 1>(ma, mb, p, grid, s);
+}
+
 template <int BN>
 cudaError_t dispatch_major(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
                            int grid, cudaStream_t s) {
@@ -396,6 +637,16 @@ cudaError_t dispatch_major(int a_mn, int b_mn, const CUtensorMap& ma, const CUte
   if (!a_mn && b_mn) return launch_tc<BN, 0, 1>(ma, mb, p, grid, s);
   if (a_mn && !b_mn) return launch_tc<BN, 1, 0>(ma, mb, p, grid, s);
   return launch_tc<BN, 1, 1>(ma, mb, p, grid, s);
+}
+
+// OASES_GEMM_PAIR=0 forces the single-CTA kernel (A/B comparisons).
+bool use_pairs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("OASES_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int sm_count() {
@@ -443,9 +694,12 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
     st.err = "gemm_tc: causal K-range modes need M == K";
     return st;
   }
+  // CTA pairs (256 x 256 tiles) for the large non-causal GEMMs; causal K
+  // ranges are defined at 128-row granularity, so attention stays single-CTA.
+  const bool pair = use_pairs() && d.causal == OASES_CAUSAL_NONE && d.M > BM && d.N > 128;
   CUtensorMap ma, mb;
   if (!make_map(&ma, d.a, 64, d.a.mn_major ? 64 : BM, &st.err)) return st;
-  if (!make_map(&mb, d.b, 64, d.b.mn_major ? 64 : BN, &st.err)) return st;
+  if (!make_map(&mb, d.b, 64, d.b.mn_major ? 64 : (pair ? 128 : BN), &st.err)) return st;
 
   TcParams p{};
   p.M = static_cast<int>(d.M);
@@ -453,8 +707,9 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
   p.K = static_cast<int>(d.K);
   p.batch = static_cast<int>(d.batch);
   p.batch_inner = static_cast<int>(d.batch_inner);
-  p.tiles_m = static_cast<int>((d.M + BM - 1) / BM);
-  p.tiles_n = static_cast<int>((d.N + BN - 1) / BN);
+  const int tm = pair ? PAIR_BM : BM, tn = pair ? PAIR_BN : BN;
+  p.tiles_m = static_cast<int>((d.M + tm - 1) / tm);
+  p.tiles_n = static_cast<int>((d.N + tn - 1) / tn);
   p.kblocks = static_cast<int>((d.K + BK - 1) / BK);
   for (int i = 0; i < 2; ++i) {
     p.a_x_off[i] = static_cast<int>(d.a.col_off[i]);
@@ -477,9 +732,17 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
   const long long tiles = static_cast<long long>(p.batch) * p.tiles_m * p.tiles_n;
   int grid = sm_count();
   if (d.max_ctas > 0 && d.max_ctas < grid) grid = d.max_ctas;
-  if (tiles < grid) grid = static_cast<int>(tiles);
-  cudaError_t e = BN == 128 ? dispatch_major<128>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream)
-                            : dispatch_major<256>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream);
+  cudaError_t e;
+  if (pair) {
+    int pairs = grid / 2;
+    if (pairs < 1) pairs = 1;
+    if (tiles < pairs) pairs = static_cast<int>(tiles);
+    e = dispatch_pair(d.a.mn_major, d.b.mn_major, ma, mb, p, 2 * pairs, stream);
+  } else {
+    if (tiles < grid) grid = static_cast<int>(tiles);
+    e = BN == 128 ? dispatch_major<128>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream)
+                  : dispatch_major<256>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream);
+  }
   if (e != cudaSuccess) {
     st.err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
     st.cuda = true;
