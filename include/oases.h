@@ -184,6 +184,8 @@ typedef struct {
   const void* unique_id;  /* NCCL id bytes (required when tp > 1 and local_workers == 1) */
   int32_t nccl_max_ctas;  /* 0 = NCCL default */
   int32_t gemm_max_ctas;  /* persistent GEMM grid cap while comm may overlap (0 = all SMs) */
+  int32_t comm_disabled;  /* 1: one rank's shard of a tp-way group, AllReduces skipped (calibration
+                             of per-degree compute costs on a single device) */
 } oases_ctx_desc;
 
 oases_status oases_ctx_create(const oases_ctx_desc* desc, oases_ctx** out);

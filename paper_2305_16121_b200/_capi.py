@@ -73,6 +73,7 @@ class CtxDesc(C.Structure):
         ("unique_id", C.c_void_p),
         ("nccl_max_ctas", C.c_int32),
         ("gemm_max_ctas", C.c_int32),
+        ("comm_disabled", C.c_int32),
     ]
 
 

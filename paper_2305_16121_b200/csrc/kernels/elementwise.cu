@@ -283,9 +283,12 @@ bool vec_ok(const void* a, const void* b, long long n, int cols) {
 
 size_t colsum_workspace(long long rows, int cols) {
   // upper bound over both the vector (V columns per thread) and scalar layouts
-  const ColSplit s = col_split(rows, (cols + kThreads - 1) / kThreads);
-  const ColSplit v = col_split(rows, (cols + kThreads * 4 - 1) / (kThreads * 4));
-  return static_cast<size_t>(s.chunks > v.chunks ? s.chunks : v.chunks) * cols * sizeof(float) + 256;
+  int chunks = 1;
+  for (int v : {1, 4, 8}) {  // scalar, f32 and bf16 vector layouts
+    const ColSplit s = col_split(rows, (cols + kThreads * v - 1) / (kThreads * v));
+    if (s.chunks > chunks) chunks = s.chunks;
+  }
+  return static_cast<size_t>(chunks) * cols * sizeof(float) + 256;
 }
 
 cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias, const void* res, void* out,

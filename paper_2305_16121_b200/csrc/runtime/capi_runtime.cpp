@@ -10,9 +10,19 @@
 #include "stack.h"
 #include "status.h"
 
+// Contexts are reference counted: every stack holds one reference, so the
+// destruction order chosen by a garbage collector cannot free the streams or
+// the NCCL communicator under a live stack.
 struct oases_ctx {
   std::unique_ptr<oases::Context> ctx;
+  int refs = 1;
 };
+
+namespace {
+void ctx_release(oases_ctx* c) {
+  if (c && --c->refs == 0) delete c;
+}
+}  // namespace
 
 struct oases_stack {
   oases_ctx* owner = nullptr;
@@ -102,15 +112,16 @@ oases_status oases_ctx_create(const oases_ctx_desc* desc, oases_ctx** out) {
 }
 
 oases_status oases_ctx_destroy(oases_ctx* ctx) {
-  return guarded([&] { delete ctx; });
+  return guarded([&] { ctx_release(ctx); });
 }
 
 oases_status oases_stack_create(oases_ctx* ctx, const oases_model_desc* model, oases_stack** out) {
   return guarded([&] {
     if (!ctx || !ctx->ctx || !model || !out) throw ConfigError("null argument");
     auto h = std::make_unique<oases_stack>();
-    h->owner = ctx;
     h->stack = std::make_unique<oases::Stack>(*ctx->ctx, to_cfg(*model));
+    h->owner = ctx;
+    ++ctx->refs;
     *out = h.release();
   });
 }
@@ -121,6 +132,7 @@ oases_status oases_stack_destroy(oases_stack* s) {
       if (s->stack) cudaStreamSynchronize(s->stack->ctx().compute);
       s->exec.reset();
       s->stack.reset();
+      ctx_release(s->owner);
       delete s;
     }
   });

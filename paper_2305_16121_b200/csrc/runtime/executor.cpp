@@ -195,7 +195,7 @@ tmpsim::SimResult Executor::step(bool trace) {
       r.trace.push_back({i, stream ? tmpsim::Stream::Comm : tmpsim::Stream::Compute, s0, s1});
       if (stream) {
         // tp == 1 AllReduces are empty: they contribute no interval
-        if (stack_.ctx().tp > 1) comm.emplace_back(s0, s1);
+        if (stack_.ctx().tp > 1 && !stack_.ctx().comm_disabled) comm.emplace_back(s0, s1);
       } else {
         comp.emplace_back(s0, s1);
         busy += s1 - s0;

@@ -48,7 +48,7 @@ std::unique_ptr<Context> make_context(const oases_ctx_desc& d) {
   if (d.local_workers != 1 && d.local_workers != d.tp)
     throw ConfigError("ctx: local_workers must be 1 (one rank per process) or equal tp (in-process emulation)");
   if (d.local_workers > 8) throw ConfigError("ctx: at most 8 in-process workers");
-  if (d.tp > 1 && d.local_workers == 1 && !d.unique_id)
+  if (d.tp > 1 && d.local_workers == 1 && !d.unique_id && !d.comm_disabled)
     throw ConfigError("ctx: tp > 1 with one rank per process needs the NCCL unique id");
   if (d.rank < 0 || (d.local_workers == 1 && d.rank >= d.tp)) throw ConfigError("ctx: rank out of range");
   int ndev = 0;
@@ -70,7 +70,8 @@ std::unique_ptr<Context> make_context(const oases_ctx_desc& d) {
   // The comm stream gets the highest priority so NCCL's CTAs are scheduled as
   // soon as the overlapped GEMM frees SMs.
   check_cuda(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi), "comm stream");
-  if (d.tp > 1 && d.local_workers == 1) {
+  ctx->comm_disabled = d.comm_disabled != 0;
+  if (d.tp > 1 && d.local_workers == 1 && !ctx->comm_disabled) {
     ncclUniqueId id;
     static_assert(sizeof(ncclUniqueId) == OASES_UNIQUE_ID_BYTES, "unique id size");
     std::memcpy(&id, d.unique_id, sizeof(id));
@@ -776,7 +777,7 @@ void Stack::tail(int wi, int sb) {
 }
 
 void Stack::allreduce(tmpsim::Pass pass, int block, int sb, bool both) {
-  if (ctx_.tp == 1) return;
+  if (ctx_.tp == 1 || ctx_.comm_disabled) return;
   const int par = block % 2;
   auto pick = [&](Worker& w) -> void* {
     auto& arr = pass == tmpsim::Pass::Forward ? w.fwd_ar[par] : pass == tmpsim::Pass::Recompute ? w.rec_ar[par] : w.bwd_ar[par];

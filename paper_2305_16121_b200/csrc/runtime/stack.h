@@ -25,6 +25,7 @@ struct Context {
   int local_workers = 1;  // >1: all TMP ranks emulated in-process on `device`
   int gemm_max_ctas = 0;
   int nccl_max_ctas = 0;
+  bool comm_disabled = false;  // calibration: one rank's shard, no collectives
   cudaStream_t compute = nullptr;
   cudaStream_t comm = nullptr;
   ncclComm_t nccl = nullptr;

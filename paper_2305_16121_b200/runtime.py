@@ -117,10 +117,10 @@ def unique_id() -> bytes:
 
 class Context:
     def __init__(self, tp=1, rank=0, device=0, local_workers=1, unique_id: bytes | None = None, nccl_max_ctas=0,
-                 gemm_max_ctas=0):
+                 gemm_max_ctas=0, comm_disabled=False):
         self._uid = (C.c_char * 128).from_buffer_copy(unique_id) if unique_id else None
         d = capi.CtxDesc(tp, rank, device, local_workers, C.cast(self._uid, C.c_void_p) if self._uid else None,
-                         nccl_max_ctas, gemm_max_ctas)
+                         nccl_max_ctas, gemm_max_ctas, int(comm_disabled))
         self._h = C.c_void_p()
         check(capi.lib().oases_ctx_create(C.byref(d), C.byref(self._h)))
         self.tp, self.rank, self.local_workers = tp, rank, local_workers
