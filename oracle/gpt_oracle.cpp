@@ -220,8 +220,8 @@ struct Oracle {
     const int s = cfg.seq, d = dh, H = cfg.heads;
     const double scale = 1.0 / std::sqrt(static_cast<double>(d));
     const float p = cfg.attention_dropout;
-    const uint32_t thr = oracle::keep_threshold(static_cast<double>(p));
-    const double ks = p > 0.f ? 1.0 / (1.0 - static_cast<double>(p)) : 1.0;
+    const uint32_t thr = oracle::keep_threshold(p);
+    const double ks = oracle::keep_scale(p);
     ctx = Mat(T, Ht * d);
     P = Mat(cfg.batch * Ht * s, s);
     Pd = Mat(cfg.batch * Ht * s, s);
@@ -268,8 +268,8 @@ struct Oracle {
     const int s = cfg.seq, d = dh;
     const double scale = 1.0 / std::sqrt(static_cast<double>(d));
     const float p = cfg.attention_dropout;
-    const uint32_t thr = oracle::keep_threshold(static_cast<double>(p));
-    const double ks = p > 0.f ? 1.0 / (1.0 - static_cast<double>(p)) : 1.0;
+    const uint32_t thr = oracle::keep_threshold(p);
+    const double ks = oracle::keep_scale(p);
     const int H = cfg.heads;
     (void)H;
     dqkv = Mat(T, 3 * Ht * d);
@@ -320,8 +320,8 @@ struct Oracle {
   void bdr_fwd(int block, const Mat& in, const Mat* bias, const Mat* res, Mat& out) const {
     const int h = cfg.hidden, s = cfg.seq;
     const float p = cfg.hidden_dropout;
-    const uint32_t thr = oracle::keep_threshold(static_cast<double>(p));
-    const double ks = p > 0.f ? 1.0 / (1.0 - static_cast<double>(p)) : 1.0;
+    const uint32_t thr = oracle::keep_threshold(p);
+    const double ks = oracle::keep_scale(p);
     out = Mat(T, h);
     for (int r = 0; r < T; ++r) {
       const int n = r / s, sb = n / half();
@@ -339,8 +339,8 @@ struct Oracle {
     const float p = cfg.hidden_dropout;
     out = g;
     if (!(p > 0.f)) return;
-    const uint32_t thr = oracle::keep_threshold(static_cast<double>(p));
-    const double ks = 1.0 / (1.0 - static_cast<double>(p));
+    const uint32_t thr = oracle::keep_threshold(p);
+    const double ks = oracle::keep_scale(p);
     for (int r = 0; r < T; ++r) {
       const int n = r / s, sb = n / half();
       const uint64_t rl = static_cast<uint64_t>(r - sb * half() * s);

@@ -182,11 +182,23 @@ def philox4x32_10(seed: int, offset: int, ctr: np.ndarray) -> np.ndarray:
     return np.stack([c0, c1, c2, c3], axis=-1).astype(np.uint32)
 
 
+def keep_threshold(p: float) -> int:
+    """thr8 = round(p * 256) in float32 arithmetic, clamped to [1, 255] (0 when p <= 0)."""
+    if not p > 0:
+        return 0
+    t = int(np.float32(p) * np.float32(256.0) + np.float32(0.5))
+    return min(255, max(1, t))
+
+
+def keep_scale(p: float) -> float:
+    t = keep_threshold(p)
+    return 256.0 / (256.0 - t) if t else 1.0
+
+
 def keep_mask(seed: int, offset: int, n: int, p: float) -> np.ndarray:
-    """Keep-mask of elements 0..n-1 under (seed, offset) for dropout probability p (float32 semantics)."""
-    thr = float(np.float32(p)) * 4294967296.0
-    thr = 0xFFFFFFFF if thr >= 4294967295.0 else int(thr)
-    e = np.arange(n, dtype=np.uint64)
-    words = philox4x32_10(seed, offset, e >> np.uint64(2))
-    u = words[np.arange(n), (e & np.uint64(3)).astype(np.int64)]
-    return u >= np.uint32(thr)
+    """Keep-mask of elements 0..n-1 under (seed, offset): byte (e & 15) of Philox(e >> 4) >= thr8."""
+    thr = keep_threshold(p)
+    ctrs = (n + 15) // 16
+    words = philox4x32_10(seed, offset, np.arange(ctrs, dtype=np.uint64))  # [ctrs, 4]
+    byts = words.astype("<u4").view(np.uint8).reshape(ctrs * 16)  # byte b of word w at 4w + b (little endian)
+    return byts[:n] >= np.uint8(thr)

@@ -1,7 +1,8 @@
 // TEST INFRASTRUCTURE (oracle). Philox4x32-10 exactly as specified for the
 // dropout masks of the B200 build: element e of a
-// tensor under key (seed, offset) is kept iff word (e & 3) of
-// Philox(counter = e >> 2 | offset << 64, key = seed) >= p * 2^32.
+// tensor under key (seed, offset) is kept iff byte (e & 15) of the 16 output
+// bytes of Philox(counter = e >> 4 | offset << 64, key = seed) is >= thr8,
+// thr8 = round(p * 256) clamped to [1, 255]; kept values scale by 256/(256-thr8).
 #pragma once
 #include <cstdint>
 
@@ -24,15 +25,22 @@ inline void philox4x32_10(uint64_t seed, uint64_t offset, uint64_t ctr, uint32_t
   for (int i = 0; i < 4; ++i) out[i] = c[i];
 }
 
-inline uint32_t keep_threshold(double p) {
-  const double t = p * 4294967296.0;
-  return t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+inline uint32_t keep_threshold(float p) {
+  if (!(p > 0.f)) return 0u;
+  int t = static_cast<int>(p * 256.f + 0.5f);
+  return static_cast<uint32_t>(t < 1 ? 1 : (t > 255 ? 255 : t));
+}
+
+inline double keep_scale(float p) {
+  const uint32_t t = keep_threshold(p);
+  return t ? 256.0 / (256.0 - t) : 1.0;
 }
 
 inline bool keep(uint64_t seed, uint64_t offset, uint64_t e, uint32_t thr) {
   uint32_t u[4];
-  philox4x32_10(seed, offset, e >> 2, u);
-  return u[e & 3] >= thr;
+  philox4x32_10(seed, offset, e >> 4, u);
+  const unsigned b = static_cast<unsigned>(e & 15);
+  return ((u[b >> 2] >> (8 * (b & 3))) & 0xFFu) >= thr;
 }
 
 }  // namespace oracle

@@ -127,10 +127,38 @@ struct Philox {
     out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
   }
 };
-// keep element if u32 >= p * 2^32
+// Dropout masks use one byte of Philox output per element (16 elements per
+// Philox call, as FlashAttention does): element e keeps iff byte (e & 15) of
+// Philox(ctr = e >> 4) >= thr8, thr8 = round(p * 256). The effective drop
+// probability is thr8 / 256 and kept values are scaled by 256 / (256 - thr8),
+// so the expectation is preserved exactly.
 __host__ __device__ inline uint32_t dropout_threshold(float p) {
-  const double t = static_cast<double>(p) * 4294967296.0;
-  return t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+  if (!(p > 0.f)) return 0u;
+  int t = static_cast<int>(p * 256.f + 0.5f);
+  return static_cast<uint32_t>(t < 1 ? 1 : (t > 255 ? 255 : t));
+}
+__host__ __device__ inline float dropout_keep_scale(float p) {
+  const uint32_t t = dropout_threshold(p);
+  return t ? 256.f / static_cast<float>(256u - t) : 1.f;
+}
+__device__ __forceinline__ bool keep_byte(const uint32_t (&u)[4], unsigned b, uint32_t thr) {
+  return ((u[b >> 2] >> (8 * (b & 3))) & 0xFFu) >= thr;
+}
+// Applies the keep-mask of elements [e, e+V) to v; requires e % V == 0, V in {4, 8}.
+template <int V>
+__device__ __forceinline__ void apply_dropout(float (&v)[V], unsigned long long e, uint64_t seed, uint64_t offset,
+                                              uint32_t thr, float ks) {
+  uint32_t u[4];
+  Philox::gen(seed, offset, e >> 4, u);
+  const unsigned b0 = static_cast<unsigned>(e & 15);
+#pragma unroll
+  for (int q = 0; q < V; ++q) v[q] = keep_byte(u, b0 + q, thr) ? v[q] * ks : 0.f;
+}
+__device__ __forceinline__ float dropout_one(float v, unsigned long long e, uint64_t seed, uint64_t offset,
+                                             uint32_t thr, float ks) {
+  uint32_t u[4];
+  Philox::gen(seed, offset, e >> 4, u);
+  return keep_byte(u, static_cast<unsigned>(e & 15), thr) ? v * ks : 0.f;
 }
 
 // ---------------------------------------------------------------- mbarrier

@@ -3,7 +3,7 @@
 // in-process AllReduce used to emulate TMP ranks on one device, and fills.
 //
 // All bulk paths move 16-byte vectors (8 bf16 / 4 f32) per thread; dropout
-// masks come from Philox (one call per 4 consecutive elements), so forward,
+// masks come from Philox (one byte per element, 16 elements per call), so forward,
 // recompute and backward regenerate them bit-exactly. Column reductions are
 // two-stage with a fixed summation order (deterministic, no float atomics).
 #include "common.cuh"
@@ -19,19 +19,6 @@ unsigned grid_for(long long work_items, int per_block) {
   const long long cap = 148LL * 16;
   if (g > cap) g = cap;
   return static_cast<unsigned>(g < 1 ? 1 : g);
-}
-
-// Applies the keep-mask of elements [e, e+V) (e % 4 == 0) to v.
-template <int V>
-__device__ __forceinline__ void apply_dropout(float (&v)[V], unsigned long long e, uint64_t seed, uint64_t offset,
-                                              uint32_t thr, float ks) {
-#pragma unroll
-  for (int q = 0; q < V; q += 4) {
-    uint32_t u[4];
-    Philox::gen(seed, offset, (e + q) >> 2, u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v[q + j] = (u[j] >= thr) ? v[q + j] * ks : 0.f;
-  }
 }
 
 // ---------------------------------------------------------------- bias-dropout-residual
@@ -71,15 +58,13 @@ __global__ void __launch_bounds__(kThreads) bdr_fwd_kernel(const T* __restrict__
                                                            uint64_t offset) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * 4;
   for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
-    uint32_t u[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (drop) Philox::gen(seed, offset, static_cast<unsigned long long>(i) >> 2, u);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const long long e = i + q;
       if (e >= n) break;
       float v = to_f(x[e]);
       if (bias) v += to_f(bias[e % cols]);
-      if (drop) v = (u[q] >= thr) ? v * ks : 0.f;
+      if (drop) v = dropout_one(v, static_cast<unsigned long long>(e), seed, offset, thr, ks);
       if (res) v += to_f(res[e]);
       out[e] = from_f<T>(v);
     }
@@ -130,11 +115,7 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(const T* __restrict_
   for (long long r = r0; r < r1; ++r) {
     const long long e = r * cols + c;
     float v = to_f(in[e]);
-    if (drop) {
-      uint32_t u[4];
-      Philox::gen(seed, offset, static_cast<unsigned long long>(e) >> 2, u);
-      v = (u[e & 3] >= thr) ? v * ks : 0.f;
-    }
+    if (drop) v = dropout_one(v, static_cast<unsigned long long>(e), seed, offset, thr, ks);
     if (dx) dx[e] = from_f<T>(v);
     s += v;
   }
@@ -297,7 +278,7 @@ cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias
   const long long n = rows * cols;
   const int drop = p > 0.f;
   const uint32_t thr = dropout_threshold(p);
-  const float ks = drop ? 1.f / (1.f - p) : 1.f;
+  const float ks = dropout_keep_scale(p);
   if (dtype == OASES_BF16) {
     using T = __nv_bfloat16;
     auto X = static_cast<const T*>(x);
@@ -352,7 +333,7 @@ cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, v
   float* part = out ? static_cast<float*>(ws) : nullptr;
   const int drop = p > 0.f;
   const uint32_t thr = dropout_threshold(p);
-  const float ks = drop ? 1.f / (1.f - p) : 1.f;
+  const float ks = dropout_keep_scale(p);
   int chunks = 0;
   if (dtype == OASES_BF16)
     col_pass_t<__nv_bfloat16>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);

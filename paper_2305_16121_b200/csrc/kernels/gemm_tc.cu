@@ -9,13 +9,22 @@
 // (numerics.cpp:26-32) are expressed as operand major-ness in the TMA box and
 // the UMMA smem descriptor, never as a kernel.
 //
-// Roles (192 threads, 1 CTA per SM, grid = min(tiles, SMs)):
-//   warp 0      TMA producer  (one elected lane): gmem -> smem ring, mbarrier tx
-//   warp 1      MMA issuer    (one elected lane): tcgen05.mma into a double-buffered
-//               TMEM accumulator; also owns TMEM alloc/dealloc
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> regs, fused bias/GeLU/dGeLU/accumulate,
-//               vectorised global stores
-// Tile 128 x BN x 64, BN in {128, 256}, SWIZZLE_128B operand tiles.
+// Two kernels share the pipeline structure (320 threads, 1 CTA per SM,
+// persistent over a static tile schedule):
+//   warp 0      TMA producer (one lane): gmem -> SWIZZLE_128B smem ring, mbarrier tx
+//   warp 1      MMA issuer (one lane): tcgen05.mma into a double-buffered TMEM
+//               accumulator; also owns TMEM alloc/dealloc
+//   warps 2..9  epilogue: two warps per TMEM lane quarter, each owning half of
+//               the tile's columns: tcgen05.ld -> registers -> swizzled smem ->
+//               row-contiguous 16-byte segments -> fused bias / erf-GeLU /
+//               dGeLU / f32-accumulate -> global. The epilogue is specialised at
+//               compile time (output type x epilogue x accumulate) so its inner
+//               loop is branch-free pointer arithmetic.
+// * gemm_tc_kernel<BN,...>: one CTA computes 128 x BN (BN = 128 | 256); used for
+//   the causal attention GEMMs and small problems.
+// * gemm_tc2_kernel: a 2-CTA cluster (cta_group::2) computes 256 x 256; each CTA
+//   stages half of A and half of B, the leader issues M=256 MMAs reading both
+//   CTAs' smem (half the operand traffic per MAC of the single-CTA tile).
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -30,6 +39,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int STG_FLOAT4 = EPI_WARPS * 256;  // 4 KB staging per epilogue warp (static smem)
 
 template <int BN>
 struct TcCfg {
@@ -38,9 +50,8 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int STG_BYTES = 4 * 32 * 128;  // epilogue staging, 4 KB per epilogue warp
-  static constexpr int SMEM = STAGES * STAGE_BYTES + STG_BYTES + BAR_BYTES + 1024;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
+  static constexpr int SMEM = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + 32 KB static staging
+  static constexpr uint32_t TMEM_COLS = 2 * BN;                       // two accumulator buffers
 };
 
 struct TcParams {
@@ -88,162 +99,76 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, int t, TileInfo& 
 }
 
 // ----------------------------------------------------------------- epilogue
-template <typename OutT>
-__device__ __forceinline__ void store32(OutT* dst, const float (&v)[32], int valid);
-
-template <>
-__device__ __forceinline__ void store32<float>(float* dst, const float (&v)[32], int valid) {
-  if (valid >= 32) {
+// E elements (E = 8 bf16 / 4 f32, one 16-byte vector) of one output row.
+template <typename OutT, int E>
+__device__ __forceinline__ void ld_vec(const OutT* p, float (&v)[E]) {
+  if constexpr (sizeof(OutT) == 2) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
     }
   } else {
-    for (int i = 0; i < valid; ++i) dst[i] = v[i];
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
   }
 }
-template <>
-__device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[32], int valid) {
-  if (valid >= 32) {
+template <typename OutT, int E>
+__device__ __forceinline__ void st_vec(OutT* p, const float (&v)[E]) {
+  if constexpr (sizeof(OutT) == 2) {
+    uint32_t w[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint4 u;
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
-      __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
-      __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
-      u.x = *reinterpret_cast<uint32_t*>(&h0);
-      u.y = *reinterpret_cast<uint32_t*>(&h1);
-      u.z = *reinterpret_cast<uint32_t*>(&h2);
-      u.w = *reinterpret_cast<uint32_t*>(&h3);
-      reinterpret_cast<uint4*>(dst)[i] = u;
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      w[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+// E bias values starting at column n (bias is bf16 in the tensor-core path).
+template <int E>
+__device__ __forceinline__ void ld_bias(const __nv_bfloat16* b, int n, int valid, float (&v)[E]) {
+  if (valid >= E && (E % 8 == 0)) {
+    const uint4 u = *reinterpret_cast<const uint4*>(b + n);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < E / 2; ++j) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
     }
   } else {
-    for (int i = 0; i < valid; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = i < valid ? __bfloat162float(b[n + i]) : 0.f;
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void load32(const T* src, float (&v)[32], int valid);
-template <>
-__device__ __forceinline__ void load32<float>(const float* src, float (&v)[32], int valid) {
-  if (valid >= 32) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float4 f = reinterpret_cast<const float4*>(src)[i];
-      v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
-    }
-  } else {
-    for (int i = 0; i < 32; ++i) v[i] = i < valid ? src[i] : 0.f;
-  }
-}
-template <>
-__device__ __forceinline__ void load32<__nv_bfloat16>(const __nv_bfloat16* src, float (&v)[32], int valid) {
-  if (valid >= 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 u = reinterpret_cast<const uint4*>(src)[i];
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
-        const float2 f = __bfloat1622float2(h);
-        v[8 * i + 2 * j] = f.x;
-        v[8 * i + 2 * j + 1] = f.y;
-      }
-    }
-  } else {
-    for (int i = 0; i < 32; ++i) v[i] = i < valid ? __bfloat162float(src[i]) : 0.f;
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void load4(const T* src, float (&v)[4]);
-template <>
-__device__ __forceinline__ void load4<float>(const float* src, float (&v)[4]) {
-  const float4 f = *reinterpret_cast<const float4*>(src);
-  v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-}
-template <>
-__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* src, float (&v)[4]) {
-  const uint2 u = *reinterpret_cast<const uint2*>(src);
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-}
-template <typename T>
-__device__ __forceinline__ void store4(T* dst, const float (&v)[4]);
-template <>
-__device__ __forceinline__ void store4<float>(float* dst, const float (&v)[4]) {
-  *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-}
-template <>
-__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[4]) {
-  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-  uint2 u;
-  u.x = *reinterpret_cast<uint32_t*>(&a);
-  u.y = *reinterpret_cast<uint32_t*>(&b);
-  *reinterpret_cast<uint2*>(dst) = u;
-}
-
-// Fused epilogue math for 4 consecutive output columns of one row (global
-// offsets already resolved): alpha, bias, dGeLU(aux), accumulate, store, GeLU.
-template <typename OutT>
-__device__ __forceinline__ void epilogue4(const TcParams& p, long long off, int n, const float4 a) {
-  float v[4] = {a.x * p.alpha, a.y * p.alpha, a.z * p.alpha, a.w * p.alpha};
-  const int valid = p.N - n < 4 ? p.N - n : 4;
-  OutT* c = reinterpret_cast<OutT*>(p.c) + off;
-  if (valid == 4) {
-    if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias) {
-      const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p.bias) + n);
-      const float2 b0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-      const float2 b1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-      v[0] += b0.x; v[1] += b0.y; v[2] += b1.x; v[3] += b1.y;
-    }
-    if (p.epilogue == OASES_EPI_DGELU) {
-      float x[4];
-      load4<OutT>(reinterpret_cast<const OutT*>(p.aux) + off, x);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] *= gelu_grad_f(x[i]);
-    }
-    if (p.accumulate) {
-      float o[4];
-      load4<OutT>(c, o);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] += o[i];
-    }
-    store4<OutT>(c, v);
-    if (p.epilogue == OASES_EPI_BIAS_GELU) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = gelu_f(v[i]);
-      store4<OutT>(reinterpret_cast<OutT*>(p.c2) + off, v);
-    }
-    return;
-  }
-  for (int i = 0; i < valid; ++i) {
-    float x = v[i];
-    if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias)
-      x += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n + i]);
-    if (p.epilogue == OASES_EPI_DGELU) x *= gelu_grad_f(to_f(reinterpret_cast<const OutT*>(p.aux)[off + i]));
-    if (p.accumulate) x += to_f(c[i]);
-    c[i] = from_f<OutT>(x);
-    if (p.epilogue == OASES_EPI_BIAS_GELU) reinterpret_cast<OutT*>(p.c2)[off + i] = from_f<OutT>(gelu_f(x));
-  }
-}
-
-// One warp's 32-row stripe of an accumulator tile. TMEM -> registers (thread =
-// row) -> 128B-swizzled smem staging -> read back as 4-wide row segments so
-// every global access of the warp covers 4 contiguous rows (8 lanes per row)
-// instead of 32 scattered rows -> fused epilogue -> global.
-template <typename OutT>
-__device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_base, int n0, int ncols,
+// One warp's 32-row x ncols stripe of an accumulator tile (ncols % 32 == 0).
+// TMEM -> registers (thread = row) -> 128B-swizzled smem staging -> each lane
+// takes one 16-byte column group of a row, so a warp's global access covers
+// 32/LPR full row segments -> fused epilogue -> global.
+template <typename OutT, int EPI, bool ACC>
+__device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_base, int nbeg, int ncols,
                                                 uint32_t taddr, float4* stg, int lane) {
+  constexpr int E = 16 / sizeof(OutT);  // elements per lane per row
+  constexpr int LPR = 32 / E;           // lanes per row (4 | 8)
+  constexpr int RPI = 32 / LPR;         // rows per iteration (8 | 4)
+  constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU;
   const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
-  const long long row0 = p.c_row_off[0] * zo + p.c_row_off[1] * zi;
+  const long long row0 = p.c_row_off[0] * zo + p.c_row_off[1] * zi + m_base;
   const long long col0 = p.c_col_off[0] * zo + p.c_col_off[1] * zi;
+  const int lr = lane / LPR, lc = lane % LPR;
+  const int rows_left = p.M - m_base;  // rows of this stripe inside the problem
+  const long long step = static_cast<long long>(RPI) * p.ldc;
+  const bool scale = p.alpha != 1.f;
 #pragma unroll 1
   for (int c = 0; c < ncols / 32; ++c) {
-    const int nc = n0 + c * 32;
+    const int nc = nbeg + c * 32;
     uint32_t r[32];
     tmem_ld32(taddr + static_cast<uint32_t>(c * 32), r);
     tmem_wait_ld();
@@ -253,27 +178,130 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
       stg[lane * 8 + (j ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                                      __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
     __syncwarp();
+    const int n = nc + lc * E;
+    const int valid = p.N - n;  // elements of this lane's group inside the problem
+    if (valid > 0) {
+      float b[E];
+      if constexpr (BIAS) {
+        if (p.bias) ld_bias<E>(reinterpret_cast<const __nv_bfloat16*>(p.bias), n, valid, b);
+        else
+#pragma unroll
+          for (int i = 0; i < E; ++i) b[i] = 0.f;
+      }
+      OutT* cp = reinterpret_cast<OutT*>(p.c) + (row0 + lr) * p.ldc + col0 + n;
 #pragma unroll 2
-    for (int it = 0; it < 8; ++it) {
-      const int row = it * 4 + (lane >> 3), ch = lane & 7;
-      const float4 a = stg[row * 8 + (ch ^ (row & 7))];
-      const int m = m_base + row, n = nc + ch * 4;
-      if (m < p.M && n < p.N) epilogue4<OutT>(p, (row0 + m) * p.ldc + col0 + n, n, a);
+      for (int it = 0; it < 32 / RPI; ++it, cp += step) {
+        const int row = it * RPI + lr;
+        if (row >= rows_left) break;
+        float v[E];
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q) {
+          const int ch = lc * (E / 4) + q;
+          const float4 a = stg[row * 8 + (ch ^ (row & 7))];
+          v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+        }
+        if (scale)
+#pragma unroll
+          for (int i = 0; i < E; ++i) v[i] *= p.alpha;
+        if constexpr (BIAS)
+#pragma unroll
+          for (int i = 0; i < E; ++i) v[i] += b[i];
+        const long long rel = cp - reinterpret_cast<OutT*>(p.c);
+        if (valid >= E) {
+          if constexpr (EPI == OASES_EPI_DGELU) {
+            float x[E];
+            ld_vec<OutT, E>(reinterpret_cast<const OutT*>(p.aux) + rel, x);
+#pragma unroll
+            for (int i = 0; i < E; ++i) v[i] *= gelu_grad_f(x[i]);
+          }
+          if constexpr (ACC) {
+            float o[E];
+            ld_vec<OutT, E>(cp, o);
+#pragma unroll
+            for (int i = 0; i < E; ++i) v[i] += o[i];
+          }
+          st_vec<OutT, E>(cp, v);
+          if constexpr (EPI == OASES_EPI_BIAS_GELU) {
+#pragma unroll
+            for (int i = 0; i < E; ++i) v[i] = gelu_f(v[i]);
+            st_vec<OutT, E>(reinterpret_cast<OutT*>(p.c2) + rel, v);
+          }
+        } else {
+          for (int i = 0; i < valid; ++i) {
+            float x = v[i];
+            if constexpr (EPI == OASES_EPI_DGELU)
+              x *= gelu_grad_f(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
+            if constexpr (ACC) x += to_f(cp[i]);
+            cp[i] = from_f<OutT>(x);
+            if constexpr (EPI == OASES_EPI_BIAS_GELU)
+              reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_f(x));
+          }
+        }
+      }
     }
     __syncwarp();
   }
 }
 
-// ----------------------------------------------------------------- kernel
+// Calls BODY(OutT, EPI, ACC) for the runtime mode of p (compile-time specialised).
+#define OASES_EPI_DISPATCH(p, BODY)                                                      \
+  do {                                                                                   \
+    const int mode_ = ((p).c_f32 ? 8 : 0) + (p).epilogue * 2 + ((p).accumulate ? 1 : 0); \
+    switch (mode_) {                                                                     \
+      case 0: BODY(__nv_bfloat16, 0, false); break;                                      \
+      case 1: BODY(__nv_bfloat16, 0, true); break;                                       \
+      case 2: BODY(__nv_bfloat16, 1, false); break;                                      \
+      case 3: BODY(__nv_bfloat16, 1, true); break;                                       \
+      case 4: BODY(__nv_bfloat16, 2, false); break;                                      \
+      case 5: BODY(__nv_bfloat16, 2, true); break;                                       \
+      case 6: BODY(__nv_bfloat16, 3, false); break;                                      \
+      case 7: BODY(__nv_bfloat16, 3, true); break;                                       \
+      case 8: BODY(float, 0, false); break;                                              \
+      case 9: BODY(float, 0, true); break;                                               \
+      case 10: BODY(float, 1, false); break;                                             \
+      case 11: BODY(float, 1, true); break;                                              \
+      case 12: BODY(float, 2, false); break;                                             \
+      case 13: BODY(float, 2, true); break;                                              \
+      case 14: BODY(float, 3, false); break;                                             \
+      default: BODY(float, 3, true); break;                                              \
+    }                                                                                    \
+  } while (0)
+
+// ----------------------------------------------------------------- single-CTA kernel
+template <typename OutT, int EPI, bool ACC, int BN>
+__device__ __forceinline__ void epilogue_role_single(const TcParams& p, uint64_t* tfull, uint64_t* tempty,
+                                                     uint32_t tmem_base, float4* stg, int warp, int lane) {
+  const int q = warp & 3;            // TMEM lane quarter this warp may access
+  const int half = (warp - 2) >> 2;  // which half of the tile's columns
+  const int total = p.batch * p.tiles_m * p.tiles_n;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    TileInfo ti;
+    if (!decode_tile<BN>(p, t, ti)) continue;
+    mbar_wait(&tfull[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                           static_cast<uint32_t>(acc * BN + half * (BN / 2));
+    epilogue_stripe<OutT, EPI, ACC>(p, ti.z, ti.m0 + q * 32, ti.n0 + half * (BN / 2), BN / 2, taddr, stg, lane);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[acc]);
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+}
+
 template <int BN, int A_MN, int B_MN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const TcParams p) {
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
+  // Statically shared staging so the compiler emits STS/LDS (a generic-pointer
+  // LD after STG stalls on store ordering).
+  __shared__ __align__(16) float4 stg_all[STG_FLOAT4];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float4* stg_all = reinterpret_cast<float4*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -292,7 +320,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -323,13 +351,15 @@ __global__ void __launch_bounds__(192, 1)
           const int k0 = kb * BK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, &tma_a, &full[stage], ax + ti.m0 + 64 * j, ay + k0);
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sa + j * 8192, &tma_a, &full[stage], ax + ti.m0 + 64 * j, ay + k0);
           } else {
             tma_load_2d(sa, &tma_a, &full[stage], ax + k0, ay + ti.m0);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tma_b, &full[stage], bx + ti.n0 + 64 * j, by + k0);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * 8192, &tma_b, &full[stage], bx + ti.n0 + 64 * j, by + k0);
           } else {
             tma_load_2d(sb, &tma_b, &full[stage], bx + k0, by + ti.n0);
           }
@@ -373,24 +403,11 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..5)
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      TileInfo ti;
-      if (!decode_tile<BN>(p, t, ti)) continue;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      float4* stg = stg_all + (warp - 2) * 256;
-      if (p.c_f32) epilogue_stripe<float>(p, ti.z, ti.m0 + q * 32, ti.n0, BN, taddr, stg, lane);
-      else epilogue_stripe<__nv_bfloat16>(p, ti.z, ti.m0 + q * 32, ti.n0, BN, taddr, stg, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-    }
+    // ------------------------------------------------ epilogue (warps 2..9)
+    float4* stg = stg_all + (warp - 2) * 256;
+#define OASES_SINGLE_BODY(T, E, A) epilogue_role_single<T, E, A, BN>(p, tfull, tempty, tmem_base, stg, warp, lane)
+    OASES_EPI_DISPATCH(p, OASES_SINGLE_BODY);
+#undef OASES_SINGLE_BODY
   }
 
   tc_fence_before();
@@ -406,23 +423,56 @@ __global__ void __launch_bounds__(192, 1)
 // TPC computes a 256 x 256 tile. Each CTA stages its own 128-row half of A and
 // 128-row half of B (TMA completion counted on the leader's barrier); the
 // leader's single thread issues tcgen05.mma.cta_group::2 (M = 256) reading
-// both CTAs' smem, so per SM the operand traffic per MAC halves relative to
-// the 128 x 256 single-CTA tile. Accumulators: 2 x 256 TMEM columns per CTA.
+// both CTAs' smem. Accumulators: 2 x 256 TMEM columns per CTA. Causal K ranges
+// are defined at 128-row granularity, so attention stays on the single-CTA kernel.
 constexpr int PAIR_BM = 256, PAIR_BN = 256, PAIR_STAGES = 6;
-constexpr int PAIR_HALF_BYTES = 128 * BK * 2;               // 16 KB
-constexpr int PAIR_STAGE_BYTES = 2 * PAIR_HALF_BYTES;       // A half + B half
-constexpr int PAIR_STG_BYTES = 4 * 32 * 128;
-constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + PAIR_STG_BYTES + 256 + 1024;
+constexpr int PAIR_HALF_BYTES = 128 * BK * 2;          // 16 KB
+constexpr int PAIR_STAGE_BYTES = 2 * PAIR_HALF_BYTES;  // A half + B half
+constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 256 + 1024;  // + 32 KB static staging
 constexpr uint32_t PAIR_TMEM_COLS = 512;
 
+__device__ __forceinline__ void pair_decode(const TcParams& p, int t, int& z, int& m0, int& n0) {
+  const int per_z = p.tiles_m * p.tiles_n;
+  z = t / per_z;
+  const int r = t - z * per_z;
+  const int mt = r / p.tiles_n;
+  m0 = mt * PAIR_BM;
+  n0 = (r - mt * p.tiles_n) * PAIR_BN;
+}
+
+template <typename OutT, int EPI, bool ACC>
+__device__ __forceinline__ void epilogue_role_pair(const TcParams& p, uint64_t* tfull, uint64_t* tempty,
+                                                   uint32_t tmem_base, float4* stg, int warp, int lane,
+                                                   uint32_t rank) {
+  const int q = warp & 3, half = (warp - 2) >> 2;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int total = p.batch * p.tiles_m * p.tiles_n;
+  int acc = 0;
+  uint32_t acc_phase = 0;
+  for (int t = pair; t < total; t += npairs) {
+    int z, m0, n0;
+    pair_decode(p, t, z, m0, n0);
+    mbar_wait(&tfull[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                           static_cast<uint32_t>(acc * PAIR_BN + half * (PAIR_BN / 2));
+    const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
+    epilogue_stripe<OutT, EPI, ACC>(p, z, mb, n0 + half * (PAIR_BN / 2), PAIR_BN / 2, taddr, stg, lane);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+  }
+}
+
 template <int A_MN, int B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                     const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(16) float4 stg_all[STG_FLOAT4];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float4* stg_all = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + PAIR_STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES);
   uint64_t* empty = full + PAIR_STAGES;
   uint64_t* tfull = empty + PAIR_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -444,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs (leader's copy is used)
     }
     fence_barrier_init();
   }
@@ -454,22 +504,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto decode = [&](int t, int& z, int& m0, int& n0) {
-    const int per_z = p.tiles_m * p.tiles_n;
-    z = t / per_z;
-    const int r = t - z * per_z;
-    const int mt = r / p.tiles_n;
-    m0 = mt * PAIR_BM;
-    n0 = (r - mt * p.tiles_n) * PAIR_BN;
-  };
-
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total_tiles; t += npairs) {
         int z, m0, n0;
-        decode(t, z, m0, n0);
+        pair_decode(p, t, z, m0, n0);
         const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
         const int ax = p.a_x_off[0] * zo + p.a_x_off[1] * zi, ay = p.a_y_off[0] * zo + p.a_y_off[1] * zi;
         const int bx = p.b_x_off[0] * zo + p.b_x_off[1] * zi, by = p.b_y_off[0] * zo + p.b_y_off[1] * zi;
@@ -529,24 +570,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
     }
   } else {
-    const int q = warp & 3;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = pair; t < total_tiles; t += npairs) {
-      int z, m0, n0;
-      decode(t, z, m0, n0);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * PAIR_BN);
-      float4* stg = stg_all + (warp - 2) * 256;
-      const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
-      if (p.c_f32) epilogue_stripe<float>(p, z, mb, n0, PAIR_BN, taddr, stg, lane);
-      else epilogue_stripe<__nv_bfloat16>(p, z, mb, n0, PAIR_BN, taddr, stg, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-    }
+    float4* stg = stg_all + (warp - 2) * 256;
+#define OASES_PAIR_BODY(T, E, A) epilogue_role_pair<T, E, A>(p, tfull, tempty, tmem_base, stg, warp, lane, rank)
+    OASES_EPI_DISPATCH(p, OASES_PAIR_BODY);
+#undef OASES_PAIR_BODY
   }
 
   tc_fence_before();
@@ -604,7 +631,7 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcPara
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_tc_kernel<BN, A_MN, B_MN><<<grid, 192, Cfg::SMEM, stream>>>(ma, mb, p);
+  gemm_tc_kernel<BN, A_MN, B_MN><<<grid, THREADS, Cfg::SMEM, stream>>>(ma, mb, p);
   return cudaGetLastError();
 }
 
@@ -618,7 +645,7 @@ cudaError_t launch_tc2(const CUtensorMap& ma, const CUtensorMap& mb, const TcPar
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_tc2_kernel<A_MN, B_MN><<<grid, 192, PAIR_SMEM, stream>>>(ma, mb, p);
+  gemm_tc2_kernel<A_MN, B_MN><<<grid, THREADS, PAIR_SMEM, stream>>>(ma, mb, p);
   return cudaGetLastError();
 }
 
@@ -670,12 +697,17 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
     st.err = "gemm_tc: operand base/ld must be 16-byte aligned (ld % 8 == 0)";
     return st;
   }
-  if (d.ldc % 8 || !aligned(d.c, 16) || (d.c_col_off[0] % 8) || (d.c_col_off[1] % 8)) {
-    st.err = "gemm_tc: output base/ld/column offsets must be 16-byte aligned";
+  if (d.ldc % 8 || !aligned(d.c, 16) || (d.c_col_off[0] % 8) || (d.c_col_off[1] % 8) ||
+      (d.c2 && !aligned(d.c2, 16)) || (d.aux && !aligned(d.aux, 16)) || (d.bias && !aligned(d.bias, 16))) {
+    st.err = "gemm_tc: output/aux/bias bases, ld and column offsets must be 16-byte aligned";
     return st;
   }
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0 || d.batch_inner <= 0) {
     st.err = "gemm_tc: empty problem";
+    return st;
+  }
+  if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_DGELU) {
+    st.err = "gemm_tc: unknown epilogue";
     return st;
   }
   const int BN = (d.N <= 128) ? 128 : 256;
@@ -694,8 +726,6 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
     st.err = "gemm_tc: causal K-range modes need M == K";
     return st;
   }
-  // CTA pairs (256 x 256 tiles) for the large non-causal GEMMs; causal K
-  // ranges are defined at 128-row granularity, so attention stays single-CTA.
   const bool pair = use_pairs() && d.causal == OASES_CAUSAL_NONE && d.M > BM && d.N > 128;
   CUtensorMap ma, mb;
   if (!make_map(&ma, d.a, 64, d.a.mn_major ? 64 : BM, &st.err)) return st;

@@ -296,11 +296,17 @@ __global__ void __launch_bounds__(256) colpair_finalize_kernel(const float* __re
 // Dropout element index uses the GLOBAL head (head_offset + local head) so the
 // mask does not depend on the TMP degree: row r = (n*Hl + jl)*seq + i maps to
 // global row (n*Hg + head_offset + jl)*seq + i.
-__device__ __forceinline__ unsigned long long global_row(long long row, int seq, int hl, int hg, int hoff) {
-  const long long per = static_cast<long long>(hl) * seq;
-  const long long n = row / per, rem = row - n * per;
-  const long long jl = rem / seq, i = rem - jl * seq;
-  return static_cast<unsigned long long>((n * hg + hoff + jl) * seq + i);
+struct RowIdx {
+  int i;                    // query position within the sequence
+  unsigned long long ebase; // global element index of (row, 0) for the dropout key
+};
+__device__ __forceinline__ RowIdx row_index(unsigned row, int seq, int hl, int hg, int hoff) {
+  const unsigned per = static_cast<unsigned>(hl) * static_cast<unsigned>(seq);
+  const unsigned n = row / per, rem = row - n * per;
+  const unsigned jl = rem / static_cast<unsigned>(seq), i = rem - jl * static_cast<unsigned>(seq);
+  const unsigned long long grow =
+      (static_cast<unsigned long long>(n) * hg + hoff + jl) * static_cast<unsigned long long>(seq) + i;
+  return {static_cast<int>(i), grow * static_cast<unsigned long long>(seq)};
 }
 
 template <typename T, int NV>
@@ -309,42 +315,48 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const T* __restrict__ 
                                                           uint32_t thr, float keep_scale, uint64_t seed,
                                                           uint64_t offset, int hl, int hg, int hoff) {
   constexpr int V = Vec<T>::N;
-  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const unsigned row = blockIdx.x * 8u + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int lane = threadIdx.x & 31;
-  const int i = static_cast<int>(row % seq);
-  const T* sr = s + row * seq;
+  const RowIdx ri = row_index(row, seq, hl, hg, hoff);
+  const int i = ri.i;
+  const size_t roff = static_cast<size_t>(row) * seq;
+  const T* sr = s + roff;
+  const float sl2 = scale * 1.44269504088896341f;  // exp(x*scale) = exp2(x*scale*log2 e)
   float v[NV][V];
   float mx = -INFINITY;
 #pragma unroll
   for (int t = 0; t < NV; ++t) {
     const int c = (t * 32 + lane) * V;
-    if (c < seq && c <= i) {
+    if (c <= i) {  // c <= i < seq
       vload(sr + c, v[t]);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        v[t][e] = (c + e <= i) ? v[t][e] * scale : -INFINITY;
+        v[t][e] = (c + e <= i) ? v[t][e] * sl2 : -INFINITY;
         mx = fmaxf(mx, v[t][e]);
       }
-    } else {
-#pragma unroll
-      for (int e = 0; e < V; ++e) v[t][e] = -INFINITY;
     }
   }
   mx = warp_max(mx);
   float sum = 0.f;
 #pragma unroll
-  for (int t = 0; t < NV; ++t)
+  for (int t = 0; t < NV; ++t) {
+    const int c = (t * 32 + lane) * V;
+    if (c <= i) {
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const float ex = v[t][e] == -INFINITY ? 0.f : __expf(v[t][e] - mx);
-      v[t][e] = ex;
-      sum += ex;
+      for (int e = 0; e < V; ++e) {
+        v[t][e] = exp2f(v[t][e] - mx);  // exp2(-inf) = 0
+        sum += v[t][e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[t][e] = 0.f;
     }
+  }
   sum = warp_sum(sum);
   const float inv = 1.f / sum;
-  T* pr = p + row * seq;
-  T* pdr = pd ? pd + row * seq : nullptr;
+  T* pr = p + roff;
+  T* pdr = pd ? pd + roff : nullptr;
   // Only the band [0, round_up(i+1, 128)) is ever read by the causal P.V /
   // P^T.dO GEMMs (their K ranges stop at the 128-row tile edge), so the zero
   // tail beyond it is never written.
@@ -356,18 +368,9 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const T* __restrict__ 
 #pragma unroll
     for (int e = 0; e < V; ++e) v[t][e] *= inv;
     vstore(pr + c, v[t]);
-    if (pdr && c > i) {
-      vstore(pdr + c, v[t]);  // all zeros: no mask needed
-    } else if (pdr) {
-      const unsigned long long base = global_row(row, seq, hl, hg, hoff) * seq + c;
-#pragma unroll
-      for (int e = 0; e < V; e += 4) {
-        uint32_t u[4];
-        Philox::gen(seed, offset, (base + e) >> 2, u);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[t][e + q] = (u[q] >= thr) ? v[t][e + q] * keep_scale : 0.f;
-      }
-      vstore(pdr + c, v[t]);
+    if (pdr) {
+      if (c <= i) apply_dropout<V>(v[t], ri.ebase + c, seed, offset, thr, keep_scale);
+      vstore(pdr + c, v[t]);  // beyond i: zeros, no mask needed
     }
   }
 }
@@ -379,31 +382,24 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ 
                                                           uint32_t thr, float keep_scale, int use_dropout,
                                                           uint64_t seed, uint64_t offset, int hl, int hg, int hoff) {
   constexpr int V = Vec<T>::N;
-  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const unsigned row = blockIdx.x * 8u + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int lane = threadIdx.x & 31;
-  const int i = static_cast<int>(row % seq);
+  const RowIdx ri = row_index(row, seq, hl, hg, hoff);
+  const int i = ri.i;
+  const size_t roff = static_cast<size_t>(row) * seq;
   float pv[NV][V], dv[NV][V];
   float dot = 0.f;
 #pragma unroll
   for (int t = 0; t < NV; ++t) {
     const int c = (t * 32 + lane) * V;
-    if (c < seq && c <= i) {
-      vload(p + row * seq + c, pv[t]);
-      vload(dpd + row * seq + c, dv[t]);
-      if (use_dropout) {
-        const unsigned long long base = global_row(row, seq, hl, hg, hoff) * seq + c;
-#pragma unroll
-        for (int e = 0; e < V; e += 4) {
-          uint32_t u[4];
-          Philox::gen(seed, offset, (base + e) >> 2, u);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dv[t][e + q] = (u[q] >= thr) ? dv[t][e + q] * keep_scale : 0.f;
-        }
-      }
+    if (c <= i) {
+      vload(p + roff + c, pv[t]);
+      vload(dpd + roff + c, dv[t]);
+      if (use_dropout) apply_dropout<V>(dv[t], ri.ebase + c, seed, offset, thr, keep_scale);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        if (c + e > i) { pv[t][e] = 0.f; dv[t][e] = 0.f; }
+        if (c + e > i) dv[t][e] = 0.f;  // P is 0 there; dP_drop may be unwritten
         dot += pv[t][e] * dv[t][e];
       }
     } else {
@@ -419,7 +415,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const T* __restrict__ 
     if (c >= band) continue;
 #pragma unroll
     for (int e = 0; e < V; ++e) pv[t][e] = scale * pv[t][e] * (dv[t][e] - dot);
-    vstore(ds + row * seq + c, pv[t]);
+    vstore(ds + roff + c, pv[t]);
   }
 }
 
@@ -548,7 +544,7 @@ cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long b
                         float dropout_p, uint64_t seed, uint64_t offset, int hl, int hg, int hoff, cudaStream_t st) {
   const long long rows = batch * seq;
   const uint32_t thr = dropout_threshold(dropout_p);
-  const float ks = dropout_p > 0.f ? 1.f / (1.f - dropout_p) : 1.f;
+  const float ks = dropout_keep_scale(dropout_p);
   if (dropout_p <= 0.f) pd = nullptr;
   if (dtype == OASES_BF16)
     return launch_rows_nv<__nv_bfloat16, SoftmaxFwdL>(seq, rows, st, static_cast<const __nv_bfloat16*>(s),
@@ -562,7 +558,7 @@ cudaError_t softmax_bwd(int dtype, const void* p, const void* dpd, void* ds, lon
                         float dropout_p, uint64_t seed, uint64_t offset, int hl, int hg, int hoff, cudaStream_t st) {
   const long long rows = batch * seq;
   const uint32_t thr = dropout_threshold(dropout_p);
-  const float ks = dropout_p > 0.f ? 1.f / (1.f - dropout_p) : 1.f;
+  const float ks = dropout_keep_scale(dropout_p);
   const int use = dropout_p > 0.f ? 1 : 0;
   if (dtype == OASES_BF16)
     return launch_rows_nv<__nv_bfloat16, SoftmaxBwdL>(seq, rows, st, static_cast<const __nv_bfloat16*>(p),

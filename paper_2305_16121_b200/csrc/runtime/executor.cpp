@@ -195,7 +195,8 @@ tmpsim::SimResult Executor::step(bool trace) {
       r.trace.push_back({i, stream ? tmpsim::Stream::Comm : tmpsim::Stream::Compute, s0, s1});
       if (stream) {
         // tp == 1 AllReduces are empty: they contribute no interval
-        if (stack_.ctx().tp > 1 && !stack_.ctx().comm_disabled) comm.emplace_back(s0, s1);
+        const Context& cx = stack_.ctx();
+        if (!cx.comm_disabled && (cx.tp > 1 || cx.nccl)) comm.emplace_back(s0, s1);
       } else {
         comp.emplace_back(s0, s1);
         busy += s1 - s0;

@@ -71,7 +71,9 @@ std::unique_ptr<Context> make_context(const oases_ctx_desc& d) {
   // soon as the overlapped GEMM frees SMs.
   check_cuda(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi), "comm stream");
   ctx->comm_disabled = d.comm_disabled != 0;
-  if (d.tp > 1 && d.local_workers == 1 && !ctx->comm_disabled) {
+  // tp == 1 with an id: a single-rank NCCL communicator (AllReduce is the
+  // identity) -- exercises the NCCL path, including graph capture, on one GPU.
+  if (d.local_workers == 1 && !ctx->comm_disabled && (d.tp > 1 || d.unique_id)) {
     ncclUniqueId id;
     static_assert(sizeof(ncclUniqueId) == OASES_UNIQUE_ID_BYTES, "unique id size");
     std::memcpy(&id, d.unique_id, sizeof(id));
@@ -777,7 +779,7 @@ void Stack::tail(int wi, int sb) {
 }
 
 void Stack::allreduce(tmpsim::Pass pass, int block, int sb, bool both) {
-  if (ctx_.tp == 1 || ctx_.comm_disabled) return;
+  if (ctx_.comm_disabled || (ctx_.tp == 1 && !ctx_.nccl)) return;
   const int par = block % 2;
   auto pick = [&](Worker& w) -> void* {
     auto& arr = pass == tmpsim::Pass::Forward ? w.fwd_ar[par] : pass == tmpsim::Pass::Recompute ? w.rec_ar[par] : w.bwd_ar[par];

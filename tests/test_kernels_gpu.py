@@ -9,7 +9,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from paper_2305_16121_b200 import ops  # noqa: E402
-from oracle.oracle import keep_mask  # noqa: E402
+from oracle.oracle import keep_mask, keep_scale  # noqa: E402
 
 
 def rel(a, b):
@@ -28,13 +28,13 @@ def test_bias_dropout_residual_and_colsum(cuda, dt, tol, rows, cols):
     p = 0.1 if rows * cols % 4 == 0 else 0.0
     ops.bias_dropout_residual_fwd(x, b, r, out, dropout_p=p, seed=5, offset=9)
     keep = torch.tensor(keep_mask(5, 9, rows * cols, p), device=cuda).view(rows, cols).double()
-    ref = r.double() + (x.double() + b.double()) * keep / (1 - p)
+    ref = r.double() + (x.double() + b.double()) * keep * keep_scale(p)
     torch.cuda.synchronize()
     assert rel(out, ref) < tol
     dx = torch.empty_like(x)
     db = torch.zeros(cols, device=cuda)
     ops.bias_dropout_residual_bwd(x, dx, db, dropout_p=p, seed=5, offset=9)
-    ref_dx = x.double() * keep / (1 - p)
+    ref_dx = x.double() * keep * keep_scale(p)
     torch.cuda.synchronize()
     assert rel(dx, ref_dx) < tol
     assert rel(db, ref_dx.sum(0)) < (1e-4 if dt == torch.float32 else 2e-2)
@@ -93,11 +93,11 @@ def test_causal_softmax_fwd_bwd(cuda, dt, tol, seq, p):
         keep = torch.zeros(rows, seq, dtype=torch.float64, device=cuda)
         km = torch.tensor(keep_mask(3, 11, n * hg * seq * seq, p), device=cuda).view(n, hg, seq, seq)
         keep = km[:, hoff:hoff + hl].reshape(rows, seq).double()
-        assert rel(Pd[band], (ref * keep / (1 - p))[band]) < tol
+        assert rel(Pd[band], (ref * keep * keep_scale(p))[band]) < tol
     dpd = torch.randn(rows, seq, device=cuda).to(dt)
     ds = torch.empty_like(s)
     ops.softmax_bwd(P, dpd, ds, n * hl, seq, scale, p, 3, 11, hl, hg, hoff)
-    dp = dpd.double() * (keep / (1 - p) if p > 0 else 1.0)
+    dp = dpd.double() * (keep * keep_scale(p) if p > 0 else 1.0)
     dp = dp.masked_fill(~causal, 0.0)
     ref_ds = scale * ref * (dp - (ref * dp).sum(-1, keepdim=True))
     torch.cuda.synchronize()

@@ -9,7 +9,7 @@ import math
 import numpy as np
 import torch
 
-from oracle.oracle import B_COL, B_ROW, LN_BETA, LN_GAMMA, W_COL, W_ROW, keep_mask
+from oracle.oracle import B_COL, B_ROW, LN_BETA, LN_GAMMA, W_COL, W_ROW, keep_mask, keep_scale
 
 
 def run_torch_ref(orc):
@@ -31,7 +31,7 @@ def run_torch_ref(orc):
         for sb in range((T + rows_per_sb - 1) // rows_per_sb):
             k = keep_mask(cfg.seed, (b * 2 + sb) * 4 + 0, rows_per_sb * h, cfg.hidden_dropout)
             m[sb * rows_per_sb:(sb + 1) * rows_per_sb] = k.reshape(rows_per_sb, h)
-        return torch.tensor(m / (1.0 - float(np.float32(cfg.hidden_dropout))))
+        return torch.tensor(m * keep_scale(cfg.hidden_dropout))
 
     def attn_mask(b, r):
         Ht = cfg.heads // cfg.tp
@@ -42,7 +42,7 @@ def run_torch_ref(orc):
             k = keep_mask(cfg.seed, (b * 2 + sb) * 4 + 1, half * H * s * s, cfg.attention_dropout)
             k = k.reshape(half, H, s, s)
             m[n] = k[nl, r * Ht:(r + 1) * Ht]
-        return torch.tensor(m / (1.0 - float(np.float32(cfg.attention_dropout))))
+        return torch.tensor(m * keep_scale(cfg.attention_dropout))
 
     x = x0
     for b in range(orc.num_blocks):
