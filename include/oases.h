@@ -103,6 +103,43 @@ typedef struct {
 oases_status oases_gemm(const oases_gemm_desc* desc, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Fused causal attention (tcgen05 flash kernels; bf16, head_dim 64 | 128,   */
+/* seq % 128 == 0). Same arithmetic as the unfused QK^T -> softmax ->        */
+/* dropout -> PV chain (numerics.cpp attention, dropout keys of DESIGN.md)  */
+/* without materialising the [seq, seq] probabilities.                      */
+/*   qkv   [samples*seq, ld_qkv]: Q | K | V column blocks of                 */
+/*         heads_local*head_dim each (head h at h*head_dim inside a block)   */
+/*   out   [samples*seq, ld_out]: ctx, head h at column h*head_dim           */
+/*   lse   [samples*heads_local*seq] f32 row log-sum-exp (log2 domain)       */
+/*   bwd:  dout like out; dqkv like qkv (all three blocks written);          */
+/*         ds [samples*heads_local*seq, seq] bf16 scratch (dS, causal band); */
+/*         workspace: oases_attention_bwd_workspace() bytes                  */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t dtype; /* OASES_BF16 */
+  int32_t samples, heads_local, heads_total, head_offset, head_dim, seq;
+  int32_t max_ctas; /* dQ GEMM CTA cap (0 = all SMs) */
+  const void* qkv;
+  int64_t ld_qkv;
+  void* out;
+  int64_t ld_out;
+  float* lse;
+  const void* dout;
+  int64_t ld_dout;
+  void* dqkv;
+  int64_t ld_dqkv;
+  void* ds;
+  void* workspace;
+  float scale, dropout_p;
+  uint64_t seed, offset;
+} oases_attn_desc;
+
+int32_t oases_attention_supported(int dtype, int32_t head_dim, int32_t seq);
+oases_status oases_attention_fwd(const oases_attn_desc* desc, void* stream);
+size_t oases_attention_bwd_workspace(const oases_attn_desc* desc);
+oases_status oases_attention_bwd(const oases_attn_desc* desc, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* HBM-bound kernels (vectorised, warp-shuffle reductions).                  */
 /* All row-major [rows x cols]; dtype selects f32 or bf16 activations;       */
 /* statistics, parameters' gradients and loss are always f32.               */

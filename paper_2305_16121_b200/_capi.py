@@ -64,6 +64,34 @@ class GemmDesc(C.Structure):
     ]
 
 
+class AttnDesc(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int32),
+        ("samples", C.c_int32),
+        ("heads_local", C.c_int32),
+        ("heads_total", C.c_int32),
+        ("head_offset", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("seq", C.c_int32),
+        ("max_ctas", C.c_int32),
+        ("qkv", C.c_void_p),
+        ("ld_qkv", C.c_int64),
+        ("out", C.c_void_p),
+        ("ld_out", C.c_int64),
+        ("lse", C.c_void_p),
+        ("dout", C.c_void_p),
+        ("ld_dout", C.c_int64),
+        ("dqkv", C.c_void_p),
+        ("ld_dqkv", C.c_int64),
+        ("ds", C.c_void_p),
+        ("workspace", C.c_void_p),
+        ("scale", C.c_float),
+        ("dropout_p", C.c_float),
+        ("seed", C.c_uint64),
+        ("offset", C.c_uint64),
+    ]
+
+
 class CtxDesc(C.Structure):
     _fields_ = [
         ("tp", C.c_int32),
@@ -155,6 +183,10 @@ _SIGNATURES = [
     ("oases_version", C.c_char_p, []),
     ("oases_device_sm_count", C.c_int, []),
     ("oases_gemm", C.c_int, [C.POINTER(GemmDesc), C.c_void_p]),
+    ("oases_attention_supported", C.c_int32, [C.c_int, C.c_int32, C.c_int32]),
+    ("oases_attention_fwd", C.c_int, [C.POINTER(AttnDesc), C.c_void_p]),
+    ("oases_attention_bwd_workspace", C.c_size_t, [C.POINTER(AttnDesc)]),
+    ("oases_attention_bwd", C.c_int, [C.POINTER(AttnDesc), C.c_void_p]),
     ("oases_layernorm_fwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                        C.c_float, C.c_void_p]),
     ("oases_layernorm_bwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,

@@ -1,0 +1,865 @@
+// Fused causal self-attention on tcgen05 (bf16, head_dim 64 | 128, seq % 128 == 0).
+//
+// The reference's attention (proj/src/numerics.cpp, the per-head
+// softmax(Q K^T / sqrt(d)) V of the TMP layer, with attention dropout on the
+// probabilities) is computed here without materialising the [seq, seq]
+// probability matrix in HBM:
+//
+//   attn_fwd_kernel   one CTA per (sample x local head, 128-query tile).
+//                     S_j = Q K_j^T into TMEM (double-buffered), online
+//                     softmax in registers (one query row per thread), the
+//                     dropout keep-mask of DESIGN.md "Dropout keys" applied to
+//                     the unnormalised probabilities, P_j -> swizzled smem,
+//                     O += P_j V_j accumulated in TMEM (rescaled in place when
+//                     the running max grows). Writes ctx (bf16) and the row
+//                     log-sum-exp (log2 domain, f32) for the backward.
+//   attn_dsum_kernel  D_i = sum_d dO_i,d * O_i,d  (= sum_j P_ij dP_ij).
+//   attn_dkdv_kernel  one CTA per (sample x head, 128-key tile), streaming the
+//                     query tiles at or below the diagonal: S = Q K^T and
+//                     dP_drop = dO V^T into TMEM, P = exp2(S - lse), the
+//                     dropped P -> smem -> dV += P_drop^T dO; dS = P o (dP - D)
+//                     -> smem -> dK += dS^T Q. dS is also TMA-stored to HBM so
+//                     dQ = dS K runs as one batched causal tcgen05 GEMM
+//                     (deterministic: no atomics anywhere).
+//
+// Warp roles (320 threads, 1 CTA per SM): warp 0 TMA producer, warp 1 MMA
+// issuer + TMEM owner, warps 2..9 the row-wise math: warp w owns TMEM lanes
+// 32*(w%4) .. +31 (query/key rows of the 128-row tile) and half (w-2)/4 of the
+// 128 key columns; the two warps of a row exchange their partial row maxima
+// through smem (forward only -- the backward needs no row reductions).
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "kernels.h"
+
+namespace oases {
+
+namespace {
+
+constexpr int kTile = 128;
+constexpr int kRowWarps = 8;                    // two warps per TMEM lane quarter, 64 columns each
+constexpr int kThreads = 64 + 32 * kRowWarps;  // + TMA warp + MMA warp
+constexpr float kLog2e = 1.44269504088896341f;
+
+struct AttnParams {
+  int seq, hl, hg, hoff, Z, nq;
+  int q_col, k_col, v_col;  // columns of head 0 of Q / K / V in the qkv (and dqkv) rows
+  int do_col;               // column of head 0 in dout / out rows
+  long long ld_out;         // fwd: ctx row stride; bwd: dqkv row stride
+  void* out;                // fwd: ctx; bwd: dqkv
+  float* lse;               // [Z * seq], log2 domain
+  const float* dsum;        // [Z * seq]
+  float sl2;                // scale * log2(e)
+  float scale;
+  uint32_t thr;             // dropout byte threshold (0 = no dropout)
+  float ks;                 // keep scale
+  uint64_t seed, offset;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_bf16(uint32_t w) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 16-byte chunk `ch` (8 bf16 columns, ch in 0..15 over 128 columns) of row r of a
+// [128 x 128] bf16 tile stored as two SW128 K-major [128 x 64] halves 16 KB apart.
+__device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int r, int ch) {
+  return reinterpret_cast<uint4*>(tile + (ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+// Philox4x32-10 (common.cuh) with the round keys and
+// the offset words hoisted out of the per-call path: they are the same for
+// every call of a launch.
+struct PhiloxState {
+  uint32_t k0[10], k1[10];
+  uint32_t o0, o1;
+  uint32_t thr4;
+};
+__device__ __forceinline__ void philox_init(const AttnParams& p, PhiloxState& ps) {
+  uint32_t a = static_cast<uint32_t>(p.seed), b = static_cast<uint32_t>(p.seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    ps.k0[r] = a;
+    ps.k1[r] = b;
+    a += 0x9E3779B9u;
+    b += 0xBB67AE85u;
+  }
+  ps.o0 = static_cast<uint32_t>(p.offset);
+  ps.o1 = static_cast<uint32_t>(p.offset >> 32);
+  ps.thr4 = p.thr * 0x01010101u;
+}
+// Keep masks of 16 consecutive elements (Philox counter ctr) as 8 bf16x2 lane
+// masks: m[k] covers elements 2k (low half) and 2k+1.
+__device__ __forceinline__ void keep_masks16(const PhiloxState& ps, unsigned long long ctr, uint32_t (&m)[8]) {
+  uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = ps.o0, c3 = ps.o1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = static_cast<unsigned long long>(0xD2511F53u) * c0;
+    const unsigned long long p1 = static_cast<unsigned long long>(0xCD9E8D57u) * c2;
+    const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ ps.k0[r];
+    const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ ps.k1[r];
+    c1 = static_cast<uint32_t>(p1);
+    c3 = static_cast<uint32_t>(p0);
+    c0 = n0;
+    c2 = n2;
+  }
+  const uint32_t u[4] = {c0, c1, c2, c3};
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t k = __vcmpgeu4(u[w], ps.thr4);
+    m[2 * w] = __byte_perm(k, 0, 0x1100);
+    m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
+  }
+}
+
+template <int DH>
+struct FwdCfg {
+  static constexpr int TILE_BYTES = kTile * DH * 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
+  static constexpr int P_OFF = V_OFF + 2 * TILE_BYTES;
+  static constexpr int RED_OFF = P_OFF + kTile * kTile * 2;  // row-sum exchange [2][128]
+  static constexpr int BAR_OFF = RED_OFF + 1024;
+  static constexpr int SMEM = BAR_OFF + 256;
+  static constexpr uint32_t TMEM_COLS = 512;  // S x2 (256) + O (DH)
+};
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, const AttnParams p) {
+  using C = FwdCfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* v_full = bars + 3;    // [2]
+  uint64_t* k_empty = bars + 5;   // [2] freed by the S MMA
+  uint64_t* s_full = bars + 7;    // [2]
+  uint64_t* s_empty = bars + 9;   // [2]
+  uint64_t* p_full = bars + 11;
+  uint64_t* pv_done = bars + 12;
+  uint64_t* v_empty = bars + 13;  // [2] freed by the PV MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = p.nq - 1 - static_cast<int>(blockIdx.x) / p.Z;  // longest rows first
+  const int z = static_cast<int>(blockIdx.x) % p.Z;
+  const int n = z / p.hl, jl = z - n * p.hl;
+  const int nkv = qt + 1;
+  const int row0 = n * p.seq;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], kRowWarps);
+    }
+    mbar_init(p_full, kRowWarps);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&tqkv);
+      mbar_arrive_expect_tx(q_full, C::TILE_BYTES);
+#pragma unroll
+      for (int g = 0; g < DH / 64; ++g)
+        tma_load_2d(smem + C::Q_OFF + g * 16384, &tqkv, q_full, p.q_col + jl * DH + g * 64, row0 + qt * kTile);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
+#pragma unroll
+        for (int g = 0; g < DH / 64; ++g)
+          tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + g * 16384, &tqkv, &k_full[st],
+                      p.k_col + jl * DH + g * 64, row0 + j * kTile);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
+#pragma unroll
+        for (int g = 0; g < DH / 64; ++g)
+          tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + g * 16384, &tqkv, &v_full[st],
+                      p.v_col + jl * DH + g * 64, row0 + j * kTile);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = umma_idesc_bf16(kTile, kTile, 0, 0);
+      constexpr uint32_t id_o = umma_idesc_bf16(kTile, DH, 0, 1);
+      const uint32_t sb = smem_u32(smem);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qa = sb + C::Q_OFF, kb = sb + C::K_OFF + st * C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + st * kTile, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
+                    id_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[st]);
+        umma_commit(&k_empty[st]);
+      };
+      auto issue_pv = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t pa = sb + C::P_OFF, vb = sb + C::V_OFF + st * C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {
+          const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = umma_desc_sw128(vb + kk * 2048, 16384, 1024);
+          umma_bf16(tmem + 2 * kTile, ad, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&v_empty[st]);
+        umma_commit(pv_done);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);
+        issue_pv(j);
+      }
+    }
+  } else {
+    // ------------------------------------------------ row warps: query row r, key columns [c0, c0 + 64)
+    const int q = warp & 3, hf = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const int i = qt * kTile + r;
+    const int c0 = hf * 64;
+    const unsigned long long ebase =
+        (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i) * static_cast<unsigned long long>(p.seq) +
+        c0;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t to = tl + 2 * kTile + hf * (DH / 2);  // this warp's half of the O accumulator
+    uint8_t* pbuf = smem + C::P_OFF;
+    float* xsum = reinterpret_cast<float*>(smem + C::RED_OFF);  // [half][row]
+    PhiloxState ph;
+    philox_init(p, ph);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      // the row max needs all 128 keys: read the partner half too (TMEM reads are cheap)
+      uint32_t u[2][32], w[2][32];
+      tmem_ld32(tl + st * kTile + c0, u[0]);
+      tmem_ld32(tl + st * kTile + c0 + 32, u[1]);
+      tmem_ld32(tl + st * kTile + (c0 ^ 64), w[0]);
+      tmem_ld32(tl + st * kTile + (c0 ^ 64) + 32, w[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);
+      float mloc = -INFINITY;
+      if (j == qt) {
+        int lim = r - c0, limw = r - (c0 ^ 64);  // keys > r are masked
+        asm volatile("" : "+r"(lim), "+r"(limw));  // keep the comparisons inside the (rare) diagonal branch
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          if (k > lim) u[k >> 5][k & 31] = __float_as_uint(-INFINITY);
+          if (k > limw) w[k >> 5][k & 31] = __float_as_uint(-INFINITY);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 64; ++k)
+        mloc = fmaxf(mloc, fmaxf(__uint_as_float(u[k >> 5][k & 31]), __uint_as_float(w[k >> 5][k & 31])));
+      const float mx = fmaxf(m, mloc * p.sl2);
+      const float alpha = ex2(m - mx);
+      const float nmx = -mx;
+      float sum = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int k = 0; k < 64; k += 2) {
+        const float a = ex2(fmaf(__uint_as_float(u[k >> 5][k & 31]), p.sl2, nmx));
+        const float b = ex2(fmaf(__uint_as_float(u[k >> 5][(k & 31) + 1]), p.sl2, nmx));
+        sum += a + b;
+        pk[k >> 1] = pack_bf16(a, b);
+      }
+      l = l * alpha + sum;
+      m = mx;
+      if (p.thr) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t km[8];
+          keep_masks16(ph, (ebase + static_cast<unsigned long long>(j) * kTile + g * 16) >> 4, km);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
+        }
+      }
+      if (j > 0) {
+        // P buffer free and O holds P_{j-1} V_{j-1}: rescale O to the new max.
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c) {
+            uint32_t o[32];
+            tmem_ld32(to + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            tmem_st32(to + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        *tile_chunk(pbuf, r, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    xsum[hf * 128 + r] = l;
+    named_bar_sync(1 + q, 64);
+    const float lt = l + xsum[(hf ^ 1) * 128 + r];
+    mbar_wait(pv_done, (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = p.ks / lt;
+    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + i) * p.ld_out +
+                          p.do_col + jl * DH + hf * (DH / 2);
+#pragma unroll
+    for (int c = 0; c < DH / 64; ++c) {
+      uint32_t o[32];
+      tmem_ld32(to + c * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float* f = reinterpret_cast<const float*>(o + 8 * k);
+        *reinterpret_cast<uint4*>(orow + c * 32 + k * 8) =
+            make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                       pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+      }
+    }
+    if (hf == 0) p.lse[static_cast<long long>(z) * p.seq + i] = m + log2f(lt);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// D[z, i] = sum_d dO[i, d] * O[i, d] (head z's columns); one warp per row.
+template <int DH>
+__global__ void __launch_bounds__(256) attn_dsum_kernel(const __nv_bfloat16* __restrict__ dout,
+                                                        const __nv_bfloat16* __restrict__ out, long long ld,
+                                                        float* __restrict__ dsum, int seq, int hl, int col0,
+                                                        long long rows) {
+  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const long long per = static_cast<long long>(hl) * seq;
+  const int n = static_cast<int>(row / per);
+  const int rem = static_cast<int>(row - n * per);
+  const int jl = rem / seq, i = rem - jl * seq;
+  const long long off = static_cast<long long>(n * seq + i) * ld + col0 + jl * DH;
+  float acc = 0.f;
+  for (int d = lane * 4; d < DH; d += 128) {
+    const uint2 a = *reinterpret_cast<const uint2*>(dout + off + d);
+    const uint2 b = *reinterpret_cast<const uint2*>(out + off + d);
+    const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.x));
+    const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.y));
+    const float2 b0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b.x));
+    const float2 b1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b.y));
+    acc += a0.x * b0.x + a0.y * b0.y + a1.x * b1.x + a1.y * b1.y;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) dsum[row] = acc;
+}
+
+template <int DH>
+struct BwdCfg {
+  static constexpr int TILE_BYTES = kTile * DH * 2;
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = TILE_BYTES;
+  static constexpr int STAGE_OFF = 2 * TILE_BYTES;
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES + 1024;  // Q_i, dO_i, lse_i[128], D_i[128]
+  static constexpr int BUF_OFF = STAGE_OFF + 2 * STAGE_BYTES;
+  static constexpr int BAR_OFF = BUF_OFF + kTile * kTile * 2;
+  static constexpr int SMEM = BAR_OFF + 256;
+  static constexpr uint32_t TMEM_COLS = 512;  // S, dP (128 each), dV, dK (DH each)
+};
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_dkdv_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
+                     const __grid_constant__ CUtensorMap tds, const AttnParams p) {
+  using C = BwdCfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* kv_full = bars;
+  uint64_t* st_full = bars + 1;   // [2] Q_i, dO_i, lse_i, D_i
+  uint64_t* st_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // S_i in TMEM
+  uint64_t* s_free = bars + 6;    // row warps read S_i
+  uint64_t* dp_full = bars + 7;   // dP_i in TMEM
+  uint64_t* dp_free = bars + 8;   // row warps read dP_i
+  uint64_t* pd_full = bars + 9;   // keep o P_i in the buffer
+  uint64_t* buf_free1 = bars + 10;  // dV MMA done with it
+  uint64_t* ds_full = bars + 11;    // dS_i in the buffer
+  uint64_t* buf_free2 = bars + 12;  // dK MMA done with it
+  uint64_t* acc_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = static_cast<int>(blockIdx.x) / p.Z;  // longest column (kt = 0) first
+  const int z = static_cast<int>(blockIdx.x) % p.Z;
+  const int n = z / p.hl, jl = z - n * p.hl;
+  const int ni = p.nq - kt;
+  const int row0 = n * p.seq;
+  const uint32_t t_s = 0, t_dp = kTile, t_dv = 2 * kTile, t_dk = 2 * kTile + DH;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, kRowWarps);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_free, kRowWarps);
+    mbar_init(pd_full, kRowWarps);
+    mbar_init(buf_free1, 1);
+    mbar_init(ds_full, 1);
+    mbar_init(buf_free2, 1);
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch(&tqkv);
+      tma_prefetch(&tdo);
+      mbar_arrive_expect_tx(kv_full, 2 * C::TILE_BYTES);
+#pragma unroll
+      for (int g = 0; g < DH / 64; ++g) {
+        tma_load_2d(smem + C::K_OFF + g * 16384, &tqkv, kv_full, p.k_col + jl * DH + g * 64, row0 + kt * kTile);
+        tma_load_2d(smem + C::V_OFF + g * 16384, &tqkv, kv_full, p.v_col + jl * DH + g * 64, row0 + kt * kTile);
+      }
+      for (int it = 0; it < ni; ++it) {
+        const int st = it & 1, i = kt + it;
+        mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        uint8_t* sp = smem + C::STAGE_OFF + st * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&st_full[st], C::STAGE_BYTES);
+#pragma unroll
+        for (int g = 0; g < DH / 64; ++g) {
+          tma_load_2d(sp + g * 16384, &tqkv, &st_full[st], p.q_col + jl * DH + g * 64, row0 + i * kTile);
+          tma_load_2d(sp + C::TILE_BYTES + g * 16384, &tdo, &st_full[st], p.do_col + jl * DH + g * 64,
+                      row0 + i * kTile);
+        }
+        const long long ro = static_cast<long long>(z) * p.seq + i * kTile;
+        bulk_load(sp + 2 * C::TILE_BYTES, p.lse + ro, 512, &st_full[st]);
+        bulk_load(sp + 2 * C::TILE_BYTES + 512, p.dsum + ro, 512, &st_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // Issue order per query tile i: dV_i, S_{i+1}, dK_i, dP_{i+1} -- S_{i+1} runs under
+      // the row warps' dS pass of tile i, dP_{i+1} under their P pass of tile i+1.
+      constexpr uint32_t id_s = umma_idesc_bf16(kTile, kTile, 0, 0);
+      constexpr uint32_t id_g = umma_idesc_bf16(kTile, DH, 1, 1);
+      const uint32_t sb = smem_u32(smem);
+      const uint32_t ka = sb + C::K_OFF, va = sb + C::V_OFF, buf = sb + C::BUF_OFF;
+      auto stage_addr = [&](int it) { return sb + C::STAGE_OFF + (it & 1) * C::STAGE_BYTES; };
+      auto issue_s = [&](int it) {  // S = Q_i K^T
+        mbar_wait(&st_full[it & 1], (it >> 1) & 1);
+        mbar_wait(s_free, (it & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qa = stage_addr(it);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + t_s, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(ka + off, 16, 1024), id_s,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);
+      };
+      auto issue_dp = [&](int it) {  // dP_drop = dO_i V^T
+        mbar_wait(dp_free, (it & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t da = stage_addr(it) + C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + t_dp, umma_desc_sw128(da + off, 16, 1024), umma_desc_sw128(va + off, 16, 1024), id_s,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(dp_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      issue_dp(0);
+      for (int it = 0; it < ni; ++it) {
+        const uint32_t qa = stage_addr(it), da = qa + C::TILE_BYTES;
+        // dV += (keep o P)^T dO   (A: keys x queries, MN-major view of the [query][key] buffer)
+        mbar_wait(pd_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          umma_bf16(tmem + t_dv, umma_desc_sw128(buf + kk * 2048, 16384, 1024),
+                    umma_desc_sw128(da + kk * 2048, 16384, 1024), id_g, (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(buf_free1);
+        if (it + 1 < ni) issue_s(it + 1);
+        // dK += dS^T Q
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          umma_bf16(tmem + t_dk, umma_desc_sw128(buf + kk * 2048, 16384, 1024),
+                    umma_desc_sw128(qa + kk * 2048, 16384, 1024), id_g, (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&st_empty[it & 1]);
+        umma_commit(buf_free2);
+        if (it + 1 < ni) issue_dp(it + 1);
+      }
+      umma_commit(acc_full);
+    }
+  } else {
+    // ------------------------------------------------ row warps: query row r of tile i, keys [c0, c0 + 64)
+    const int q = warp & 3, hf = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const int c0 = hf * 64;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    uint8_t* buf = smem + C::BUF_OFF;
+    const bool leader = threadIdx.x == 64;
+    PhiloxState ph;
+    philox_init(p, ph);
+    for (int it = 0; it < ni; ++it) {
+      const int st = it & 1, i = kt + it;
+      const uint8_t* sp = smem + C::STAGE_OFF + st * C::STAGE_BYTES;
+      mbar_wait(&st_full[st], (it >> 1) & 1);
+      const float nlse = -reinterpret_cast<const float*>(sp + 2 * C::TILE_BYTES)[r];
+      const float dsum = reinterpret_cast<const float*>(sp + 2 * C::TILE_BYTES + 512)[r];
+      int lim = it == 0 ? r - c0 : 1 << 20;  // keys c0 + k > r are masked on the diagonal tile
+      asm volatile("" : "+r"(lim));
+      const unsigned long long ebase =
+          (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i * kTile + r) *
+              static_cast<unsigned long long>(p.seq) +
+          static_cast<unsigned long long>(kt) * kTile + c0;
+      // pass 1: P = exp2(S*sl2 - lse) (kept in registers as bf16), keep o P -> buffer
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t u[2][32];
+      tmem_ld32(tl + t_s + c0, u[0]);
+      tmem_ld32(tl + t_s + c0 + 32, u[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);
+      uint32_t pp[32];  // P, bf16x2
+#pragma unroll
+      for (int k = 0; k < 64; k += 2) {
+        float a = ex2(fmaf(__uint_as_float(u[k >> 5][k & 31]), p.sl2, nlse));
+        float b = ex2(fmaf(__uint_as_float(u[k >> 5][(k & 31) + 1]), p.sl2, nlse));
+        if (k > lim) a = 0.f;
+        if (k + 1 > lim) b = 0.f;
+        pp[k >> 1] = pack_bf16(a, b);
+      }
+      uint32_t pk[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) pk[k] = pp[k];
+      if (p.thr) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t km[8];
+          keep_masks16(ph, (ebase + g * 16) >> 4, km);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
+        }
+      }
+      // the previous dK MMA and dS store must be done with the buffer
+      if (it > 0) {
+        mbar_wait(buf_free2, (it - 1) & 1);
+        if (leader) bulk_wait_read0();
+        named_bar_sync(1, 32 * kRowWarps);
+      }
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        *tile_chunk(buf, r, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pd_full);
+      // pass 2: dS = scale * (ks * (keep o P) o dP_drop - P D) -> buffer (after the dV MMA read it)
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      uint32_t v[2][32];
+      tmem_ld32(tl + t_dp + c0, v[0]);
+      tmem_ld32(tl + t_dp + c0 + 32, v[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dp_free);
+      const float c1 = p.scale * p.ks, c2 = -p.scale * dsum;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float2 pr = unpack_bf16(pp[k]);
+        const float2 kp = unpack_bf16(pk[k]);
+        const float d0 = fmaf(kp.x * c1, __uint_as_float(v[k >> 4][(2 * k) & 31]), pr.x * c2);
+        const float d1 = fmaf(kp.y * c1, __uint_as_float(v[k >> 4][(2 * k + 1) & 31]), pr.y * c2);
+        pk[k] = pack_bf16(d0, d1);
+      }
+      mbar_wait(buf_free1, it & 1);
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        *tile_chunk(buf, r, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      fence_proxy_async();
+      named_bar_sync(1, 32 * kRowWarps);
+      if (leader) {
+        mbar_arrive(ds_full);
+        const int y = z * p.seq + i * kTile;
+        tma_store_2d(&tds, buf, kt * kTile, y);
+        tma_store_2d(&tds, buf + 16384, kt * kTile + 64, y);
+        bulk_commit();
+      }
+    }
+    // epilogue: rows r of this CTA's key tile, columns [hf*DH/2, +DH/2) of dV (x keep scale) and dK
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    __nv_bfloat16* base = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + kt * kTile + r) * p.ld_out;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      __nv_bfloat16* dst = base + (which ? p.k_col : p.v_col) + jl * DH + hf * (DH / 2);
+      const uint32_t tc = (which ? t_dk : t_dv) + hf * (DH / 2);
+      const float sc = which ? 1.f : p.ks;
+#pragma unroll
+      for (int c = 0; c < DH / 64; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tl + tc + c * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float* f = reinterpret_cast<const float*>(o + 8 * k);
+          *reinterpret_cast<uint4*>(dst + c * 32 + k * 8) =
+              make_uint4(pack_bf16(f[0] * sc, f[1] * sc), pack_bf16(f[2] * sc, f[3] * sc),
+                         pack_bf16(f[4] * sc, f[5] * sc), pack_bf16(f[6] * sc, f[7] * sc));
+        }
+      }
+    }
+    if (leader) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+bool fill_common(AttnParams& p, const oases_attn_desc& d, std::string* err) {
+  if (d.head_dim != 64 && d.head_dim != 128) {
+    *err = "attention: head_dim must be 64 or 128";
+    return false;
+  }
+  if (d.seq <= 0 || d.seq % kTile) {
+    *err = "attention: seq must be a positive multiple of 128";
+    return false;
+  }
+  if (d.samples <= 0 || d.heads_local <= 0 || d.heads_total < d.heads_local || d.head_offset < 0 ||
+      d.head_offset + d.heads_local > d.heads_total) {
+    *err = "attention: bad head / sample counts";
+    return false;
+  }
+  const long long hd = static_cast<long long>(d.heads_local) * d.head_dim;
+  if (d.ld_qkv < 3 * hd || d.ld_qkv % 8 || d.ld_out < hd || d.ld_out % 8) {
+    *err = "attention: qkv rows need >= 3*heads*head_dim columns, ctx rows >= heads*head_dim (ld % 8 == 0)";
+    return false;
+  }
+  p.seq = d.seq;
+  p.hl = d.heads_local;
+  p.hg = d.heads_total;
+  p.hoff = d.head_offset;
+  p.Z = d.samples * d.heads_local;
+  p.nq = d.seq / kTile;
+  p.q_col = 0;
+  p.k_col = static_cast<int>(hd);
+  p.v_col = static_cast<int>(2 * hd);
+  p.do_col = 0;
+  p.sl2 = d.scale * kLog2e;
+  p.scale = d.scale;
+  p.thr = dropout_threshold(d.dropout_p);
+  p.ks = dropout_keep_scale(d.dropout_p);
+  p.seed = d.seed;
+  p.offset = d.offset;
+  return true;
+}
+
+}  // namespace
+
+bool attention_supported(int dtype, int head_dim, int seq) {
+  return dtype == OASES_BF16 && (head_dim == 64 || head_dim == 128) && seq > 0 && seq % kTile == 0;
+}
+
+size_t attention_bwd_workspace(const oases_attn_desc& d) {
+  return static_cast<size_t>(d.samples) * d.heads_local * d.seq * sizeof(float);
+}
+
+GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
+  GemmStatus st;
+  AttnParams p{};
+  if (d.dtype != OASES_BF16) {
+    st.err = "attention: fused kernels are bf16-only";
+    return st;
+  }
+  if (!fill_common(p, d, &st.err)) return st;
+  if (!d.qkv || !d.out || !d.lse) {
+    st.err = "attention_fwd: null qkv / out / lse";
+    return st;
+  }
+  const long long rows = static_cast<long long>(d.samples) * d.seq;
+  CUtensorMap tqkv;
+  if (!make_tma_bf16_2d(&tqkv, d.qkv, rows, 3LL * d.heads_local * d.head_dim, d.ld_qkv, 64, kTile, &st.err))
+    return st;
+  p.out = d.out;
+  p.ld_out = d.ld_out;
+  p.lse = d.lse;
+  const unsigned grid = static_cast<unsigned>(p.Z * p.nq);
+  cudaError_t e;
+  if (d.head_dim == 128) {
+    static cudaError_t once = set_smem(attn_fwd_kernel<128>, FwdCfg<128>::SMEM);
+    if ((e = once) == cudaSuccess) {
+      attn_fwd_kernel<128><<<grid, kThreads, FwdCfg<128>::SMEM, stream>>>(tqkv, p);
+      e = cudaGetLastError();
+    }
+  } else {
+    static cudaError_t once = set_smem(attn_fwd_kernel<64>, FwdCfg<64>::SMEM);
+    if ((e = once) == cudaSuccess) {
+      attn_fwd_kernel<64><<<grid, kThreads, FwdCfg<64>::SMEM, stream>>>(tqkv, p);
+      e = cudaGetLastError();
+    }
+  }
+  if (e != cudaSuccess) {
+    st.err = std::string("attention_fwd launch: ") + cudaGetErrorString(e);
+    st.cuda = true;
+    return st;
+  }
+  st.ok = true;
+  return st;
+}
+
+GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream) {
+  GemmStatus st;
+  AttnParams p{};
+  if (d.dtype != OASES_BF16) {
+    st.err = "attention: fused kernels are bf16-only";
+    return st;
+  }
+  if (!fill_common(p, d, &st.err)) return st;
+  if (!d.qkv || !d.out || !d.lse || !d.dout || !d.dqkv || !d.ds || !d.workspace) {
+    st.err = "attention_bwd: null qkv / out / lse / dout / dqkv / ds / workspace";
+    return st;
+  }
+  if (d.ld_dout < static_cast<long long>(d.heads_local) * d.head_dim || d.ld_dout % 8 || d.ld_dqkv % 8 ||
+      d.ld_dqkv < 3LL * d.heads_local * d.head_dim) {
+    st.err = "attention_bwd: bad dout / dqkv leading dimensions";
+    return st;
+  }
+  const long long rows = static_cast<long long>(d.samples) * d.seq;
+  const long long hd = static_cast<long long>(d.heads_local) * d.head_dim;
+  CUtensorMap tqkv, tdo, tds;
+  if (!make_tma_bf16_2d(&tqkv, d.qkv, rows, 3 * hd, d.ld_qkv, 64, kTile, &st.err)) return st;
+  if (!make_tma_bf16_2d(&tdo, d.dout, rows, hd, d.ld_dout, 64, kTile, &st.err)) return st;
+  if (!make_tma_bf16_2d(&tds, d.ds, static_cast<long long>(p.Z) * d.seq, d.seq, d.seq, 64, kTile, &st.err))
+    return st;
+  float* dsum = static_cast<float*>(d.workspace);
+  // D = rowsum(dO o O) (ld of out must equal ld of dout for the shared row walk)
+  if (d.ld_out != d.ld_dout) {
+    st.err = "attention_bwd: out and dout must share a leading dimension";
+    return st;
+  }
+  const long long drows = static_cast<long long>(p.Z) * d.seq;
+  const unsigned dgrid = static_cast<unsigned>((drows + 7) / 8);
+  if (d.head_dim == 128)
+    attn_dsum_kernel<128><<<dgrid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(d.dout),
+                                                      static_cast<const __nv_bfloat16*>(d.out), d.ld_dout, dsum,
+                                                      d.seq, d.heads_local, 0, drows);
+  else
+    attn_dsum_kernel<64><<<dgrid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(d.dout),
+                                                     static_cast<const __nv_bfloat16*>(d.out), d.ld_dout, dsum,
+                                                     d.seq, d.heads_local, 0, drows);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    p.out = d.dqkv;
+    p.ld_out = d.ld_dqkv;
+    p.lse = const_cast<float*>(d.lse);
+    p.dsum = dsum;
+    const unsigned grid = static_cast<unsigned>(p.Z * p.nq);
+    if (d.head_dim == 128) {
+      static cudaError_t once = set_smem(attn_dkdv_kernel<128>, BwdCfg<128>::SMEM);
+      if ((e = once) == cudaSuccess) {
+        attn_dkdv_kernel<128><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tqkv, tdo, tds, p);
+        e = cudaGetLastError();
+      }
+    } else {
+      static cudaError_t once = set_smem(attn_dkdv_kernel<64>, BwdCfg<64>::SMEM);
+      if ((e = once) == cudaSuccess) {
+        attn_dkdv_kernel<64><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tqkv, tdo, tds, p);
+        e = cudaGetLastError();
+      }
+    }
+  }
+  if (e != cudaSuccess) {
+    st.err = std::string("attention_bwd launch: ") + cudaGetErrorString(e);
+    st.cuda = true;
+    return st;
+  }
+  // dQ = dS K per (sample, head): causal K range, deterministic tcgen05 GEMM.
+  oases_gemm_desc g{};
+  g.dtype = OASES_BF16;
+  g.c_dtype = OASES_BF16;
+  g.M = d.seq;
+  g.N = d.head_dim;
+  g.K = d.seq;
+  g.batch = p.Z;
+  g.batch_inner = d.heads_local;
+  g.a = oases_gemm_operand{d.ds, static_cast<long long>(p.Z) * d.seq, d.seq, d.seq, 0, 0,
+                           {static_cast<long long>(d.heads_local) * d.seq, d.seq}, {0, 0}};
+  g.b = oases_gemm_operand{static_cast<const char*>(d.qkv) + hd * 2, rows, 2 * hd, d.ld_qkv, 1, 0,
+                           {d.seq, 0}, {0, d.head_dim}};
+  g.c = d.dqkv;
+  g.ldc = d.ld_dqkv;
+  g.c_row_off[0] = d.seq;
+  g.c_col_off[1] = d.head_dim;
+  g.alpha = 1.f;
+  g.causal = OASES_CAUSAL_K_UPTO_M;
+  g.max_ctas = d.max_ctas;
+  return gemm_tc(g, stream);
+}
+
+}  // namespace oases

@@ -97,6 +97,29 @@ template <typename T>
 __device__ __forceinline__ void vstore(T* p, const float (&v)[Vec<T>::N]) {
   *reinterpret_cast<typename Vec<T>::raw*>(p) = Vec<T>::pack(v);
 }
+// 16 consecutive elements (one Philox dropout counter) as 16-byte vectors.
+template <typename T>
+__device__ __forceinline__ void load16(const T* p, float (&v)[16]) {
+  constexpr int V = Vec<T>::N;
+#pragma unroll
+  for (int k = 0; k < 16 / V; ++k) {
+    float t[V];
+    vload(p + k * V, t);
+#pragma unroll
+    for (int e = 0; e < V; ++e) v[k * V + e] = t[e];
+  }
+}
+template <typename T>
+__device__ __forceinline__ void store16(T* p, const float (&v)[16]) {
+  constexpr int V = Vec<T>::N;
+#pragma unroll
+  for (int k = 0; k < 16 / V; ++k) {
+    float t[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) t[e] = v[k * V + e];
+    vstore(p + k * V, t);
+  }
+}
 
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based RNG: the dropout mask of element i under key (seed, offset) is a
@@ -153,6 +176,14 @@ __device__ __forceinline__ void apply_dropout(float (&v)[V], unsigned long long 
   const unsigned b0 = static_cast<unsigned>(e & 15);
 #pragma unroll
   for (int q = 0; q < V; ++q) v[q] = keep_byte(u, b0 + q, thr) ? v[q] * ks : 0.f;
+}
+// Keep-mask of the 16 elements [e, e+16) (e % 16 == 0): one Philox call.
+__device__ __forceinline__ void apply_dropout16(float (&v)[16], unsigned long long e, uint64_t seed, uint64_t offset,
+                                                uint32_t thr, float ks) {
+  uint32_t u[4];
+  Philox::gen(seed, offset, e >> 4, u);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = keep_byte(u, q, thr) ? v[q] * ks : 0.f;
 }
 __device__ __forceinline__ float dropout_one(float v, unsigned long long e, uint64_t seed, uint64_t offset,
                                              uint32_t thr, float ks) {
@@ -246,6 +277,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 32 registers per thread -> 32 lanes x 32 consecutive f32 columns.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA store operands).
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// smem tile -> global through a tensor map (bulk async group of this thread).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// 1-D bulk copy global -> smem (16 B aligned, bytes % 16 == 0), completion counted on `bar`.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 // UMMA shared-memory descriptor (sm_100 "version 1"), SWIZZLE_128B.
 //   K-major tile: 8-row x 128 B atoms stacked every 1024 B (SBO); LBO unused.

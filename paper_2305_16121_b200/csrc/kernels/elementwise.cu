@@ -50,6 +50,42 @@ __global__ void __launch_bounds__(kThreads) bdr_fwd_vec_kernel(const T* __restri
   }
 }
 
+// 16 elements per thread (one Philox counter, 2-4 vectors); cols % 16 == 0 so
+// the 16 share one row. IDX = 32-bit indexing when n < 2^32.
+template <typename T, typename IDX>
+__global__ void __launch_bounds__(kThreads) bdr_fwd16_kernel(const T* __restrict__ x, const T* __restrict__ bias,
+                                                             const T* __restrict__ res, T* __restrict__ out, IDX n,
+                                                             IDX cols, uint32_t thr, float ks, int drop, uint64_t seed,
+                                                             uint64_t offset) {
+  const IDX stride = static_cast<IDX>(gridDim.x) * blockDim.x * 16;
+  for (IDX i = (static_cast<IDX>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; i < n; i += stride) {
+    float v[16];
+    load16(x + i, v);
+    if (res) {
+      float r[16];
+      load16(res + i, r);
+      if (bias) {
+        float b[16];
+        load16(bias + (i % cols), b);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] += b[q];
+      }
+      if (drop) apply_dropout16(v, static_cast<unsigned long long>(i), seed, offset, thr, ks);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] += r[q];
+    } else {
+      if (bias) {
+        float b[16];
+        load16(bias + (i % cols), b);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] += b[q];
+      }
+      if (drop) apply_dropout16(v, static_cast<unsigned long long>(i), seed, offset, thr, ks);
+    }
+    store16(out + i, v);
+  }
+}
+
 // scalar fallback for shapes that are not 16-byte multiples (toy checker sizes)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bdr_fwd_kernel(const T* __restrict__ x, const T* __restrict__ bias,
@@ -120,6 +156,82 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(const T* __restrict_
     s += v;
   }
   if (part) part[static_cast<long long>(blockIdx.y) * cols + c] = s;
+}
+
+// Column-pass tiling for 16-column lanes: a warp covers 512 columns (lane = 16
+// consecutive columns = one Philox counter), the 8 warps of a block split a
+// chunk of rows (4 rows in flight per warp), and the block's column partials
+// are reduced over its warps in a fixed order into part[chunk][col].
+template <typename T>
+__global__ void __launch_bounds__(kThreads) col_pass16_kernel(const T* __restrict__ in, T* __restrict__ dx,
+                                                              float* __restrict__ part, long long rows, int cols,
+                                                              int rows_per_chunk, uint32_t thr, float ks, int drop,
+                                                              uint64_t seed, uint64_t offset) {
+  __shared__ float sm[8][16][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 512 + lane * 16;
+  const long long r0 = static_cast<long long>(blockIdx.y) * rows_per_chunk;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  float s[16] = {};
+  if (c < cols) {
+    long long r = r0 + warp;
+    for (; r + 24 < r1; r += 32) {  // 4 rows in flight
+      float v[4][16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load16(in + (r + 8 * u) * cols + c, v[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long e = (r + 8 * u) * cols + c;
+        if (drop) apply_dropout16(v[u], static_cast<unsigned long long>(e), seed, offset, thr, ks);
+        if (dx) store16(dx + e, v[u]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s[q] += v[u][q];
+      }
+    }
+    for (; r < r1; r += 8) {
+      const long long e = r * cols + c;
+      float v[16];
+      load16(in + e, v);
+      if (drop) apply_dropout16(v, static_cast<unsigned long long>(e), seed, offset, thr, ks);
+      if (dx) store16(dx + e, v);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) s[q] += v[q];
+    }
+  }
+  if (!part) return;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) sm[warp][q][lane] = s[q];
+  __syncthreads();
+  // thread t finalises columns t and t + 256 of the block's 512
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = threadIdx.x + h * 256;  // column within the block
+    const int ln = j >> 4, q = j & 15;
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += sm[w][q][ln];
+    const int col = blockIdx.x * 512 + j;
+    if (col < cols) part[static_cast<long long>(blockIdx.y) * cols + col] = t;
+  }
+}
+
+// out[c] (+)= sum_k part[k][c] for k in chunk order; one thread per column,
+// 8 independent loads in flight (the summation order stays k = 0, 1, ...).
+__global__ void __launch_bounds__(kThreads) col_finalize_fast_kernel(const float* __restrict__ part, int chunks,
+                                                                     int cols, float* __restrict__ out, int acc) {
+  const int c = blockIdx.x * kThreads + threadIdx.x;
+  if (c >= cols) return;
+  float t = 0.f;
+  int k = 0;
+  for (; k + 8 <= chunks; k += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(part + static_cast<long long>(k + u) * cols + c);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += v[u];
+  }
+  for (; k < chunks; ++k) t += __ldg(part + static_cast<long long>(k) * cols + c);
+  out[c] = acc ? out[c] + t : t;
 }
 
 // out[c] (+)= sum_k part[k][c], fixed order: 8 interleaved partial sums per
@@ -253,11 +365,37 @@ ColSplit col_split(long long rows, int col_blocks) {
   return {static_cast<int>((rows + rpc - 1) / rpc), rpc};
 }
 
+// (512-column groups) x (row chunks) ~ 2 CTAs per SM, >= 32 rows per chunk
+ColSplit col_split16(long long rows, int cols) {
+  const int groups = (cols + 511) / 512;
+  long long chunks = (2LL * 148 + groups - 1) / groups;
+  const long long maxc = (rows + 31) / 32;
+  if (chunks > maxc) chunks = maxc;
+  if (chunks < 1) chunks = 1;
+  const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
+  return {static_cast<int>((rows + rpc - 1) / rpc), rpc};
+}
+
 template <typename T>
 bool vec_ok(const void* a, const void* b, long long n, int cols) {
   constexpr int V = 16 / sizeof(T);
   auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
   return n % V == 0 && cols % V == 0 && al(a) && al(b);
+}
+
+template <typename T>
+void bdr16(const T* X, const T* B, const T* R, T* O, long long n, int cols, uint32_t thr, float ks, int drop,
+           uint64_t seed, uint64_t offset, cudaStream_t st) {
+  long long g = (n / 16 + kThreads - 1) / kThreads;
+  if (g > 148LL * 8) g = 148LL * 8;
+  if (g < 1) g = 1;
+  if (n < (1LL << 31))  // 32-bit index arithmetic cannot wrap
+    bdr_fwd16_kernel<T, uint32_t><<<static_cast<unsigned>(g), kThreads, 0, st>>>(
+        X, B, R, O, static_cast<uint32_t>(n), static_cast<uint32_t>(cols), thr, ks, drop, seed, offset);
+  else
+    bdr_fwd16_kernel<T, unsigned long long><<<static_cast<unsigned>(g), kThreads, 0, st>>>(
+        X, B, R, O, static_cast<unsigned long long>(n), static_cast<unsigned long long>(cols), thr, ks, drop, seed,
+        offset);
 }
 
 }  // namespace
@@ -269,6 +407,7 @@ size_t colsum_workspace(long long rows, int cols) {
     const ColSplit s = col_split(rows, (cols + kThreads * v - 1) / (kThreads * v));
     if (s.chunks > chunks) chunks = s.chunks;
   }
+  if (col_split16(rows, cols).chunks > chunks) chunks = col_split16(rows, cols).chunks;
   return static_cast<size_t>(chunks) * cols * sizeof(float) + 256;
 }
 
@@ -285,7 +424,9 @@ cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias
     auto B = static_cast<const T*>(bias);
     auto R = static_cast<const T*>(res);
     auto O = static_cast<T*>(out);
-    if (vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
+    if (cols % 16 == 0 && vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
+      bdr16<T>(X, B, R, O, n, cols, thr, ks, drop, seed, offset, st);
+    else if (vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
       bdr_fwd_vec_kernel<T><<<grid_for(n, kThreads * 8), kThreads, 0, st>>>(X, B, R, O, n, cols, thr, ks, drop, seed,
                                                                           offset);
     else
@@ -297,7 +438,9 @@ cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias
     auto B = static_cast<const T*>(bias);
     auto R = static_cast<const T*>(res);
     auto O = static_cast<T*>(out);
-    if (vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
+    if (cols % 16 == 0 && vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
+      bdr16<T>(X, B, R, O, n, cols, thr, ks, drop, seed, offset, st);
+    else if (vec_ok<T>(x, out, n, cols) && vec_ok<T>(bias, res, n, cols))
       bdr_fwd_vec_kernel<T><<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(X, B, R, O, n, cols, thr, ks, drop, seed,
                                                                           offset);
     else
@@ -308,9 +451,17 @@ cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias
 }
 
 template <typename T>
-static void col_pass_t(const void* in, void* dx, float* part, long long rows, int cols, uint32_t thr, float ks,
+static bool col_pass_t(const void* in, void* dx, float* part, long long rows, int cols, uint32_t thr, float ks,
                        int drop, uint64_t seed, uint64_t offset, int* chunks_out, cudaStream_t st) {
   constexpr int V = 16 / sizeof(T);
+  if (cols % 16 == 0 && vec_ok<T>(in, dx, rows * cols, cols)) {
+    const ColSplit sp = col_split16(rows, cols);
+    col_pass16_kernel<T><<<dim3((cols + 511) / 512, sp.chunks), kThreads, 0, st>>>(
+        static_cast<const T*>(in), static_cast<T*>(dx), part, rows, cols, sp.rows_per_chunk, thr, ks, drop, seed,
+        offset);
+    *chunks_out = sp.chunks;
+    return true;
+  }
   if (vec_ok<T>(in, dx, rows * cols, cols)) {
     const int cb = (cols + kThreads * V - 1) / (kThreads * V);
     const ColSplit sp = col_split(rows, cb);
@@ -326,6 +477,7 @@ static void col_pass_t(const void* in, void* dx, float* part, long long rows, in
                                                                   offset);
     *chunks_out = sp.chunks;
   }
+  return false;
 }
 
 cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, void* ws, long long rows, int cols,
@@ -335,11 +487,17 @@ cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, v
   const uint32_t thr = dropout_threshold(p);
   const float ks = dropout_keep_scale(p);
   int chunks = 0;
+  bool fast;
   if (dtype == OASES_BF16)
-    col_pass_t<__nv_bfloat16>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
+    fast = col_pass_t<__nv_bfloat16>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
   else
-    col_pass_t<float>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
-  if (out) col_finalize_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
+    fast = col_pass_t<float>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
+  if (out) {
+    if (fast)
+      col_finalize_fast_kernel<<<(cols + kThreads - 1) / kThreads, kThreads, 0, st>>>(part, chunks, cols, out, acc);
+    else
+      col_finalize_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
+  }
   return cudaGetLastError();
 }
 

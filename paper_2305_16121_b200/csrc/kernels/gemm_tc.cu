@@ -601,23 +601,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 bool make_map(CUtensorMap* map, const oases_gemm_operand& o, uint32_t box_inner, uint32_t box_outer,
               std::string* err) {
-  auto enc = get_encode();
-  if (!enc) {
-    *err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 2};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(o.ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    *err = "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")";
-    return false;
-  }
-  return true;
+  return make_tma_bf16_2d(map, o.ptr, o.rows, o.cols, o.ld, box_inner, box_outer, err);
 }
 
 template <int BN, int A_MN, int B_MN>
@@ -687,6 +671,27 @@ int sm_count() {
 }
 
 }  // namespace
+
+bool make_tma_bf16_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, uint32_t box_inner,
+                      uint32_t box_outer, std::string* err) {
+  auto enc = get_encode();
+  if (!enc) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")";
+    return false;
+  }
+  return true;
+}
 
 GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
   GemmStatus st;

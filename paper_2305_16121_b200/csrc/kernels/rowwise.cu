@@ -228,6 +228,214 @@ __global__ void __launch_bounds__(256) ln_bwd_cached_kernel(const T* __restrict_
   }
 }
 
+// Block-per-row variants (256 threads, NVEC 16-byte vectors per thread, cols ==
+// 256 * V * NVEC): every thread holds a few vectors, so residency is high and
+// the loads of many rows are in flight at once. Statistics are exact two-pass
+// in f32 with fixed-order block reductions.
+template <int N>
+__device__ __forceinline__ void block_sum(float (&v)[N], float* sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < N; ++i) sm[warp * N + i] = v[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += sm[w * N + i];
+    v[i] = t;
+  }
+  __syncthreads();
+}
+
+template <typename T, int NVEC>
+__global__ void __launch_bounds__(256) ln_fwd_block_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
+                                                           const T* __restrict__ beta, T* __restrict__ y, int cols,
+                                                           float eps) {
+  constexpr int V = Vec<T>::N;
+  __shared__ float sm[16];
+  const long long off = static_cast<long long>(blockIdx.x) * cols;
+  float v[NVEC][V], g[NVEC][V], b[NVEC][V];
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t) {
+    const int c = (t * 256 + threadIdx.x) * V;
+    vload(x + off + c, v[t]);
+    vload(gamma + c, g[t]);
+    vload(beta + c, b[t]);
+  }
+  float s[1] = {0.f};
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t)
+#pragma unroll
+    for (int e = 0; e < V; ++e) s[0] += v[t][e];
+  block_sum<1>(s, sm);
+  const float mean = s[0] / static_cast<float>(cols);
+  float q[1] = {0.f};
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t)
+#pragma unroll
+    for (int e = 0; e < V; ++e) q[0] += (v[t][e] - mean) * (v[t][e] - mean);
+  block_sum<1>(q, sm);
+  const float rstd = rsqrtf(q[0] / static_cast<float>(cols) + eps);
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) v[t][e] = (v[t][e] - mean) * rstd * g[t][e] + b[t][e];
+    vstore(y + off + (t * 256 + threadIdx.x) * V, v[t]);
+  }
+}
+
+template <typename T, int NVEC>
+__global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
+                                                           const T* __restrict__ dy, T* __restrict__ dx, int acc,
+                                                           float2* __restrict__ stats, int cols, float eps) {
+  constexpr int V = Vec<T>::N;
+  __shared__ float sm[16];
+  const long long off = static_cast<long long>(blockIdx.x) * cols;
+  float xv[NVEC][V], gv[NVEC][V], o[NVEC][V];
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t) {
+    const int c = (t * 256 + threadIdx.x) * V;
+    float d[V], g[V];
+    vload(x + off + c, xv[t]);
+    vload(dy + off + c, d);
+    vload(gamma + c, g);
+    if (acc) vload(dx + off + c, o[t]);
+#pragma unroll
+    for (int e = 0; e < V; ++e) gv[t][e] = d[e] * g[e];
+  }
+  float s[1] = {0.f};
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t)
+#pragma unroll
+    for (int e = 0; e < V; ++e) s[0] += xv[t][e];
+  block_sum<1>(s, sm);
+  const float mean = s[0] / static_cast<float>(cols);
+  float q[1] = {0.f};
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t)
+#pragma unroll
+    for (int e = 0; e < V; ++e) q[0] += (xv[t][e] - mean) * (xv[t][e] - mean);
+  block_sum<1>(q, sm);
+  const float rstd = rsqrtf(q[0] / static_cast<float>(cols) + eps);
+  float s12[2] = {0.f, 0.f};
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t)
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      xv[t][e] = (xv[t][e] - mean) * rstd;  // xhat
+      s12[0] += gv[t][e];
+      s12[1] += gv[t][e] * xv[t][e];
+    }
+  block_sum<2>(s12, sm);
+  const float m1 = s12[0] / static_cast<float>(cols), m2 = s12[1] / static_cast<float>(cols);
+  if (threadIdx.x == 0) stats[blockIdx.x] = make_float2(mean, rstd);
+#pragma unroll
+  for (int t = 0; t < NVEC; ++t) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const float r = rstd * (gv[t][e] - m1 - xv[t][e] * m2);
+      o[t][e] = acc ? o[t][e] + r : r;
+    }
+    vstore(dx + off + (t * 256 + threadIdx.x) * V, o[t]);
+  }
+}
+
+// LN parameter-gradient partials with 16-column lanes (512 columns per warp,
+// 8 warps splitting a chunk of rows, 4 rows in flight per warp):
+// part[chunk][0][c] = sum dy * xhat, part[chunk][1][c] = sum dy.
+template <typename T>
+__global__ void __launch_bounds__(256) ln_param16_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                                         const float2* __restrict__ stats, float* __restrict__ part,
+                                                         long long rows, int cols, int rows_per_chunk) {
+  __shared__ float sm[8][16][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 512 + lane * 16;
+  const long long r0 = static_cast<long long>(blockIdx.y) * rows_per_chunk;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  float sg[16] = {}, sb[16] = {};
+  if (c < cols) {
+    long long r = r0 + warp;
+    for (; r + 8 < r1; r += 16) {  // 2 rows in flight
+      float d[2][16], xv[2][16];
+      float2 st[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        load16(dy + (r + 8 * u) * cols + c, d[u]);
+        load16(x + (r + 8 * u) * cols + c, xv[u]);
+        st[u] = stats[r + 8 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          sg[e] += d[u][e] * (xv[u][e] - st[u].x) * st[u].y;
+          sb[e] += d[u][e];
+        }
+    }
+    for (; r < r1; r += 8) {
+      float d[16], xv[16];
+      load16(dy + r * cols + c, d);
+      load16(x + r * cols + c, xv);
+      const float2 st = stats[r];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        sg[e] += d[e] * (xv[e] - st.x) * st.y;
+        sb[e] += d[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int which = 0; which < 2; ++which) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sm[warp][q][lane] = which ? sb[q] : sg[q];
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = threadIdx.x + h * 256;
+      const int ln = j >> 4, q = j & 15;
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += sm[w][q][ln];
+      const int col = blockIdx.x * 512 + j;
+      if (col < cols) part[(static_cast<long long>(blockIdx.y) * 2 + which) * cols + col] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// out0/out1[c] (+)= sum_k part[k][0/1][c] in chunk order, 8 loads in flight.
+__global__ void __launch_bounds__(256) colpair_finalize_fast_kernel(const float* __restrict__ part, int chunks,
+                                                                    int cols, float* __restrict__ out0,
+                                                                    float* __restrict__ out1, int acc) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  float ta = 0.f, tb = 0.f;
+  int k = 0;
+  for (; k + 4 <= chunks; k += 4) {
+    float a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = __ldg(part + (static_cast<long long>(k + u) * 2 + 0) * cols + c);
+      b[u] = __ldg(part + (static_cast<long long>(k + u) * 2 + 1) * cols + c);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ta += a[u];
+      tb += b[u];
+    }
+  }
+  for (; k < chunks; ++k) {
+    ta += __ldg(part + (static_cast<long long>(k) * 2 + 0) * cols + c);
+    tb += __ldg(part + (static_cast<long long>(k) * 2 + 1) * cols + c);
+  }
+  if (out0) out0[c] = acc ? out0[c] + ta : ta;
+  if (out1) out1[c] = acc ? out1[c] + tb : tb;
+}
+
 // Column partial sums over a chunk of rows: part[chunk][0][c] = sum dy*xhat,
 // part[chunk][1][c] = sum dy. Each thread owns V consecutive columns.
 template <typename T>
@@ -478,6 +686,26 @@ ParamSplit param_split(long long rows, int cols) {
   return {cb, static_cast<int>((rows + rpc - 1) / rpc), rpc};
 }
 
+// (512-column groups) x (row chunks) ~ 2 CTAs per SM, >= 32 rows per chunk
+ParamSplit param_split16(long long rows, int cols) {
+  const int groups = (cols + 511) / 512;
+  long long chunks = (2LL * 148 + groups - 1) / groups;
+  const long long maxc = (rows + 31) / 32;
+  if (chunks > maxc) chunks = maxc;
+  if (chunks < 1) chunks = 1;
+  const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
+  return {groups, static_cast<int>((rows + rpc - 1) / rpc), rpc};
+}
+
+// NVEC for the block-per-row kernels (0 = not applicable)
+template <typename T>
+int block_nvec(int cols) {
+  constexpr int V = Vec<T>::N;
+  if (cols % (256 * V)) return 0;
+  const int n = cols / (256 * V);
+  return (n == 1 || n == 2 || n == 4) ? n : 0;
+}
+
 template <typename T>
 cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx, int acc_dx, float* dgamma,
                      float* dbeta, int acc_params, void* workspace, long long rows, int cols, float eps,
@@ -490,17 +718,31 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   auto G = static_cast<const T*>(gamma);
   auto DX = static_cast<T*>(dx);
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
-  if (cols <= 16 * 32 * Vec<T>::N) {
+  const int nvec = block_nvec<T>(cols);
+  if (nvec && rows < (1LL << 31)) {
+    const unsigned g = static_cast<unsigned>(rows);
+    if (nvec == 1) ln_bwd_block_kernel<T, 1><<<g, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, cols, eps);
+    else if (nvec == 2) ln_bwd_block_kernel<T, 2><<<g, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, cols, eps);
+    else ln_bwd_block_kernel<T, 4><<<g, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, cols, eps);
+  } else if (cols <= 16 * 32 * Vec<T>::N) {
     const cudaError_t e = launch_rows_nv<T, LnBwdL>(cols, rows, st, X, G, DY, DX, acc_dx, stats, rows, cols, eps);
     if (e != cudaSuccess) return e;
   } else {
     ln_bwd_kernel<T><<<grid, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows, cols, eps);
   }
   if (dgamma || dbeta) {
-    const ParamSplit sp = param_split<T>(rows, cols);
-    ln_param_partial_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
-                                                                               sp.rows_per_chunk);
-    colpair_finalize_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta, acc_params);
+    if (cols % 16 == 0) {
+      const ParamSplit sp = param_split16(rows, cols);
+      ln_param16_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
+                                                                         sp.rows_per_chunk);
+      colpair_finalize_fast_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta,
+                                                                       acc_params);
+    } else {
+      const ParamSplit sp = param_split<T>(rows, cols);
+      ln_param_partial_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
+                                                                                 sp.rows_per_chunk);
+      colpair_finalize_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta, acc_params);
+    }
   }
   return cudaGetLastError();
 }
@@ -512,6 +754,14 @@ cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y
   auto G = static_cast<const T*>(gamma);
   auto B = static_cast<const T*>(beta);
   auto Y = static_cast<T*>(y);
+  const int nvec = block_nvec<T>(cols);
+  if (nvec && rows < (1LL << 31)) {
+    const unsigned g = static_cast<unsigned>(rows);
+    if (nvec == 1) ln_fwd_block_kernel<T, 1><<<g, 256, 0, st>>>(X, G, B, Y, cols, eps);
+    else if (nvec == 2) ln_fwd_block_kernel<T, 2><<<g, 256, 0, st>>>(X, G, B, Y, cols, eps);
+    else ln_fwd_block_kernel<T, 4><<<g, 256, 0, st>>>(X, G, B, Y, cols, eps);
+    return cudaGetLastError();
+  }
   if (cols <= 16 * 32 * Vec<T>::N) return launch_rows_nv<T, LnFwdL>(cols, rows, st, X, G, B, Y, rows, cols, eps);
   ln_fwd_kernel<T><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(X, G, B, Y, rows, cols, eps);
   return cudaGetLastError();
@@ -521,7 +771,8 @@ cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y
 
 size_t layernorm_bwd_workspace(long long rows, int cols) {
   const ParamSplit a = param_split<float>(rows, cols), b = param_split<__nv_bfloat16>(rows, cols);
-  const int chunks = a.chunks > b.chunks ? a.chunks : b.chunks;
+  int chunks = a.chunks > b.chunks ? a.chunks : b.chunks;
+  if (param_split16(rows, cols).chunks > chunks) chunks = param_split16(rows, cols).chunks;
   return ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)) +
          static_cast<size_t>(chunks) * 2 * cols * sizeof(float) + 256;
 }

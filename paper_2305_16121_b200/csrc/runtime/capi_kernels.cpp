@@ -67,6 +67,38 @@ oases_status oases_gemm(const oases_gemm_desc* d, void* stream) {
   });
 }
 
+namespace {
+void gemm_status_throw(const oases::GemmStatus& st) {
+  if (st.ok) return;
+  if (st.cuda) throw oases::CudaError(st.err);
+  throw tmpsim::ConfigError(st.err);
+}
+}  // namespace
+
+int32_t oases_attention_supported(int dtype, int32_t head_dim, int32_t seq) {
+  return oases::attention_supported(dtype, head_dim, seq) ? 1 : 0;
+}
+
+oases_status oases_attention_fwd(const oases_attn_desc* d, void* stream) {
+  return guarded([&] {
+    if (!d) throw tmpsim::ConfigError("oases_attention_fwd: null descriptor");
+    need_device();
+    gemm_status_throw(oases::attention_fwd(*d, S(stream)));
+  });
+}
+
+size_t oases_attention_bwd_workspace(const oases_attn_desc* d) {
+  return d ? oases::attention_bwd_workspace(*d) : 0;
+}
+
+oases_status oases_attention_bwd(const oases_attn_desc* d, void* stream) {
+  return guarded([&] {
+    if (!d) throw tmpsim::ConfigError("oases_attention_bwd: null descriptor");
+    need_device();
+    gemm_status_throw(oases::attention_bwd(*d, S(stream)));
+  });
+}
+
 oases_status oases_layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y,
                                  int64_t rows, int64_t cols, float eps, void* stream) {
   return guarded([&] {

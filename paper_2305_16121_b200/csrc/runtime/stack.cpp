@@ -21,6 +21,7 @@
 #include "stack.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -149,6 +150,11 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
     if (cfg.attention && (cfg.s % 128 || dh_ % 64 || nrow_attn_ % 64))
       throw ConfigError("stack: bf16 attention needs seq % 128 == 0 and head dim % 64 == 0");
   }
+  // Fused tcgen05 attention unless OASES_FUSED_ATTN=0 (A/B runs of the unfused chain).
+  {
+    const char* e = std::getenv("OASES_FUSED_ATTN");
+    fused_attn_ = cfg.attention && attention_supported(dtype(), dh_, static_cast<int>(cfg.s)) && !(e && e[0] == '0');
+  }
   const int W = ctx.local_workers;
   workers_.resize(static_cast<size_t>(W));
   for (int w = 0; w < W; ++w) workers_[static_cast<size_t>(w)].rank = W > 1 ? w : ctx.rank;
@@ -237,7 +243,9 @@ void Stack::alloc_all() {
         ws.ln = cfg_.ln ? arena_.alloc(static_cast<size_t>(Ts * h) * es) : nullptr;
         ws.col = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
         ws.act = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
-        if (prob) {
+        if (prob && fused_attn_) {
+          ws.lse = static_cast<float*>(arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float)));
+        } else if (prob) {
           ws.p = arena_.alloc(static_cast<size_t>(prob) * es);
           ws.pd = cfg_.p_attn > 0.f ? arena_.alloc(static_cast<size_t>(prob) * es) : ws.p;
         }
@@ -247,6 +255,7 @@ void Stack::alloc_all() {
     w.du = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
     w.dcol = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
     if (prob) w.dp = arena_.alloc(static_cast<size_t>(prob) * es);
+    if (prob && fused_attn_) w.attn_ws = arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float));
     w.y = arena_.alloc(static_cast<size_t>(Ts * h) * es);
     w.ln_ws = arena_.alloc(layernorm_bwd_workspace(Ts, static_cast<int>(h)));
     w.col_ws = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
@@ -450,11 +459,49 @@ double Stack::read_loss() {
 }
 
 // ------------------------------------------------------------------ attention
+oases_attn_desc Stack::attn_desc(Worker& w, int block, int sb, const Workspace& ws) {
+  oases_attn_desc a{};
+  a.dtype = dtype();
+  a.samples = static_cast<int>(cfg_.b / 2);
+  a.heads_local = hl_;
+  a.heads_total = static_cast<int>(cfg_.heads);
+  a.head_offset = w.rank * hl_;
+  a.head_dim = dh_;
+  a.seq = static_cast<int>(cfg_.s);
+  a.max_ctas = ctx_.gemm_max_ctas;
+  a.qkv = ws.col;
+  a.ld_qkv = ncol_attn_;
+  a.out = ws.act;
+  a.ld_out = nrow_attn_;
+  a.lse = ws.lse;
+  a.dout = w.du;
+  a.ld_dout = nrow_attn_;
+  a.dqkv = w.dcol;
+  a.ld_dqkv = ncol_attn_;
+  a.ds = w.dp;
+  a.workspace = w.attn_ws;
+  a.scale = 1.f / std::sqrt(static_cast<float>(dh_));
+  a.dropout_p = cfg_.p_attn;
+  a.seed = cfg_.seed;
+  a.offset = drop_offset(block, sb, 1);
+  return a;
+}
+
 void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws) {
   const int64_t s = cfg_.s, Ts = tokens_sub(), bh = cfg_.b / 2, Z = bh * hl_, nc = ncol_attn_, nr = nrow_attn_;
   const int64_t hd = static_cast<int64_t>(hl_) * dh_;
   const char* qkv = static_cast<const char*>(ws.col);
   const size_t es = esize();
+  if (fused_attn_) {
+    const oases_attn_desc a = attn_desc(w, block, sb, ws);
+    const GemmStatus st = oases::attention_fwd(a, ctx_.compute);
+    if (!st.ok) {
+      if (st.cuda) throw CudaError(st.err);
+      throw ConfigError(st.err);
+    }
+    ++launches_;
+    return;
+  }
   oases_gemm_desc d{};
   // S = Q K^T per (sample, head); tiles above the diagonal are skipped.
   d = oases_gemm_desc{};
@@ -489,6 +536,16 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   const size_t es = esize();
   const char* qkv = static_cast<const char*>(ws.col);
   char* dqkv = static_cast<char*>(w.dcol);
+  if (fused_attn_) {
+    const oases_attn_desc a = attn_desc(w, block, sb, ws);
+    const GemmStatus st = oases::attention_bwd(a, ctx_.compute);
+    if (!st.ok) {
+      if (st.cuda) throw CudaError(st.err);
+      throw ConfigError(st.err);
+    }
+    launches_ += 3;  // rowsum(dO o O), dK/dV kernel, dQ GEMM
+    return;
+  }
   oases_gemm_desc d{};
   // dP_drop = dctx V^T
   d.c_dtype = dtype();

@@ -70,6 +70,7 @@ struct Workspace {
   void* act = nullptr;  // [T_sub, nrow]  ctx | gelu(pre)
   void* p = nullptr;    // [bh*Hl*s, s]   S then P (in place)
   void* pd = nullptr;   // dropped P (== p when attention dropout is 0)
+  float* lse = nullptr; // [bh*Hl*s] row log-sum-exp of the fused attention (log2 domain)
 };
 
 struct Worker {
@@ -85,7 +86,8 @@ struct Worker {
   void* gar = nullptr;   // [T_sub, h]  dropout'(g)
   void* du = nullptr;    // [T_sub, nmax] d(row GEMM input)
   void* dcol = nullptr;  // [T_sub, ncol_max]
-  void* dp = nullptr;    // [bh*Hl*s, s]  dP_drop then dS
+  void* dp = nullptr;    // [bh*Hl*s, s]  dP_drop then dS (fused attention: dS only)
+  void* attn_ws = nullptr;  // fused attention backward workspace (rowsum(dO o O))
   void* y = nullptr;     // [T_sub, h] final output for the loss head
   void* ln_ws = nullptr;
   void* col_ws = nullptr;
@@ -139,6 +141,7 @@ class Stack {
   void alloc_all();
   void gemm(const oases_gemm_desc& d);
   void ln_fwd(const void* x, const void* g, const void* b, void* y);
+  oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);
   void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
   Workspace& ws_for(Worker& w, int block, int sb);
@@ -150,6 +153,7 @@ class Stack {
   DeviceArena arena_;
   std::vector<Worker> workers_;
   int nblocks_ = 0;
+  bool fused_attn_ = false;  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;

@@ -86,6 +86,46 @@ def layernorm_bwd(x, gamma, dy, dx, dgamma, dbeta, accumulate_dx=False, acc_para
                                          _stream(stream)))
 
 
+def attention_supported(dtype: torch.dtype, head_dim: int, seq: int) -> bool:
+    return bool(capi.lib().oases_attention_supported(_dtype(torch.empty(0, dtype=dtype)), head_dim, seq))
+
+
+def _attn_desc(qkv, samples, heads, head_dim, seq, scale, dropout_p, seed, offset, heads_total, head_offset):
+    d = capi.AttnDesc()
+    d.dtype = _dtype(qkv)
+    d.samples, d.heads_local, d.head_dim, d.seq = samples, heads, head_dim, seq
+    d.heads_total = heads_total or heads
+    d.head_offset = head_offset
+    d.qkv, d.ld_qkv = _ptr(qkv), qkv.stride(0)
+    d.scale, d.dropout_p, d.seed, d.offset = scale, dropout_p, seed, offset
+    return d
+
+
+def attention_fwd(qkv, out, lse, samples, heads, head_dim, seq, scale, dropout_p=0.0, seed=0, offset=0,
+                  heads_total=0, head_offset=0, stream=None):
+    """Fused causal attention: qkv [samples*seq, >=3*heads*head_dim] (Q|K|V blocks) -> out (ctx), lse (f32)."""
+    d = _attn_desc(qkv, samples, heads, head_dim, seq, scale, dropout_p, seed, offset, heads_total, head_offset)
+    d.out, d.ld_out, d.lse = _ptr(out), out.stride(0), _ptr(lse)
+    check(capi.lib().oases_attention_fwd(C.byref(d), _stream(stream)))
+
+
+def attention_bwd(qkv, out, lse, dout, dqkv, samples, heads, head_dim, seq, scale, dropout_p=0.0, seed=0, offset=0,
+                  heads_total=0, head_offset=0, ds=None, stream=None):
+    """Backward of attention_fwd: writes dQ | dK | dV into dqkv (dS scratch allocated when not given)."""
+    d = _attn_desc(qkv, samples, heads, head_dim, seq, scale, dropout_p, seed, offset, heads_total, head_offset)
+    d.out, d.ld_out, d.lse = _ptr(out), out.stride(0), _ptr(lse)
+    d.dout, d.ld_dout = _ptr(dout), dout.stride(0)
+    d.dqkv, d.ld_dqkv = _ptr(dqkv), dqkv.stride(0)
+    if ds is None:
+        ds = torch.empty(samples * heads * seq, seq, dtype=qkv.dtype, device=qkv.device)
+    d.ds = _ptr(ds)
+    ws = torch.empty(capi.lib().oases_attention_bwd_workspace(C.byref(d)) // 4 + 4, dtype=torch.float32,
+                     device=qkv.device)
+    d.workspace = _ptr(ws)
+    check(capi.lib().oases_attention_bwd(C.byref(d), _stream(stream)))
+    return ds
+
+
 def softmax_fwd(s, p, p_drop, batch, seq, scale, dropout_p=0.0, seed=0, offset=0, heads_local=1, heads_total=1,
                 head_offset=0, stream=None):
     check(capi.lib().oases_softmax_fwd(_dtype(s), _ptr(s), _ptr(p), _ptr(p_drop), batch, seq, scale, dropout_p, seed,
