@@ -227,7 +227,9 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
             st_vec<OutT, E>(reinterpret_cast<OutT*>(p.c2) + rel, v);
           }
         } else {
-          for (int i = 0; i < valid; ++i) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) {  // compile-time indices keep v[] in registers
+            if (i >= valid) break;
             float x = v[i];
             if constexpr (EPI == OASES_EPI_DGELU)
               x *= gelu_grad_f(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
