@@ -365,32 +365,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// D[z, i] = sum_d dO[i, d] * O[i, d] (head z's columns); one warp per row.
+// D[z, i] = sum_d dO[i, d] * O[i, d] (head z's columns); DH/8 threads per row,
+// one 16-byte vector of each operand per thread.
 template <int DH>
 __global__ void __launch_bounds__(256) attn_dsum_kernel(const __nv_bfloat16* __restrict__ dout,
                                                         const __nv_bfloat16* __restrict__ out, long long ld,
                                                         float* __restrict__ dsum, int seq, int hl, int col0,
                                                         long long rows) {
-  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int lane = threadIdx.x & 31;
-  const long long per = static_cast<long long>(hl) * seq;
-  const int n = static_cast<int>(row / per);
-  const int rem = static_cast<int>(row - n * per);
-  const int jl = rem / seq, i = rem - jl * seq;
-  const long long off = static_cast<long long>(n * seq + i) * ld + col0 + jl * DH;
+  constexpr int TPR = DH / 8;  // threads per row (power of two <= 32)
+  const long long row = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) / TPR;
+  const int sub = threadIdx.x % TPR;
   float acc = 0.f;
-  for (int d = lane * 4; d < DH; d += 128) {
-    const uint2 a = *reinterpret_cast<const uint2*>(dout + off + d);
-    const uint2 b = *reinterpret_cast<const uint2*>(out + off + d);
-    const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.x));
-    const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.y));
-    const float2 b0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b.x));
-    const float2 b1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b.y));
-    acc += a0.x * b0.x + a0.y * b0.y + a1.x * b1.x + a1.y * b1.y;
+  if (row < rows) {
+    const long long per = static_cast<long long>(hl) * seq;
+    const int n = static_cast<int>(row / per);
+    const int rem = static_cast<int>(row - n * per);
+    const int jl = rem / seq, i = rem - jl * seq;
+    const long long off = static_cast<long long>(n * seq + i) * ld + col0 + jl * DH + sub * 8;
+    float a[8], b[8];
+    vload(dout + off, a);
+    vload(out + off, b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += a[e] * b[e];
   }
-  acc = warp_sum(acc);
-  if (lane == 0) dsum[row] = acc;
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (row < rows && sub == 0) dsum[row] = acc;
 }
 
 template <int DH>
@@ -804,7 +804,7 @@ GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream) {
     return st;
   }
   const long long drows = static_cast<long long>(p.Z) * d.seq;
-  const unsigned dgrid = static_cast<unsigned>((drows + 7) / 8);
+  const unsigned dgrid = static_cast<unsigned>((drows * (d.head_dim / 8) + 255) / 256);
   if (d.head_dim == 128)
     attn_dsum_kernel<128><<<dgrid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(d.dout),
                                                       static_cast<const __nv_bfloat16*>(d.out), d.ld_dout, dsum,

@@ -215,23 +215,35 @@ __global__ void __launch_bounds__(kThreads) col_pass16_kernel(const T* __restric
   }
 }
 
-// out[c] (+)= sum_k part[k][c] for k in chunk order; one thread per column,
-// 8 independent loads in flight (the summation order stays k = 0, 1, ...).
+// out[c] (+)= sum_k part[k][c]: a block covers 32 columns x 8 chunk lanes; lane
+// group g sums chunks g, g+8, ... (4 loads in flight), then the 8 group sums
+// are combined in g order -- a fixed summation order, so results are
+// bit-reproducible.
 __global__ void __launch_bounds__(kThreads) col_finalize_fast_kernel(const float* __restrict__ part, int chunks,
                                                                      int cols, float* __restrict__ out, int acc) {
-  const int c = blockIdx.x * kThreads + threadIdx.x;
-  if (c >= cols) return;
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float t = 0.f;
-  int k = 0;
-  for (; k + 8 <= chunks; k += 8) {
-    float v[8];
+  if (c < cols) {
+    int k = g;
+    for (; k + 24 < chunks; k += 32) {
+      float v[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(part + static_cast<long long>(k + u) * cols + c);
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(part + static_cast<long long>(k + 8 * u) * cols + c);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t += v[u];
+      for (int u = 0; u < 4; ++u) t += v[u];
+    }
+    for (; k < chunks; k += 8) t += __ldg(part + static_cast<long long>(k) * cols + c);
   }
-  for (; k < chunks; ++k) t += __ldg(part + static_cast<long long>(k) * cols + c);
-  out[c] = acc ? out[c] + t : t;
+  sm[g][lane] = t;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += sm[j][lane];
+    out[c] = acc ? out[c] + s : s;
+  }
 }
 
 // out[c] (+)= sum_k part[k][c], fixed order: 8 interleaved partial sums per
@@ -494,7 +506,7 @@ cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, v
     fast = col_pass_t<float>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
   if (out) {
     if (fast)
-      col_finalize_fast_kernel<<<(cols + kThreads - 1) / kThreads, kThreads, 0, st>>>(part, chunks, cols, out, acc);
+      col_finalize_fast_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
     else
       col_finalize_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
   }

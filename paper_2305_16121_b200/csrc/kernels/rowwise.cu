@@ -251,96 +251,141 @@ __device__ __forceinline__ void block_sum(float (&v)[N], float* sm) {
   __syncthreads();
 }
 
-template <typename T, int NVEC>
+template <typename T, int NVEC, int R>
 __global__ void __launch_bounds__(256) ln_fwd_block_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
-                                                           const T* __restrict__ beta, T* __restrict__ y, int cols,
-                                                           float eps) {
+                                                           const T* __restrict__ beta, T* __restrict__ y, long long rows,
+                                                           int cols, float eps) {
   constexpr int V = Vec<T>::N;
-  __shared__ float sm[16];
-  const long long off = static_cast<long long>(blockIdx.x) * cols;
-  float v[NVEC][V], g[NVEC][V], b[NVEC][V];
+  __shared__ float sm[8 * R];
+  const long long row0 = static_cast<long long>(blockIdx.x) * R;
+  float v[R][NVEC][V], g[NVEC][V], b[NVEC][V];
 #pragma unroll
   for (int t = 0; t < NVEC; ++t) {
     const int c = (t * 256 + threadIdx.x) * V;
-    vload(x + off + c, v[t]);
     vload(gamma + c, g[t]);
     vload(beta + c, b[t]);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (row0 + k < rows) vload(x + (row0 + k) * cols + c, v[k][t]);
+      else
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[k][t][e] = 0.f;
+    }
   }
-  float s[1] = {0.f};
+  float s[R];
 #pragma unroll
-  for (int t = 0; t < NVEC; ++t)
+  for (int k = 0; k < R; ++k) {
+    s[k] = 0.f;
 #pragma unroll
-    for (int e = 0; e < V; ++e) s[0] += v[t][e];
-  block_sum<1>(s, sm);
-  const float mean = s[0] / static_cast<float>(cols);
-  float q[1] = {0.f};
+    for (int t = 0; t < NVEC; ++t)
 #pragma unroll
-  for (int t = 0; t < NVEC; ++t)
+      for (int e = 0; e < V; ++e) s[k] += v[k][t][e];
+  }
+  block_sum<R>(s, sm);
+  float mean[R], q[R];
 #pragma unroll
-    for (int e = 0; e < V; ++e) q[0] += (v[t][e] - mean) * (v[t][e] - mean);
-  block_sum<1>(q, sm);
-  const float rstd = rsqrtf(q[0] / static_cast<float>(cols) + eps);
+  for (int k = 0; k < R; ++k) {
+    mean[k] = s[k] / static_cast<float>(cols);
+    q[k] = 0.f;
 #pragma unroll
-  for (int t = 0; t < NVEC; ++t) {
+    for (int t = 0; t < NVEC; ++t)
 #pragma unroll
-    for (int e = 0; e < V; ++e) v[t][e] = (v[t][e] - mean) * rstd * g[t][e] + b[t][e];
-    vstore(y + off + (t * 256 + threadIdx.x) * V, v[t]);
+      for (int e = 0; e < V; ++e) q[k] += (v[k][t][e] - mean[k]) * (v[k][t][e] - mean[k]);
+  }
+  block_sum<R>(q, sm);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (row0 + k >= rows) continue;
+    const float rstd = rsqrtf(q[k] / static_cast<float>(cols) + eps);
+#pragma unroll
+    for (int t = 0; t < NVEC; ++t) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[k][t][e] = (v[k][t][e] - mean[k]) * rstd * g[t][e] + b[t][e];
+      vstore(y + (row0 + k) * cols + (t * 256 + threadIdx.x) * V, v[k][t]);
+    }
   }
 }
 
-template <typename T, int NVEC>
+template <typename T, int NVEC, int R>
 __global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
                                                            const T* __restrict__ dy, T* __restrict__ dx, int acc,
-                                                           float2* __restrict__ stats, int cols, float eps) {
+                                                           float2* __restrict__ stats, long long rows, int cols,
+                                                           float eps) {
   constexpr int V = Vec<T>::N;
-  __shared__ float sm[16];
-  const long long off = static_cast<long long>(blockIdx.x) * cols;
-  float xv[NVEC][V], gv[NVEC][V], o[NVEC][V];
+  __shared__ float sm[16 * R];
+  const long long row0 = static_cast<long long>(blockIdx.x) * R;
+  float xv[R][NVEC][V], gv[R][NVEC][V], o[R][NVEC][V];
 #pragma unroll
   for (int t = 0; t < NVEC; ++t) {
     const int c = (t * 256 + threadIdx.x) * V;
-    float d[V], g[V];
-    vload(x + off + c, xv[t]);
-    vload(dy + off + c, d);
+    float g[V];
     vload(gamma + c, g);
-    if (acc) vload(dx + off + c, o[t]);
 #pragma unroll
-    for (int e = 0; e < V; ++e) gv[t][e] = d[e] * g[e];
+    for (int k = 0; k < R; ++k) {
+      float d[V];
+      if (row0 + k < rows) {
+        vload(x + (row0 + k) * cols + c, xv[k][t]);
+        vload(dy + (row0 + k) * cols + c, d);
+        if (acc) vload(dx + (row0 + k) * cols + c, o[k][t]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) xv[k][t][e] = d[e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) gv[k][t][e] = d[e] * g[e];
+    }
   }
-  float s[1] = {0.f};
+  float s[R];
 #pragma unroll
-  for (int t = 0; t < NVEC; ++t)
+  for (int k = 0; k < R; ++k) {
+    s[k] = 0.f;
 #pragma unroll
-    for (int e = 0; e < V; ++e) s[0] += xv[t][e];
-  block_sum<1>(s, sm);
-  const float mean = s[0] / static_cast<float>(cols);
-  float q[1] = {0.f};
+    for (int t = 0; t < NVEC; ++t)
 #pragma unroll
-  for (int t = 0; t < NVEC; ++t)
+      for (int e = 0; e < V; ++e) s[k] += xv[k][t][e];
+  }
+  block_sum<R>(s, sm);
+  float mean[R], q[R];
 #pragma unroll
-    for (int e = 0; e < V; ++e) q[0] += (xv[t][e] - mean) * (xv[t][e] - mean);
-  block_sum<1>(q, sm);
-  const float rstd = rsqrtf(q[0] / static_cast<float>(cols) + eps);
-  float s12[2] = {0.f, 0.f};
+  for (int k = 0; k < R; ++k) {
+    mean[k] = s[k] / static_cast<float>(cols);
+    q[k] = 0.f;
 #pragma unroll
-  for (int t = 0; t < NVEC; ++t)
+    for (int t = 0; t < NVEC; ++t)
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      xv[t][e] = (xv[t][e] - mean) * rstd;  // xhat
-      s12[0] += gv[t][e];
-      s12[1] += gv[t][e] * xv[t][e];
+      for (int e = 0; e < V; ++e) q[k] += (xv[k][t][e] - mean[k]) * (xv[k][t][e] - mean[k]);
+  }
+  block_sum<R>(q, sm);
+  float rstd[R], s12[2 * R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    rstd[k] = rsqrtf(q[k] / static_cast<float>(cols) + eps);
+    s12[2 * k] = 0.f;
+    s12[2 * k + 1] = 0.f;
+#pragma unroll
+    for (int t = 0; t < NVEC; ++t)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        xv[k][t][e] = (xv[k][t][e] - mean[k]) * rstd[k];  // xhat
+        s12[2 * k] += gv[k][t][e];
+        s12[2 * k + 1] += gv[k][t][e] * xv[k][t][e];
+      }
+  }
+  block_sum<2 * R>(s12, sm);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (row0 + k >= rows) continue;
+    const float m1 = s12[2 * k] / static_cast<float>(cols), m2 = s12[2 * k + 1] / static_cast<float>(cols);
+    if (threadIdx.x == 0) stats[row0 + k] = make_float2(mean[k], rstd[k]);
+#pragma unroll
+    for (int t = 0; t < NVEC; ++t) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const float r = rstd[k] * (gv[k][t][e] - m1 - xv[k][t][e] * m2);
+        o[k][t][e] = acc ? o[k][t][e] + r : r;
+      }
+      vstore(dx + (row0 + k) * cols + (t * 256 + threadIdx.x) * V, o[k][t]);
     }
-  block_sum<2>(s12, sm);
-  const float m1 = s12[0] / static_cast<float>(cols), m2 = s12[1] / static_cast<float>(cols);
-  if (threadIdx.x == 0) stats[blockIdx.x] = make_float2(mean, rstd);
-#pragma unroll
-  for (int t = 0; t < NVEC; ++t) {
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const float r = rstd * (gv[t][e] - m1 - xv[t][e] * m2);
-      o[t][e] = acc ? o[t][e] + r : r;
-    }
-    vstore(dx + off + (t * 256 + threadIdx.x) * V, o[t]);
   }
 }
 
@@ -407,33 +452,48 @@ __global__ void __launch_bounds__(256) ln_param16_kernel(const T* __restrict__ x
   }
 }
 
-// out0/out1[c] (+)= sum_k part[k][0/1][c] in chunk order, 8 loads in flight.
+// out0/out1[c] (+)= sum_k part[k][0/1][c]: 32 columns x 8 chunk lanes per
+// block, group g sums chunks g, g+8, ... (2x2 loads in flight), group sums
+// combined in g order (fixed order, bit-reproducible).
 __global__ void __launch_bounds__(256) colpair_finalize_fast_kernel(const float* __restrict__ part, int chunks,
                                                                     int cols, float* __restrict__ out0,
                                                                     float* __restrict__ out1, int acc) {
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  if (c >= cols) return;
+  __shared__ float sm[2][8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float ta = 0.f, tb = 0.f;
-  int k = 0;
-  for (; k + 4 <= chunks; k += 4) {
-    float a[4], b[4];
+  if (c < cols) {
+    int k = g;
+    for (; k + 8 < chunks; k += 16) {
+      float a[2], b[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a[u] = __ldg(part + (static_cast<long long>(k + u) * 2 + 0) * cols + c);
-      b[u] = __ldg(part + (static_cast<long long>(k + u) * 2 + 1) * cols + c);
+      for (int u = 0; u < 2; ++u) {
+        a[u] = __ldg(part + (static_cast<long long>(k + 8 * u) * 2 + 0) * cols + c);
+        b[u] = __ldg(part + (static_cast<long long>(k + 8 * u) * 2 + 1) * cols + c);
+      }
+      ta += a[0];
+      ta += a[1];
+      tb += b[0];
+      tb += b[1];
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      ta += a[u];
-      tb += b[u];
+    for (; k < chunks; k += 8) {
+      ta += __ldg(part + (static_cast<long long>(k) * 2 + 0) * cols + c);
+      tb += __ldg(part + (static_cast<long long>(k) * 2 + 1) * cols + c);
     }
   }
-  for (; k < chunks; ++k) {
-    ta += __ldg(part + (static_cast<long long>(k) * 2 + 0) * cols + c);
-    tb += __ldg(part + (static_cast<long long>(k) * 2 + 1) * cols + c);
+  sm[0][g][lane] = ta;
+  sm[1][g][lane] = tb;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sa += sm[0][j][lane];
+      sb += sm[1][j][lane];
+    }
+    if (out0) out0[c] = acc ? out0[c] + sa : sa;
+    if (out1) out1[c] = acc ? out1[c] + sb : sb;
   }
-  if (out0) out0[c] = acc ? out0[c] + ta : ta;
-  if (out1) out1[c] = acc ? out1[c] + tb : tb;
 }
 
 // Column partial sums over a chunk of rows: part[chunk][0][c] = sum dy*xhat,
@@ -720,10 +780,16 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
   const int nvec = block_nvec<T>(cols);
   if (nvec && rows < (1LL << 31)) {
-    const unsigned g = static_cast<unsigned>(rows);
-    if (nvec == 1) ln_bwd_block_kernel<T, 1><<<g, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, cols, eps);
-    else if (nvec == 2) ln_bwd_block_kernel<T, 2><<<g, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, cols, eps);
-    else ln_bwd_block_kernel<T, 4><<<g, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, cols, eps);
+    // one row per block (measured faster than 2 for the backward)
+    if (nvec == 1)
+      ln_bwd_block_kernel<T, 1, 1><<<static_cast<unsigned>(rows), 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows,
+                                                                                cols, eps);
+    else if (nvec == 2)
+      ln_bwd_block_kernel<T, 2, 1><<<static_cast<unsigned>(rows), 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows,
+                                                                                cols, eps);
+    else
+      ln_bwd_block_kernel<T, 4, 1><<<static_cast<unsigned>(rows), 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows,
+                                                                                cols, eps);
   } else if (cols <= 16 * 32 * Vec<T>::N) {
     const cudaError_t e = launch_rows_nv<T, LnBwdL>(cols, rows, st, X, G, DY, DX, acc_dx, stats, rows, cols, eps);
     if (e != cudaSuccess) return e;
@@ -735,8 +801,8 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
       const ParamSplit sp = param_split16(rows, cols);
       ln_param16_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
                                                                          sp.rows_per_chunk);
-      colpair_finalize_fast_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta,
-                                                                       acc_params);
+      colpair_finalize_fast_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta,
+                                                                     acc_params);
     } else {
       const ParamSplit sp = param_split<T>(rows, cols);
       ln_param_partial_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
@@ -756,10 +822,12 @@ cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y
   auto Y = static_cast<T*>(y);
   const int nvec = block_nvec<T>(cols);
   if (nvec && rows < (1LL << 31)) {
-    const unsigned g = static_cast<unsigned>(rows);
-    if (nvec == 1) ln_fwd_block_kernel<T, 1><<<g, 256, 0, st>>>(X, G, B, Y, cols, eps);
-    else if (nvec == 2) ln_fwd_block_kernel<T, 2><<<g, 256, 0, st>>>(X, G, B, Y, cols, eps);
-    else ln_fwd_block_kernel<T, 4><<<g, 256, 0, st>>>(X, G, B, Y, cols, eps);
+    if (nvec == 1)
+      ln_fwd_block_kernel<T, 1, 4><<<static_cast<unsigned>((rows + 3) / 4), 256, 0, st>>>(X, G, B, Y, rows, cols, eps);
+    else if (nvec == 2)
+      ln_fwd_block_kernel<T, 2, 2><<<static_cast<unsigned>((rows + 1) / 2), 256, 0, st>>>(X, G, B, Y, rows, cols, eps);
+    else
+      ln_fwd_block_kernel<T, 4, 1><<<static_cast<unsigned>(rows), 256, 0, st>>>(X, G, B, Y, rows, cols, eps);
     return cudaGetLastError();
   }
   if (cols <= 16 * 32 * Vec<T>::N) return launch_rows_nv<T, LnFwdL>(cols, rows, st, X, G, B, Y, rows, cols, eps);
