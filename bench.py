@@ -110,7 +110,7 @@ def cpu_baseline(cfg, seconds=12.0):
     """The reference's own CPU path (tmpsim::recompute_elision_equivalence) on the host cores."""
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
     threads = os.cpu_count() or 1
-    rows = 64
+    rows = 16  # one reference call ~ 3.8 GMAC at C2 widths: a few seconds per sample
     h, f = cfg["hidden"], 4 * cfg["hidden"]
     macs_per_sample = step_flops(cfg) / 2.0 / cfg["batch"]
     if os.path.exists(exe):
@@ -145,7 +145,7 @@ def load_traffic():
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("gemm_dram_bytes_per_launch_ratio"), d
+        return d.get("dominant_dram_bytes_per_launch"), d
     except (OSError, ValueError):
         return None, None
 
