@@ -101,6 +101,10 @@ typedef struct {
 } oases_gemm_desc;
 
 oases_status oases_gemm(const oases_gemm_desc* desc, void* stream);
+/* `count` independent problems (bf16). Two CTA-pair-shaped problems share one
+ * persistent launch (one tile list, longer-K problem first); results are
+ * bit-identical to separate oases_gemm calls. */
+oases_status oases_gemm_grouped(const oases_gemm_desc* descs, int32_t count, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Fused causal attention (tcgen05 flash kernels; bf16, head_dim 64 | 128,   */

@@ -183,6 +183,7 @@ _SIGNATURES = [
     ("oases_version", C.c_char_p, []),
     ("oases_device_sm_count", C.c_int, []),
     ("oases_gemm", C.c_int, [C.POINTER(GemmDesc), C.c_void_p]),
+    ("oases_gemm_grouped", C.c_int, [C.POINTER(GemmDesc), C.c_int32, C.c_void_p]),
     ("oases_attention_supported", C.c_int32, [C.c_int, C.c_int32, C.c_int32]),
     ("oases_attention_fwd", C.c_int, [C.POINTER(AttnDesc), C.c_void_p]),
     ("oases_attention_bwd_workspace", C.c_size_t, [C.POINTER(AttnDesc)]),

@@ -120,53 +120,71 @@ __device__ __forceinline__ void keep_masks16(const PhiloxState& ps, unsigned lon
   }
 }
 
+// Static zigzag schedule of work items over a persistent grid. Items are
+// numbered heaviest first; round r hands CTA c item r*G + c (r even) or
+// r*G + G-1-c (r odd), which balances the decreasing item sizes.
+__device__ __forceinline__ int zigzag_item(int round, int G) {
+  const int c = static_cast<int>(blockIdx.x);
+  return round * G + ((round & 1) ? G - 1 - c : c);
+}
+
 template <int DH>
 struct FwdCfg {
   static constexpr int TILE_BYTES = kTile * DH * 2;
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
+  static constexpr int Q_OFF = 0;                        // [2] double-buffered across items
+  static constexpr int K_OFF = 2 * TILE_BYTES;           // [2]
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;   // [2]
   static constexpr int P_OFF = V_OFF + 2 * TILE_BYTES;
   static constexpr int RED_OFF = P_OFF + kTile * kTile * 2;  // row-sum exchange [2][128]
   static constexpr int BAR_OFF = RED_OFF + 1024;
   static constexpr int SMEM = BAR_OFF + 256;
-  static constexpr uint32_t TMEM_COLS = 512;  // S x2 (256) + O (DH)
+  static constexpr uint32_t TMEM_COLS = 512;  // S x2 (256) + O x2 (2*DH)
 };
 
+// Persistent flash forward: each CTA walks its zigzag item list as one flat
+// sequence of (item, kv-tile) iterations; Q, K/V stages, the S buffers and the
+// O accumulator are all double-buffered across item boundaries, so the next
+// item's loads and first QK^T run under the current item's last softmax and
+// epilogue.
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, const AttnParams p) {
   using C = FwdCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;    // [2]
-  uint64_t* v_full = bars + 3;    // [2]
-  uint64_t* k_empty = bars + 5;   // [2] freed by the S MMA
-  uint64_t* s_full = bars + 7;    // [2]
-  uint64_t* s_empty = bars + 9;   // [2]
-  uint64_t* p_full = bars + 11;
-  uint64_t* pv_done = bars + 12;
-  uint64_t* v_empty = bars + 13;  // [2] freed by the PV MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* q_full = bars;        // [2]
+  uint64_t* q_empty = bars + 2;   // [2] freed by the item's last S MMA
+  uint64_t* k_full = bars + 4;    // [2]
+  uint64_t* k_empty = bars + 6;   // [2] freed by the S MMA
+  uint64_t* v_full = bars + 8;    // [2]
+  uint64_t* v_empty = bars + 10;  // [2] freed by the PV MMA
+  uint64_t* s_full = bars + 12;   // [2]
+  uint64_t* s_empty = bars + 14;  // [2]
+  uint64_t* o_free = bars + 16;   // [2] row warps drained the O buffer
+  uint64_t* p_full = bars + 18;
+  uint64_t* pv_done = bars + 19;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = p.nq - 1 - static_cast<int>(blockIdx.x) / p.Z;  // longest rows first
-  const int z = static_cast<int>(blockIdx.x) % p.Z;
-  const int n = z / p.hl, jl = z - n * p.hl;
-  const int nkv = qt + 1;
-  const int row0 = n * p.seq;
+  const int G = static_cast<int>(gridDim.x);
+  const int total = p.Z * p.nq;
+  auto item_of = [&](int t, int& qt, int& z) {
+    qt = p.nq - 1 - t / p.Z;  // heaviest (longest causal rows) first
+    z = t % p.Z;
+  };
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();
-    mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
       mbar_init(&k_full[s], 1);
-      mbar_init(&v_full[s], 1);
       mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
       mbar_init(&s_empty[s], kRowWarps);
+      mbar_init(&o_free[s], kRowWarps);
     }
     mbar_init(p_full, kRowWarps);
     mbar_init(pv_done, 1);
@@ -181,24 +199,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch(&tqkv);
-      mbar_arrive_expect_tx(q_full, C::TILE_BYTES);
+      int g = 0;  // global kv iteration
+      for (int r = 0, k = 0;; ++r, ++k) {
+        const int t = zigzag_item(r, G);
+        if (t >= total) break;
+        int qt, z;
+        item_of(t, qt, z);
+        const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
+        const int qb = k & 1;
+        mbar_wait(&q_empty[qb], ((k >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], C::TILE_BYTES);
 #pragma unroll
-      for (int g = 0; g < DH / 64; ++g)
-        tma_load_2d(smem + C::Q_OFF + g * 16384, &tqkv, q_full, p.q_col + jl * DH + g * 64, row0 + qt * kTile);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
+        for (int gg = 0; gg < DH / 64; ++gg)
+          tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + gg * 16384, &tqkv, &q_full[qb],
+                      p.q_col + jl * DH + gg * 64, row0 + qt * kTile);
+        for (int j = 0; j <= qt; ++j, ++g) {
+          const int st = g & 1, ph = ((g >> 1) & 1) ^ 1;
+          mbar_wait(&k_empty[st], ph);
+          mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
 #pragma unroll
-        for (int g = 0; g < DH / 64; ++g)
-          tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + g * 16384, &tqkv, &k_full[st],
-                      p.k_col + jl * DH + g * 64, row0 + j * kTile);
-        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
+          for (int gg = 0; gg < DH / 64; ++gg)
+            tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + gg * 16384, &tqkv, &k_full[st],
+                        p.k_col + jl * DH + gg * 64, row0 + j * kTile);
+          mbar_wait(&v_empty[st], ph);
+          mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
 #pragma unroll
-        for (int g = 0; g < DH / 64; ++g)
-          tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + g * 16384, &tqkv, &v_full[st],
-                      p.v_col + jl * DH + g * 64, row0 + j * kTile);
+          for (int gg = 0; gg < DH / 64; ++gg)
+            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + gg * 16384, &tqkv, &v_full[st],
+                        p.v_col + jl * DH + gg * 64, row0 + j * kTile);
+        }
       }
     }
   } else if (warp == 1) {
@@ -206,13 +235,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t id_s = umma_idesc_bf16(kTile, kTile, 0, 0);
       constexpr uint32_t id_o = umma_idesc_bf16(kTile, DH, 0, 1);
       const uint32_t sb = smem_u32(smem);
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
-        mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+      // S for flat iteration (item k, kv tile j, global g); commits q_empty after the item's last tile.
+      auto issue_s = [&](int k, int j, int g, bool last) {
+        const int st = g & 1, qb = k & 1;
+        if (j == 0) mbar_wait(&q_full[qb], (k >> 1) & 1);
+        mbar_wait(&k_full[st], (g >> 1) & 1);
+        mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t qa = sb + C::Q_OFF, kb = sb + C::K_OFF + st * C::TILE_BYTES;
+        const uint32_t qa = sb + C::Q_OFF + qb * C::TILE_BYTES, kb = sb + C::K_OFF + st * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -221,141 +251,201 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&s_full[st]);
         umma_commit(&k_empty[st]);
+        if (last) umma_commit(&q_empty[qb]);
       };
-      auto issue_pv = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[st], (j >> 1) & 1);
+      auto issue_pv = [&](int k, int j, int g) {
+        const int st = g & 1, ob = k & 1;
+        if (j == 0) mbar_wait(&o_free[ob], ((k >> 1) & 1) ^ 1);
+        mbar_wait(p_full, g & 1);
+        mbar_wait(&v_full[st], (g >> 1) & 1);
         tc_fence_after();
         const uint32_t pa = sb + C::P_OFF, vb = sb + C::V_OFF + st * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk) {
           const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = umma_desc_sw128(vb + kk * 2048, 16384, 1024);
-          umma_bf16(tmem + 2 * kTile, ad, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16(tmem + 2 * kTile + ob * DH, ad, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&v_empty[st]);
         umma_commit(pv_done);
       };
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_s(j + 1);
-        issue_pv(j);
+      // flat iteration cursor: (round r -> item t, k), kv tile j, global g
+      int r = 0, k = 0, j = 0, g = 0, qt = -1;
+      {
+        const int t = zigzag_item(0, G);
+        if (t < total) {
+          int z;
+          item_of(t, qt, z);
+        }
+      }
+      if (qt >= 0) {
+        issue_s(0, 0, 0, qt == 0);
+        for (;;) {
+          // successor of (k, j)
+          int k2 = k, j2 = j + 1, qt2 = qt;
+          if (j2 > qt) {
+            const int t2 = zigzag_item(r + 1, G);
+            if (t2 < total) {
+              int z2;
+              item_of(t2, qt2, z2);
+              k2 = k + 1;
+              j2 = 0;
+            } else {
+              qt2 = -1;
+            }
+          }
+          if (qt2 >= 0) issue_s(k2, j2, g + 1, j2 == qt2);
+          issue_pv(k, j, g);
+          if (qt2 < 0) break;
+          if (k2 != k) ++r;
+          k = k2;
+          j = j2;
+          qt = qt2;
+          ++g;
+        }
       }
     }
   } else {
     // ------------------------------------------------ row warps: query row r, key columns [c0, c0 + 64)
     const int q = warp & 3, hf = (warp - 2) >> 2;
-    const int r = q * 32 + lane;
-    const int i = qt * kTile + r;
+    const int rr = q * 32 + lane;
     const int c0 = hf * 64;
-    const unsigned long long ebase =
-        (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i) * static_cast<unsigned long long>(p.seq) +
-        c0;
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t to = tl + 2 * kTile + hf * (DH / 2);  // this warp's half of the O accumulator
     uint8_t* pbuf = smem + C::P_OFF;
     float* xsum = reinterpret_cast<float*>(smem + C::RED_OFF);  // [half][row]
     PhiloxState ph;
     philox_init(p, ph);
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      // the row max needs all 128 keys: read the partner half too (TMEM reads are cheap)
-      uint32_t u[2][32], w[2][32];
-      tmem_ld32(tl + st * kTile + c0, u[0]);
-      tmem_ld32(tl + st * kTile + c0 + 32, u[1]);
-      tmem_ld32(tl + st * kTile + (c0 ^ 64), w[0]);
-      tmem_ld32(tl + st * kTile + (c0 ^ 64) + 32, w[1]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[st]);
-      float mloc = -INFINITY;
-      if (j == qt) {
-        int lim = r - c0, limw = r - (c0 ^ 64);  // keys > r are masked
-        asm volatile("" : "+r"(lim), "+r"(limw));  // keep the comparisons inside the (rare) diagonal branch
-#pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          if (k > lim) u[k >> 5][k & 31] = __float_as_uint(-INFINITY);
-          if (k > limw) w[k >> 5][k & 31] = __float_as_uint(-INFINITY);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 64; ++k)
-        mloc = fmaxf(mloc, fmaxf(__uint_as_float(u[k >> 5][k & 31]), __uint_as_float(w[k >> 5][k & 31])));
-      const float mx = fmaxf(m, mloc * p.sl2);
-      const float alpha = ex2(m - mx);
-      const float nmx = -mx;
-      float sum = 0.f;
-      uint32_t pk[32];
-#pragma unroll
-      for (int k = 0; k < 64; k += 2) {
-        const float a = ex2(fmaf(__uint_as_float(u[k >> 5][k & 31]), p.sl2, nmx));
-        const float b = ex2(fmaf(__uint_as_float(u[k >> 5][(k & 31) + 1]), p.sl2, nmx));
-        sum += a + b;
-        pk[k >> 1] = pack_bf16(a, b);
-      }
-      l = l * alpha + sum;
-      m = mx;
-      if (p.thr) {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t km[8];
-          keep_masks16(ph, (ebase + static_cast<unsigned long long>(j) * kTile + g * 16) >> 4, km);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
-        }
-      }
-      if (j > 0) {
-        // P buffer free and O holds P_{j-1} V_{j-1}: rescale O to the new max.
-        mbar_wait(pv_done, (j - 1) & 1);
+    int g = 0;
+    for (int r = 0, k = 0;; ++r, ++k) {
+      const int t = zigzag_item(r, G);
+      if (t >= total) break;
+      int qt, z;
+      item_of(t, qt, z);
+      const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
+      const int i = qt * kTile + rr;
+      const int ob = k & 1;
+      const uint32_t to = tl + 2 * kTile + ob * DH + hf * (DH / 2);  // this warp's half of O
+      const unsigned long long ebase =
+          (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i) *
+              static_cast<unsigned long long>(p.seq) +
+          c0;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qt; ++j, ++g) {
+        const int st = g & 1;
+        mbar_wait(&s_full[st], (g >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        // the row max needs all 128 keys: read the partner half too (TMEM reads are cheap)
+        uint32_t u[2][32], w[2][32];
+        tmem_ld32(tl + st * kTile + c0, u[0]);
+        tmem_ld32(tl + st * kTile + c0 + 32, u[1]);
+        tmem_ld32(tl + st * kTile + (c0 ^ 64), w[0]);
+        tmem_ld32(tl + st * kTile + (c0 ^ 64) + 32, w[1]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[st]);
+        if (j == qt) {
+          int lim = rr - c0, limw = rr - (c0 ^ 64);  // keys > row are masked
+          asm volatile("" : "+r"(lim), "+r"(limw));  // keep the comparisons inside the (rare) diagonal branch
+#pragma unroll
+          for (int kk = 0; kk < 64; ++kk) {
+            if (kk > lim) u[kk >> 5][kk & 31] = __float_as_uint(-INFINITY);
+            if (kk > limw) w[kk >> 5][kk & 31] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mloc;
+        {  // 8 independent partial maxima (short dependency chains)
+          float mp[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mp[kk] = fmaxf(__uint_as_float(u[0][kk]), __uint_as_float(w[0][kk]));
+#pragma unroll
+          for (int kk = 8; kk < 64; ++kk)
+            mp[kk & 7] =
+                fmaxf(mp[kk & 7], fmaxf(__uint_as_float(u[kk >> 5][kk & 31]), __uint_as_float(w[kk >> 5][kk & 31])));
+          mloc = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+        }
+        // Conditional rescaling: keep the running max unless the row max grew by
+        // more than 8 (log2 units). P = exp2(s - m) then stays <= 256 (exact in
+        // bf16's range) and O, l are rescaled only when it pays; the result is
+        // the same softmax since O and l always share one reference max.
+        const float cand = fmaxf(m, mloc * p.sl2);
+        const float mx = cand > m + 8.f ? cand : m;
+        const float alpha = ex2(m - mx);
+        const float nmx = -mx;
+        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
+#pragma unroll
+        for (int kk = 0; kk < 64; kk += 2) {
+          const float a = ex2(fmaf(__uint_as_float(u[kk >> 5][kk & 31]), p.sl2, nmx));
+          const float b = ex2(fmaf(__uint_as_float(u[kk >> 5][(kk & 31) + 1]), p.sl2, nmx));
+          sp[(kk >> 1) & 7] += a + b;
+          pk[kk >> 1] = pack_bf16(a, b);
+        }
+        const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
+        l = l * alpha + sum;
+        m = mx;
+        if (p.thr) {
+#pragma unroll
+          for (int gq = 0; gq < 4; ++gq) {
+            uint32_t km[8];
+            keep_masks16(ph, (ebase + static_cast<unsigned long long>(j) * kTile + gq * 16) >> 4, km);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) pk[gq * 8 + kk] &= km[kk];
+          }
+        }
+        // the P buffer must be free (previous PV done, possibly the previous item's)
+        if (g > 0) {
+          mbar_wait(pv_done, (g - 1) & 1);
+          tc_fence_after();
+        }
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          // O holds P_{j-1} V_{j-1}: rescale it to the new reference max
 #pragma unroll
           for (int c = 0; c < DH / 64; ++c) {
             uint32_t o[32];
             tmem_ld32(to + c * 32, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            for (int kk = 0; kk < 32; ++kk) o[kk] = __float_as_uint(__uint_as_float(o[kk]) * alpha);
             tmem_st32(to + c * 32, o);
           }
           tmem_wait_st();
         }
-      }
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch)
-        *tile_chunk(pbuf, r, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-      fence_proxy_async();
+        for (int ch = 0; ch < 8; ++ch)
+          *tile_chunk(pbuf, rr, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      // ---- item epilogue: O / l -> ctx, lse
+      xsum[hf * 128 + rr] = l;
+      named_bar_sync(1 + q, 64);
+      const float lt = l + xsum[(hf ^ 1) * 128 + rr];
+      mbar_wait(pv_done, (g - 1) & 1);
+      tc_fence_after();
+      const float inv = p.ks / lt;
+      __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + i) * p.ld_out +
+                            p.do_col + jl * DH + hf * (DH / 2);
+#pragma unroll
+      for (int c = 0; c < DH / 64; ++c) {
+        uint32_t o[32];
+        tmem_ld32(to + c * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float* f = reinterpret_cast<const float*>(o + 8 * kk);
+          *reinterpret_cast<uint4*>(orow + c * 32 + kk * 8) =
+              make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                         pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+        }
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&o_free[ob]);
+      if (hf == 0) p.lse[static_cast<long long>(z) * p.seq + i] = m + log2f(lt);
     }
-    xsum[hf * 128 + r] = l;
-    named_bar_sync(1 + q, 64);
-    const float lt = l + xsum[(hf ^ 1) * 128 + r];
-    mbar_wait(pv_done, (nkv - 1) & 1);
-    tc_fence_after();
-    const float inv = p.ks / lt;
-    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + i) * p.ld_out +
-                          p.do_col + jl * DH + hf * (DH / 2);
-#pragma unroll
-    for (int c = 0; c < DH / 64; ++c) {
-      uint32_t o[32];
-      tmem_ld32(to + c * 32, o);
-      tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float* f = reinterpret_cast<const float*>(o + 8 * k);
-        *reinterpret_cast<uint4*>(orow + c * 32 + k * 8) =
-            make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
-                       pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
-      }
-    }
-    if (hf == 0) p.lse[static_cast<long long>(z) * p.seq + i] = m + log2f(lt);
   }
   tc_fence_before();
   __syncthreads();
@@ -749,7 +839,13 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
   p.out = d.out;
   p.ld_out = d.ld_out;
   p.lse = d.lse;
-  const unsigned grid = static_cast<unsigned>(p.Z * p.nq);
+  unsigned grid = static_cast<unsigned>(p.Z * p.nq);
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (grid > static_cast<unsigned>(sms)) grid = static_cast<unsigned>(sms);  // persistent: one CTA per SM
+  }
   cudaError_t e;
   if (d.head_dim == 128) {
     static cudaError_t once = set_smem(attn_fwd_kernel<128>, FwdCfg<128>::SMEM);

@@ -17,6 +17,9 @@ struct GemmStatus {
 
 // bf16 operands: tcgen05/TMEM/TMA persistent kernel (gemm_tc.cu).
 GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream);
+// n independent bf16 problems in one persistent launch when they are all
+// CTA-pair shaped (n == 2), else one launch each.
+GemmStatus gemm_tc_group(const oases_gemm_desc* d, int n, cudaStream_t stream);
 // f32 operands: FFMA tiled kernel for the 1e-4 parity mode (gemm_simt.cu).
 GemmStatus gemm_simt(const oases_gemm_desc& d, cudaStream_t stream);
 

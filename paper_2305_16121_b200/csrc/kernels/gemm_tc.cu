@@ -442,35 +442,83 @@ __device__ __forceinline__ void pair_decode(const TcParams& p, int t, int& z, in
   n0 = (r - mt * p.tiles_n) * PAIR_BN;
 }
 
+// Up to two independent GEMM problems in one persistent launch (a "group"):
+// their tiles form one list (problem 0 first, the host puts the problem with
+// the longer K first), walked with the usual static pair striding. Used for
+// the backward's dgrad + wgrad pairs, which read the same gradient and are
+// independent: together they fill the 74 CTA pairs' waves far better than
+// either alone. Operand majorness is a runtime property of each problem.
+struct TcGroup {
+  TcParams p[2];
+  int a_mn[2], b_mn[2];
+  int tiles0, total;
+};
+
+__device__ __forceinline__ int group_tile(const TcGroup& g, int t, int& lt) {
+  if (t < g.tiles0) {
+    lt = t;
+    return 0;
+  }
+  lt = t - g.tiles0;
+  return 1;
+}
+
 template <typename OutT, int EPI, bool ACC>
-__device__ __forceinline__ void epilogue_role_pair(const TcParams& p, uint64_t* tfull, uint64_t* tempty,
-                                                   uint32_t tmem_base, float4* stg, int warp, int lane,
-                                                   uint32_t rank) {
-  const int q = warp & 3, half = (warp - 2) >> 2;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int total = p.batch * p.tiles_m * p.tiles_n;
-  int acc = 0;
-  uint32_t acc_phase = 0;
-  for (int t = pair; t < total; t += npairs) {
-    int z, m0, n0;
-    pair_decode(p, t, z, m0, n0);
-    mbar_wait(&tfull[acc], acc_phase);
-    tc_fence_after();
-    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                           static_cast<uint32_t>(acc * PAIR_BN + half * (PAIR_BN / 2));
-    const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
-    epilogue_stripe<OutT, EPI, ACC>(p, z, mb, n0 + half * (PAIR_BN / 2), PAIR_BN / 2, taddr, stg, lane);
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_leader(&tempty[acc]);
-    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+__device__ __forceinline__ void pair_tile_epilogue(const TcParams& p, int lt, uint32_t taddr, float4* stg, int q,
+                                                   int half, int lane, uint32_t rank) {
+  int z, m0, n0;
+  pair_decode(p, lt, z, m0, n0);
+  const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
+  epilogue_stripe<OutT, EPI, ACC>(p, z, mb, n0 + half * (PAIR_BN / 2), PAIR_BN / 2, taddr, stg, lane);
+}
+
+// Producer: TMA of one k-block of a tile (compile-time operand layout).
+template <int A_MN, int B_MN>
+__device__ __forceinline__ void pair_load(uint8_t* sa, uint8_t* sb, const CUtensorMap* tma_a, const CUtensorMap* tma_b,
+                                          uint64_t* bar, int ax, int ay, int bx, int by, int am, int bn, int k0) {
+  if (A_MN) {
+    tma_load_2d_pair(sa, tma_a, bar, ax + am, ay + k0);
+    tma_load_2d_pair(sa + 8192, tma_a, bar, ax + am + 64, ay + k0);
+  } else {
+    tma_load_2d_pair(sa, tma_a, bar, ax + k0, ay + am);
+  }
+  if (B_MN) {
+    tma_load_2d_pair(sb, tma_b, bar, bx + bn, by + k0);
+    tma_load_2d_pair(sb + 8192, tma_b, bar, bx + bn + 64, by + k0);
+  } else {
+    tma_load_2d_pair(sb, tma_b, bar, bx + k0, by + bn);
   }
 }
 
+// MMA issuer: all k-blocks of one tile into the TMEM accumulator d_tmem.
 template <int A_MN, int B_MN>
+__device__ __forceinline__ void pair_mma_tile(uint32_t smem_base, uint64_t* full, uint64_t* empty, int& stage,
+                                              uint32_t& phase, uint32_t d_tmem, int kblocks) {
+  constexpr uint32_t idesc = umma_idesc_bf16(PAIR_BM, PAIR_BN, A_MN, B_MN);
+  for (int kb = 0; kb < kblocks; ++kb) {
+    mbar_wait(&full[stage], phase);
+    tc_fence_after();
+    const uint32_t sa = smem_base + stage * PAIR_STAGE_BYTES;
+    const uint32_t sb = sa + PAIR_HALF_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk) {
+      const uint64_t adesc = A_MN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024) : umma_desc_sw128(sa + kk * 32, 16, 1024);
+      const uint64_t bdesc = B_MN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024) : umma_desc_sw128(sb + kk * 32, 16, 1024);
+      umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+    }
+    umma_commit_pair(&empty[stage], 0x3);
+    if (++stage == PAIR_STAGES) { stage = 0; phase ^= 1; }
+  }
+}
+
+// Operand layouts are template parameters per problem slot (A0,B0 | A1,B1): a
+// single problem instantiates A1 = A0, B1 = B0; the backward's wgrad + dgrad
+// group is <1,1,0,1>.
+template <int A0, int B0, int A1, int B1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                    const TcParams p) {
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap tb0,
+                    const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensorMap tb1,
+                    const TcGroup g) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(16) float4 stg_all[STG_FLOAT4];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -485,11 +533,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int total_tiles = p.batch * p.tiles_m * p.tiles_n;
+  const int total_tiles = g.total;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tma_a);
-    tma_prefetch(&tma_b);
+    tma_prefetch(&ta0);
+    tma_prefetch(&tb0);
+    if (g.total > g.tiles0) {
+      tma_prefetch(&ta1);
+      tma_prefetch(&tb1);
+    }
     for (int s = 0; s < PAIR_STAGES; ++s) {
       mbar_init(&full[s], 1);   // leader's arrive.expect_tx; both CTAs' TMA bytes
       mbar_init(&empty[s], 1);  // multicast commit from the leader's MMA
@@ -511,8 +563,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total_tiles; t += npairs) {
+        int lt;
+        const int pi = group_tile(g, t, lt);
+        const TcParams& p = g.p[pi];
         int z, m0, n0;
-        pair_decode(p, t, z, m0, n0);
+        pair_decode(p, lt, z, m0, n0);
         const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
         const int ax = p.a_x_off[0] * zo + p.a_x_off[1] * zi, ay = p.a_y_off[0] * zo + p.a_y_off[1] * zi;
         const int bx = p.b_x_off[0] * zo + p.b_x_off[1] * zi, by = p.b_y_off[0] * zo + p.b_y_off[1] * zi;
@@ -522,60 +577,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PAIR_STAGE_BYTES);
           uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
           uint8_t* sb = sa + PAIR_HALF_BYTES;
-          const int k0 = kb * BK;
-          if (A_MN) {
-            tma_load_2d_pair(sa, &tma_a, &full[stage], ax + am, ay + k0);
-            tma_load_2d_pair(sa + 8192, &tma_a, &full[stage], ax + am + 64, ay + k0);
-          } else {
-            tma_load_2d_pair(sa, &tma_a, &full[stage], ax + k0, ay + am);
-          }
-          if (B_MN) {
-            tma_load_2d_pair(sb, &tma_b, &full[stage], bx + bn, by + k0);
-            tma_load_2d_pair(sb + 8192, &tma_b, &full[stage], bx + bn + 64, by + k0);
-          } else {
-            tma_load_2d_pair(sb, &tma_b, &full[stage], bx + k0, by + bn);
-          }
+          if (pi == 0)
+            pair_load<A0, B0>(sa, sb, &ta0, &tb0, &full[stage], ax, ay, bx, by, am, bn, kb * BK);
+          else
+            pair_load<A1, B1>(sa, sb, &ta1, &tb1, &full[stage], ax, ay, bx, by, am, bn, kb * BK);
           if (++stage == PAIR_STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(PAIR_BM, PAIR_BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint32_t smem_base = smem_u32(smem);
       for (int t = pair; t < total_tiles; t += npairs) {
+        int lt;
+        const int pi = group_tile(g, t, lt);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * PAIR_BN);
-        for (int kb = 0; kb < p.kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_base + stage * PAIR_STAGE_BYTES;
-          const uint32_t sb = sa + PAIR_HALF_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t adesc = A_MN ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
-                                        : umma_desc_sw128(sb + kk * 32, 16, 1024);
-            umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit_pair(&empty[stage], 0x3);
-          if (++stage == PAIR_STAGES) { stage = 0; phase ^= 1; }
-        }
+        if (pi == 0)
+          pair_mma_tile<A0, B0>(smem_base, full, empty, stage, phase, d_tmem, g.p[0].kblocks);
+        else
+          pair_mma_tile<A1, B1>(smem_base, full, empty, stage, phase, d_tmem, g.p[1].kblocks);
         umma_commit_pair(&tfull[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
+    // ------------------------------------------------ epilogue (warps 2..9), per-tile mode dispatch
     float4* stg = stg_all + (warp - 2) * 256;
-#define OASES_PAIR_BODY(T, E, A) epilogue_role_pair<T, E, A>(p, tfull, tempty, tmem_base, stg, warp, lane, rank)
-    OASES_EPI_DISPATCH(p, OASES_PAIR_BODY);
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < total_tiles; t += npairs) {
+      int lt;
+      const int pi = group_tile(g, t, lt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                             static_cast<uint32_t>(acc * PAIR_BN + half * (PAIR_BN / 2));
+      // static problem index: the parameters stay constant-bank operands
+      if (pi == 0) {
+#define OASES_PAIR_BODY(T, E, A) pair_tile_epilogue<T, E, A>(g.p[0], lt, taddr, stg, q, half, lane, rank)
+        OASES_EPI_DISPATCH(g.p[0], OASES_PAIR_BODY);
 #undef OASES_PAIR_BODY
+      } else {
+#define OASES_PAIR_BODY(T, E, A) pair_tile_epilogue<T, E, A>(g.p[1], lt, taddr, stg, q, half, lane, rank)
+        OASES_EPI_DISPATCH(g.p[1], OASES_PAIR_BODY);
+#undef OASES_PAIR_BODY
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
   }
 
   tc_fence_before();
@@ -621,26 +679,31 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcPara
   return cudaGetLastError();
 }
 
-template <int A_MN, int B_MN>
-cudaError_t launch_tc2(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p, int grid,
-                       cudaStream_t stream) {
+template <int A0, int B0, int A1, int B1>
+cudaError_t launch_group_t(const CUtensorMap (&maps)[4], const TcGroup& g, int grid, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<A0, B0, A1, B1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          PAIR_SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_tc2_kernel<A_MN, B_MN><<<grid, THREADS, PAIR_SMEM, stream>>>(ma, mb, p);
+  gemm_tc2_kernel<A0, B0, A1, B1><<<grid, THREADS, PAIR_SMEM, stream>>>(maps[0], maps[1], maps[2], maps[3], g);
   return cudaGetLastError();
 }
 
-cudaError_t dispatch_pair(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
-                          int grid, cudaStream_t s) {
-  if (!a_mn && !b_mn) return launch_tc2<0, 0>(ma, mb, p, grid, s);
-  if (!a_mn && b_mn) return launch_tc2<0, 1>(ma, mb, p, grid, s);
-  if (a_mn && !b_mn) return launch_tc2<1, 0>(ma, mb, p, grid, s);
-  return launch_tc2<1, 1>(ma, mb, p, grid, s);
+// false: no instantiation for this combination of operand layouts
+bool launch_group(const CUtensorMap (&maps)[4], const TcGroup& g, int grid, cudaStream_t stream, cudaError_t* e) {
+  const int key = g.a_mn[0] * 8 + g.b_mn[0] * 4 + g.a_mn[1] * 2 + g.b_mn[1];
+  switch (key) {
+    case 0: *e = launch_group_t<0, 0, 0, 0>(maps, g, grid, stream); return true;
+    case 5: *e = launch_group_t<0, 1, 0, 1>(maps, g, grid, stream); return true;
+    case 10: *e = launch_group_t<1, 0, 1, 0>(maps, g, grid, stream); return true;
+    case 15: *e = launch_group_t<1, 1, 1, 1>(maps, g, grid, stream); return true;
+    case 13: *e = launch_group_t<1, 1, 0, 1>(maps, g, grid, stream); return true;  // wgrad + dgrad
+    case 7: *e = launch_group_t<0, 1, 1, 1>(maps, g, grid, stream); return true;   // dgrad + wgrad
+    default: return false;
+  }
 }
 
 template <int BN>
@@ -695,27 +758,37 @@ bool make_tma_bf16_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t c
   return true;
 }
 
-GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
-  GemmStatus st;
+namespace {
+
+struct Prepared {
+  TcParams p;
+  CUtensorMap ma, mb;
+  bool pair;
+  int BN;
+  long long tiles;
+};
+
+// Validation + TMA maps + kernel parameters for one problem.
+bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
   // Shape / alignment checks: TMA needs 16 B aligned strides and bases; the
   // vectorised epilogue needs 16 B aligned output rows.
   auto aligned = [](const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; };
   if (d.a.ld % 8 || d.b.ld % 8 || !aligned(d.a.ptr, 16) || !aligned(d.b.ptr, 16)) {
-    st.err = "gemm_tc: operand base/ld must be 16-byte aligned (ld % 8 == 0)";
-    return st;
+    *err = "gemm_tc: operand base/ld must be 16-byte aligned (ld % 8 == 0)";
+    return false;
   }
   if (d.ldc % 8 || !aligned(d.c, 16) || (d.c_col_off[0] % 8) || (d.c_col_off[1] % 8) ||
       (d.c2 && !aligned(d.c2, 16)) || (d.aux && !aligned(d.aux, 16)) || (d.bias && !aligned(d.bias, 16))) {
-    st.err = "gemm_tc: output/aux/bias bases, ld and column offsets must be 16-byte aligned";
-    return st;
+    *err = "gemm_tc: output/aux/bias bases, ld and column offsets must be 16-byte aligned";
+    return false;
   }
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0 || d.batch_inner <= 0) {
-    st.err = "gemm_tc: empty problem";
-    return st;
+    *err = "gemm_tc: empty problem";
+    return false;
   }
   if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_DGELU) {
-    st.err = "gemm_tc: unknown epilogue";
-    return st;
+    *err = "gemm_tc: unknown epilogue";
+    return false;
   }
   const int BN = (d.N <= 128) ? 128 : 256;
   // Reads past the logical K would pull in neighbouring data (TMA zero-fills
@@ -725,20 +798,19 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
     const int64_t ka = d.a.mn_major ? d.a.rows : d.a.cols;
     const int64_t kb = d.b.mn_major ? d.b.rows : d.b.cols;
     if (d.batch > 1 || ka != d.K || kb != d.K) {
-      st.err = "gemm_tc: K % 64 != 0 requires K to span both operands' full extent (unbatched)";
-      return st;
+      *err = "gemm_tc: K % 64 != 0 requires K to span both operands' full extent (unbatched)";
+      return false;
     }
   }
   if (d.causal != OASES_CAUSAL_NONE && d.M != d.K && d.causal != OASES_CAUSAL_SKIP_UPPER) {
-    st.err = "gemm_tc: causal K-range modes need M == K";
-    return st;
+    *err = "gemm_tc: causal K-range modes need M == K";
+    return false;
   }
   const bool pair = use_pairs() && d.causal == OASES_CAUSAL_NONE && d.M > BM && d.N > 128;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, d.a, 64, d.a.mn_major ? 64 : BM, &st.err)) return st;
-  if (!make_map(&mb, d.b, 64, d.b.mn_major ? 64 : (pair ? 128 : BN), &st.err)) return st;
-
-  TcParams p{};
+  if (!make_map(&out.ma, d.a, 64, d.a.mn_major ? 64 : BM, err)) return false;
+  if (!make_map(&out.mb, d.b, 64, d.b.mn_major ? 64 : (pair ? 128 : BN), err)) return false;
+  TcParams& p = out.p;
+  p = TcParams{};
   p.M = static_cast<int>(d.M);
   p.N = static_cast<int>(d.N);
   p.K = static_cast<int>(d.K);
@@ -766,24 +838,95 @@ GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
   p.causal = d.causal;
   p.accumulate = d.accumulate;
   p.alpha = d.alpha;
-  const long long tiles = static_cast<long long>(p.batch) * p.tiles_m * p.tiles_n;
-  int grid = sm_count();
-  if (d.max_ctas > 0 && d.max_ctas < grid) grid = d.max_ctas;
-  cudaError_t e;
-  if (pair) {
-    int pairs = grid / 2;
-    if (pairs < 1) pairs = 1;
-    if (tiles < pairs) pairs = static_cast<int>(tiles);
-    e = dispatch_pair(d.a.mn_major, d.b.mn_major, ma, mb, p, 2 * pairs, stream);
-  } else {
-    if (tiles < grid) grid = static_cast<int>(tiles);
-    e = BN == 128 ? dispatch_major<128>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream)
-                  : dispatch_major<256>(d.a.mn_major, d.b.mn_major, ma, mb, p, grid, stream);
-  }
+  out.pair = pair;
+  out.BN = BN;
+  out.tiles = static_cast<long long>(p.batch) * p.tiles_m * p.tiles_n;
+  return true;
+}
+
+GemmStatus launch_status(cudaError_t e) {
+  GemmStatus st;
   if (e != cudaSuccess) {
     st.err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
     st.cuda = true;
     return st;
+  }
+  st.ok = true;
+  return st;
+}
+
+int grid_cap(int max_ctas) {
+  int grid = sm_count();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  return grid;
+}
+
+GemmStatus launch_pairs(const oases_gemm_desc* const* ds, const Prepared* const* pr, int n, int max_ctas,
+                        cudaStream_t stream) {
+  TcGroup g{};
+  CUtensorMap maps[4];
+  long long total = 0;
+  for (int i = 0; i < 2; ++i) {
+    const int k = i < n ? i : 0;  // a group of one repeats its maps in the unused slots
+    g.p[i] = pr[k]->p;
+    g.a_mn[i] = ds[k]->a.mn_major ? 1 : 0;
+    g.b_mn[i] = ds[k]->b.mn_major ? 1 : 0;
+    maps[2 * i] = pr[k]->ma;
+    maps[2 * i + 1] = pr[k]->mb;
+  }
+  for (int i = 0; i < n; ++i) total += pr[i]->tiles;
+  g.tiles0 = static_cast<int>(pr[0]->tiles);
+  g.total = static_cast<int>(total);
+  int pairs = grid_cap(max_ctas) / 2;
+  if (pairs < 1) pairs = 1;
+  if (total < pairs) pairs = static_cast<int>(total);
+  cudaError_t e = cudaSuccess;
+  if (!launch_group(maps, g, 2 * pairs, stream, &e)) {
+    GemmStatus st;
+    st.err = "gemm_tc: no grouped kernel for this operand-layout combination";
+    return st;
+  }
+  return launch_status(e);
+}
+
+}  // namespace
+
+GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
+  GemmStatus st;
+  Prepared pr;
+  if (!prepare(d, pr, &st.err)) return st;
+  if (pr.pair) {
+    const oases_gemm_desc* ds[1] = {&d};
+    const Prepared* ps[1] = {&pr};
+    return launch_pairs(ds, ps, 1, d.max_ctas, stream);
+  }
+  int grid = grid_cap(d.max_ctas);
+  if (pr.tiles < grid) grid = static_cast<int>(pr.tiles);
+  const cudaError_t e = pr.BN == 128 ? dispatch_major<128>(d.a.mn_major, d.b.mn_major, pr.ma, pr.mb, pr.p, grid, stream)
+                                     : dispatch_major<256>(d.a.mn_major, d.b.mn_major, pr.ma, pr.mb, pr.p, grid, stream);
+  return launch_status(e);
+}
+
+GemmStatus gemm_tc_group(const oases_gemm_desc* d, int n, cudaStream_t stream) {
+  GemmStatus st;
+  if (n == 2) {
+    Prepared a, b;
+    if (!prepare(d[0], a, &st.err) || !prepare(d[1], b, &st.err)) return st;
+    // instantiated mixed groups: (wgrad: MN/MN) with (dgrad: K/MN), either order
+    const int ka = (d[0].a.mn_major ? 2 : 0) + (d[0].b.mn_major ? 1 : 0);
+    const int kb = (d[1].a.mn_major ? 2 : 0) + (d[1].b.mn_major ? 1 : 0);
+    const bool supported = ka == kb || (ka == 3 && kb == 1) || (ka == 1 && kb == 3);
+    if (a.pair && b.pair && supported) {
+      // longer-K problem first: its tiles are the heavier ones in the shared list
+      const bool swap = b.p.kblocks > a.p.kblocks;
+      const oases_gemm_desc* ds[2] = {swap ? &d[1] : &d[0], swap ? &d[0] : &d[1]};
+      const Prepared* ps[2] = {swap ? &b : &a, swap ? &a : &b};
+      return launch_pairs(ds, ps, 2, d[0].max_ctas, stream);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    st = gemm_tc(d[i], stream);
+    if (!st.ok) return st;
   }
   st.ok = true;
   return st;

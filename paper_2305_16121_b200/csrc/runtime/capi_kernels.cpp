@@ -67,6 +67,20 @@ oases_status oases_gemm(const oases_gemm_desc* d, void* stream) {
   });
 }
 
+oases_status oases_gemm_grouped(const oases_gemm_desc* d, int32_t count, void* stream) {
+  return guarded([&] {
+    if (!d || count < 1) throw tmpsim::ConfigError("oases_gemm_grouped: need at least one descriptor");
+    need_device();
+    for (int i = 0; i < count; ++i)
+      if (d[i].dtype != OASES_BF16) throw tmpsim::ConfigError("oases_gemm_grouped: bf16 problems only");
+    const oases::GemmStatus st = oases::gemm_tc_group(d, count, S(stream));
+    if (!st.ok) {
+      if (st.cuda) throw oases::CudaError(st.err);
+      throw tmpsim::ConfigError(st.err);
+    }
+  });
+}
+
 namespace {
 void gemm_status_throw(const oases::GemmStatus& st) {
   if (st.ok) return;

@@ -312,6 +312,44 @@ void Stack::gemm(const oases_gemm_desc& d0) {
   ++launches_;
 }
 
+// Two independent GEMMs (a backward dgrad + wgrad pair) in one launch when the
+// tcgen05 CTA-pair kernel takes both (kernels/gemm_tc.cu, TcGroup).
+void Stack::gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1) {
+  if (dtype() != OASES_BF16) {
+    gemm(d0);
+    gemm(d1);
+    return;
+  }
+  oases_gemm_desc d[2] = {d0, d1};
+  for (auto& x : d) {
+    x.dtype = dtype();
+    x.max_ctas = ctx_.gemm_max_ctas;
+  }
+  const bool timed = timing_;
+  if (timed) {
+    while (tev_.size() < 2 * (timed_ + 1)) {
+      cudaEvent_t e;
+      check_cuda(cudaEventCreate(&e), "event");
+      tev_.push_back(e);
+    }
+    if (tflops_.size() < timed_ + 1) tflops_.resize(timed_ + 1);
+    tflops_[timed_] = 0.0;
+    for (const auto& x : d)
+      tflops_[timed_] += 2.0 * static_cast<double>(x.M) * static_cast<double>(x.N) * static_cast<double>(x.K);
+    check_cuda(cudaEventRecord(tev_[2 * timed_], ctx_.compute), "record");
+  }
+  GemmStatus st = gemm_tc_group(d, 2, ctx_.compute);
+  if (!st.ok) {
+    if (st.cuda) throw CudaError(st.err);
+    throw ConfigError(st.err);
+  }
+  if (timed) {
+    check_cuda(cudaEventRecord(tev_[2 * timed_ + 1], ctx_.compute), "record");
+    ++timed_;
+  }
+  launches_ += 1;
+}
+
 void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y) {
   check_cuda(layernorm_fwd(dtype(), x, g, b, y, tokens_sub(), cfg_.h, cfg_.eps, ctx_.compute), "layernorm_fwd");
   ++launches_;
@@ -756,16 +794,15 @@ void Stack::backward(int wi, int block, int sb) {
   const bool att = is_attention(block);
   const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
   // 3. row-parallel GEMM: dW_row += g_ar^T act ; d(act) = g_ar W_row
+  oases_gemm_desc dw{};
+  dw.c_dtype = OASES_F32;
+  dw.M = h; dw.N = nrow; dw.K = Ts;
+  dw.batch = 1; dw.batch_inner = 1;
+  dw.a = operand(gar, Ts, h, h, true);
+  dw.b = operand(ws.act, Ts, nrow, nrow, true);
+  dw.c = bp.g[OASES_P_W_ROW]; dw.ldc = nrow;
+  dw.alpha = 1.f; dw.accumulate = touch(w, block, OASES_P_W_ROW) ? 1 : 0;
   oases_gemm_desc d{};
-  d.c_dtype = OASES_F32;
-  d.M = h; d.N = nrow; d.K = Ts;
-  d.batch = 1; d.batch_inner = 1;
-  d.a = operand(gar, Ts, h, h, true);
-  d.b = operand(ws.act, Ts, nrow, nrow, true);
-  d.c = bp.g[OASES_P_W_ROW]; d.ldc = nrow;
-  d.alpha = 1.f; d.accumulate = touch(w, block, OASES_P_W_ROW) ? 1 : 0;
-  gemm(d);
-  d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = Ts; d.N = nrow; d.K = h;
   d.batch = 1; d.batch_inner = 1;
@@ -774,14 +811,14 @@ void Stack::backward(int wi, int block, int sb) {
   d.alpha = 1.f;
   if (att) {
     d.c = w.du; d.ldc = nrow;
-    gemm(d);
+    gemm2(dw, d);
     attention_bwd(w, block, sb, ws);
   } else {
     // dpre = (g_ar W_row) o gelu'(pre)   (hadamard + gelu_grad fused, numerics.cpp:203-204)
     d.c = w.dcol; d.ldc = ncol;
     d.epilogue = OASES_EPI_DGELU;
     d.aux = ws.col;
-    gemm(d);
+    gemm2(dw, d);
   }
   // 4. column bias
   if (cfg_.bias) {
@@ -793,15 +830,14 @@ void Stack::backward(int wi, int block, int sb) {
   }
   // 5. column-parallel GEMM: dW_col += dcol^T ln ; d_ln partial = dcol W_col -> AR_b (backward f)
   const void* ln = cfg_.ln ? ws.ln : w.xs[static_cast<size_t>(block)][usb];
-  d = oases_gemm_desc{};
-  d.c_dtype = OASES_F32;
-  d.M = ncol; d.N = h; d.K = Ts;
-  d.batch = 1; d.batch_inner = 1;
-  d.a = operand(w.dcol, Ts, ncol, ncol, true);
-  d.b = operand(ln, Ts, h, h, true);
-  d.c = bp.g[OASES_P_W_COL]; d.ldc = h;
-  d.alpha = 1.f; d.accumulate = touch(w, block, OASES_P_W_COL) ? 1 : 0;
-  gemm(d);
+  dw = oases_gemm_desc{};
+  dw.c_dtype = OASES_F32;
+  dw.M = ncol; dw.N = h; dw.K = Ts;
+  dw.batch = 1; dw.batch_inner = 1;
+  dw.a = operand(w.dcol, Ts, ncol, ncol, true);
+  dw.b = operand(ln, Ts, h, h, true);
+  dw.c = bp.g[OASES_P_W_COL]; dw.ldc = h;
+  dw.alpha = 1.f; dw.accumulate = touch(w, block, OASES_P_W_COL) ? 1 : 0;
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = Ts; d.N = h; d.K = ncol;
@@ -810,7 +846,7 @@ void Stack::backward(int wi, int block, int sb) {
   d.b = operand(bp.p[OASES_P_W_COL], ncol, h, h, true);
   d.c = w.bwd_ar[block % 2][usb]; d.ldc = h;
   d.alpha = 1.f;
-  gemm(d);
+  gemm2(dw, d);
 }
 
 void Stack::tail(int wi, int sb) {

@@ -140,6 +140,7 @@ class Stack {
  private:
   void alloc_all();
   void gemm(const oases_gemm_desc& d);
+  void gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1);
   void ln_fwd(const void* x, const void* g, const void* b, void* y);
   oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);

@@ -45,10 +45,9 @@ def operand(t: torch.Tensor, mn_major: bool = False, row_off=(0, 0), col_off=(0,
     return o
 
 
-def gemm(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_off=(0, 0), c_col_off=(0, 0),
-         c_col_base=0, epilogue=capi.EPI_NONE, causal=capi.CAUSAL_NONE, alpha=1.0, accumulate=False,
-         bias=None, aux=None, c2=None, max_ctas=0, dtype=capi.BF16, stream=None):
-    """dtype: operand dtype (capi.BF16 -> tcgen05 kernel, capi.F32 -> FFMA kernel)."""
+def gemm_desc(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_off=(0, 0), c_col_off=(0, 0),
+              c_col_base=0, epilogue=capi.EPI_NONE, causal=capi.CAUSAL_NONE, alpha=1.0, accumulate=False,
+              bias=None, aux=None, c2=None, max_ctas=0, dtype=capi.BF16):
     d = capi.GemmDesc()
     d.dtype = dtype
     d.c_dtype = _dtype(c)
@@ -68,7 +67,19 @@ def gemm(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_off=(0
     d.aux = None if aux is None else aux.data_ptr() + c_col_base * esz
     d.c2 = None if c2 is None else c2.data_ptr() + c_col_base * esz
     d.max_ctas = max_ctas
+    return d
+
+
+def gemm(M, N, K, a, b, c: torch.Tensor, *, stream=None, **kw):
+    """dtype: operand dtype (capi.BF16 -> tcgen05 kernel, capi.F32 -> FFMA kernel)."""
+    d = gemm_desc(M, N, K, a, b, c, **kw)
     check(capi.lib().oases_gemm(C.byref(d), _stream(stream)))
+
+
+def gemm_grouped(descs, stream=None):
+    """Independent bf16 problems (descriptors from gemm_desc) in one launch where possible."""
+    arr = (capi.GemmDesc * len(descs))(*descs)
+    check(capi.lib().oases_gemm_grouped(arr, len(descs), _stream(stream)))
 
 
 def layernorm_fwd(x, gamma, beta, y, eps=1e-5, stream=None):

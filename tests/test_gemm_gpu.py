@@ -148,3 +148,32 @@ def test_gemm_rejects_misaligned(cuda):
     with pytest.raises(capi.OasesError) as e:
         ops.gemm(64, 64, 60, ops.operand(A[:, :60]), ops.operand(A), C)
     assert e.value.status == capi.ERR_CONFIG
+
+
+@pytest.mark.parametrize("T,h,n", [(1024, 512, 768), (640, 384, 1024)])
+def test_gemm_grouped_dgrad_wgrad_bitwise(cuda, T, h, n):
+    """A backward dgrad (DGELU epilogue, MN-major B) and wgrad (f32 accumulate, MN-major A and B)
+    in one grouped launch give exactly the bits of two separate launches."""
+    torch.manual_seed(T + n)
+    g = torch.randn(T, h, device=cuda).bfloat16()       # gradient [T, h]
+    w = torch.randn(h, n, device=cuda).bfloat16() / 8   # W_row [out=h, in=n]
+    act = torch.randn(T, n, device=cuda).bfloat16()     # forward activation
+    pre = torch.randn(T, n, device=cuda).bfloat16()     # DGELU aux
+    outs = []
+    for grouped in (False, True):
+        dcol = torch.empty(T, n, device=cuda, dtype=torch.bfloat16)
+        dw = torch.full((h, n), 0.5, device=cuda)
+        dd = ops.gemm_desc(T, n, h, ops.operand(g), ops.operand(w, True), dcol, epilogue=capi.EPI_DGELU, aux=pre)
+        dwd = ops.gemm_desc(h, n, T, ops.operand(g, True), ops.operand(act, True), dw, accumulate=True)
+        if grouped:
+            ops.gemm_grouped([dwd, dd])
+        else:
+            ops.gemm_grouped([dwd])
+            ops.gemm_grouped([dd])
+        outs.append((dcol, dw))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    ref_d = (g.double() @ w.double()) * gelu_grad64(pre.double())
+    ref_w = 0.5 + g.double().t() @ act.double()
+    assert relerr(outs[1][0], ref_d) < 1e-2
+    assert relerr(outs[1][1], ref_w) < 1e-5
