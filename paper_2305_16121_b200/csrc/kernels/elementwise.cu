@@ -158,61 +158,50 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(const T* __restrict_
   if (part) part[static_cast<long long>(blockIdx.y) * cols + c] = s;
 }
 
-// Column-pass tiling for 16-column lanes: a warp covers 512 columns (lane = 16
-// consecutive columns = one Philox counter), the 8 warps of a block split a
-// chunk of rows (4 rows in flight per warp), and the block's column partials
-// are reduced over its warps in a fixed order into part[chunk][col].
+// Column-pass tiling for 16-column lanes: one warp per block covers 512
+// columns (lane = 16 consecutive columns = one Philox counter) over a chunk of
+// rows (4 rows in flight) and writes its column partials to part[chunk][col].
+// No shared memory, few registers: the kernel co-resides with a persistent
+// GEMM (which leaves < 3 KB of smem per SM), so on the side stream it runs
+// under the GEMMs instead of after them.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) col_pass16_kernel(const T* __restrict__ in, T* __restrict__ dx,
-                                                              float* __restrict__ part, long long rows, int cols,
-                                                              int rows_per_chunk, uint32_t thr, float ks, int drop,
-                                                              uint64_t seed, uint64_t offset) {
-  __shared__ float sm[8][16][33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32) col_pass16_kernel(const T* __restrict__ in, T* __restrict__ dx,
+                                                        float* __restrict__ part, long long rows, int cols,
+                                                        int rows_per_chunk, uint32_t thr, float ks, int drop,
+                                                        uint64_t seed, uint64_t offset) {
+  const int lane = threadIdx.x;
   const int c = blockIdx.x * 512 + lane * 16;
+  if (c >= cols) return;
   const long long r0 = static_cast<long long>(blockIdx.y) * rows_per_chunk;
   const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
   float s[16] = {};
-  if (c < cols) {
-    long long r = r0 + warp;
-    for (; r + 24 < r1; r += 32) {  // 4 rows in flight
-      float v[4][16];
+  long long r = r0;
+  for (; r + 3 < r1; r += 4) {  // 4 rows in flight
+    float v[4][16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load16(in + (r + 8 * u) * cols + c, v[u]);
+    for (int u = 0; u < 4; ++u) load16(in + (r + u) * cols + c, v[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long e = (r + 8 * u) * cols + c;
-        if (drop) apply_dropout16(v[u], static_cast<unsigned long long>(e), seed, offset, thr, ks);
-        if (dx) store16(dx + e, v[u]);
+    for (int u = 0; u < 4; ++u) {
+      const long long e = (r + u) * cols + c;
+      if (drop) apply_dropout16(v[u], static_cast<unsigned long long>(e), seed, offset, thr, ks);
+      if (dx) store16(dx + e, v[u]);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) s[q] += v[u][q];
-      }
+      for (int q = 0; q < 16; ++q) s[q] += v[u][q];
     }
-    for (; r < r1; r += 8) {
-      const long long e = r * cols + c;
-      float v[16];
-      load16(in + e, v);
-      if (drop) apply_dropout16(v, static_cast<unsigned long long>(e), seed, offset, thr, ks);
-      if (dx) store16(dx + e, v);
+  }
+  for (; r < r1; ++r) {
+    const long long e = r * cols + c;
+    float v[16];
+    load16(in + e, v);
+    if (drop) apply_dropout16(v, static_cast<unsigned long long>(e), seed, offset, thr, ks);
+    if (dx) store16(dx + e, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) s[q] += v[q];
-    }
+    for (int q = 0; q < 16; ++q) s[q] += v[q];
   }
   if (!part) return;
+  float* pp = part + static_cast<long long>(blockIdx.y) * cols + c;
 #pragma unroll
-  for (int q = 0; q < 16; ++q) sm[warp][q][lane] = s[q];
-  __syncthreads();
-  // thread t finalises columns t and t + 256 of the block's 512
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int j = threadIdx.x + h * 256;  // column within the block
-    const int ln = j >> 4, q = j & 15;
-    float t = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += sm[w][q][ln];
-    const int col = blockIdx.x * 512 + j;
-    if (col < cols) part[static_cast<long long>(blockIdx.y) * cols + col] = t;
-  }
+  for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(pp + q) = make_float4(s[q], s[q + 1], s[q + 2], s[q + 3]);
 }
 
 // out[c] (+)= sum_k part[k][c]: a block covers 32 columns x 8 chunk lanes; lane
@@ -377,11 +366,11 @@ ColSplit col_split(long long rows, int col_blocks) {
   return {static_cast<int>((rows + rpc - 1) / rpc), rpc};
 }
 
-// (512-column groups) x (row chunks) ~ 2 CTAs per SM, >= 32 rows per chunk
+// (512-column groups) x (row chunks): ~8 single-warp CTAs per SM, >= 8 rows per chunk
 ColSplit col_split16(long long rows, int cols) {
   const int groups = (cols + 511) / 512;
-  long long chunks = (2LL * 148 + groups - 1) / groups;
-  const long long maxc = (rows + 31) / 32;
+  long long chunks = (8LL * 148 + groups - 1) / groups;
+  const long long maxc = (rows + 7) / 8;
   if (chunks > maxc) chunks = maxc;
   if (chunks < 1) chunks = 1;
   const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
@@ -466,9 +455,9 @@ template <typename T>
 static bool col_pass_t(const void* in, void* dx, float* part, long long rows, int cols, uint32_t thr, float ks,
                        int drop, uint64_t seed, uint64_t offset, int* chunks_out, cudaStream_t st) {
   constexpr int V = 16 / sizeof(T);
-  if (cols % 16 == 0 && vec_ok<T>(in, dx, rows * cols, cols)) {
+  if (cols % 16 == 0 && vec_ok<T>(in, dx, rows * cols, cols) && vec_ok<T>(part, nullptr, cols, cols)) {
     const ColSplit sp = col_split16(rows, cols);
-    col_pass16_kernel<T><<<dim3((cols + 511) / 512, sp.chunks), kThreads, 0, st>>>(
+    col_pass16_kernel<T><<<dim3((cols + 511) / 512, sp.chunks), 32, 0, st>>>(
         static_cast<const T*>(in), static_cast<T*>(dx), part, rows, cols, sp.rows_per_chunk, thr, ks, drop, seed,
         offset);
     *chunks_out = sp.chunks;

@@ -389,66 +389,55 @@ __global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__
   }
 }
 
-// LN parameter-gradient partials with 16-column lanes (512 columns per warp,
-// 8 warps splitting a chunk of rows, 4 rows in flight per warp):
+// LN parameter-gradient partials with 16-column lanes: one warp per block
+// covers 512 columns over a chunk of rows (2 rows in flight); no shared
+// memory, so it co-resides with the persistent GEMMs on the side stream.
 // part[chunk][0][c] = sum dy * xhat, part[chunk][1][c] = sum dy.
 template <typename T>
-__global__ void __launch_bounds__(256) ln_param16_kernel(const T* __restrict__ x, const T* __restrict__ dy,
-                                                         const float2* __restrict__ stats, float* __restrict__ part,
-                                                         long long rows, int cols, int rows_per_chunk) {
-  __shared__ float sm[8][16][33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(32) ln_param16_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                                        const float2* __restrict__ stats, float* __restrict__ part,
+                                                        long long rows, int cols, int rows_per_chunk) {
+  const int lane = threadIdx.x;
   const int c = blockIdx.x * 512 + lane * 16;
+  if (c >= cols) return;
   const long long r0 = static_cast<long long>(blockIdx.y) * rows_per_chunk;
   const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
   float sg[16] = {}, sb[16] = {};
-  if (c < cols) {
-    long long r = r0 + warp;
-    for (; r + 8 < r1; r += 16) {  // 2 rows in flight
-      float d[2][16], xv[2][16];
-      float2 st[2];
+  long long r = r0;
+  for (; r + 1 < r1; r += 2) {  // 2 rows in flight
+    float d[2][16], xv[2][16];
+    float2 st[2];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        load16(dy + (r + 8 * u) * cols + c, d[u]);
-        load16(x + (r + 8 * u) * cols + c, xv[u]);
-        st[u] = stats[r + 8 * u];
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          sg[e] += d[u][e] * (xv[u][e] - st[u].x) * st[u].y;
-          sb[e] += d[u][e];
-        }
+    for (int u = 0; u < 2; ++u) {
+      load16(dy + (r + u) * cols + c, d[u]);
+      load16(x + (r + u) * cols + c, xv[u]);
+      st[u] = stats[r + u];
     }
-    for (; r < r1; r += 8) {
-      float d[16], xv[16];
-      load16(dy + r * cols + c, d);
-      load16(x + r * cols + c, xv);
-      const float2 st = stats[r];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        sg[e] += d[e] * (xv[e] - st.x) * st.y;
-        sb[e] += d[e];
+        sg[e] += d[u][e] * (xv[u][e] - st[u].x) * st[u].y;
+        sb[e] += d[u][e];
       }
+  }
+  for (; r < r1; ++r) {
+    float d[16], xv[16];
+    load16(dy + r * cols + c, d);
+    load16(x + r * cols + c, xv);
+    const float2 st = stats[r];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      sg[e] += d[e] * (xv[e] - st.x) * st.y;
+      sb[e] += d[e];
     }
   }
+  float* p0 = part + (static_cast<long long>(blockIdx.y) * 2 + 0) * cols + c;
+  float* p1 = part + (static_cast<long long>(blockIdx.y) * 2 + 1) * cols + c;
 #pragma unroll
-  for (int which = 0; which < 2; ++which) {
-#pragma unroll
-    for (int q = 0; q < 16; ++q) sm[warp][q][lane] = which ? sb[q] : sg[q];
-    __syncthreads();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = threadIdx.x + h * 256;
-      const int ln = j >> 4, q = j & 15;
-      float t = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += sm[w][q][ln];
-      const int col = blockIdx.x * 512 + j;
-      if (col < cols) part[(static_cast<long long>(blockIdx.y) * 2 + which) * cols + col] = t;
-    }
-    __syncthreads();
+  for (int q = 0; q < 16; q += 4) {
+    *reinterpret_cast<float4*>(p0 + q) = make_float4(sg[q], sg[q + 1], sg[q + 2], sg[q + 3]);
+    *reinterpret_cast<float4*>(p1 + q) = make_float4(sb[q], sb[q + 1], sb[q + 2], sb[q + 3]);
   }
 }
 
@@ -746,11 +735,11 @@ ParamSplit param_split(long long rows, int cols) {
   return {cb, static_cast<int>((rows + rpc - 1) / rpc), rpc};
 }
 
-// (512-column groups) x (row chunks) ~ 2 CTAs per SM, >= 32 rows per chunk
+// (512-column groups) x (row chunks): ~8 single-warp CTAs per SM, >= 8 rows per chunk
 ParamSplit param_split16(long long rows, int cols) {
   const int groups = (cols + 511) / 512;
-  long long chunks = (2LL * 148 + groups - 1) / groups;
-  const long long maxc = (rows + 31) / 32;
+  long long chunks = (8LL * 148 + groups - 1) / groups;
+  const long long maxc = (rows + 7) / 8;
   if (chunks > maxc) chunks = maxc;
   if (chunks < 1) chunks = 1;
   const int rpc = static_cast<int>((rows + chunks - 1) / chunks);
@@ -766,10 +755,13 @@ int block_nvec(int cols) {
   return (n == 1 || n == 2 || n == 4) ? n : 0;
 }
 
+// which: 1 = dx (+ row statistics into the workspace), 2 = dgamma/dbeta from
+// those statistics, 3 = both. Splitting lets the parameter reduction run on a
+// side stream under the next GEMMs (its outputs are only needed at step end).
 template <typename T>
 cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx, int acc_dx, float* dgamma,
                      float* dbeta, int acc_params, void* workspace, long long rows, int cols, float eps,
-                     cudaStream_t st) {
+                     cudaStream_t st, int which = 3) {
   float2* stats = static_cast<float2*>(workspace);
   float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) +
                                          ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)));
@@ -779,7 +771,9 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   auto DX = static_cast<T*>(dx);
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
   const int nvec = block_nvec<T>(cols);
-  if (nvec && rows < (1LL << 31)) {
+  if (!(which & 1)) {
+    // parameter pass only
+  } else if (nvec && rows < (1LL << 31)) {
     // one row per block (measured faster than 2 for the backward)
     if (nvec == 1)
       ln_bwd_block_kernel<T, 1, 1><<<static_cast<unsigned>(rows), 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows,
@@ -796,11 +790,11 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   } else {
     ln_bwd_kernel<T><<<grid, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, rows, cols, eps);
   }
-  if (dgamma || dbeta) {
+  if ((which & 2) && (dgamma || dbeta)) {
     if (cols % 16 == 0) {
       const ParamSplit sp = param_split16(rows, cols);
-      ln_param16_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
-                                                                         sp.rows_per_chunk);
+      ln_param16_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 32, 0, st>>>(X, DY, stats, part, rows, cols,
+                                                                        sp.rows_per_chunk);
       colpair_finalize_fast_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta,
                                                                      acc_params);
     } else {
@@ -849,6 +843,15 @@ cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const voi
                           int cols, float eps, cudaStream_t st) {
   if (dtype == OASES_BF16) return ln_fwd_t<__nv_bfloat16>(x, gamma, beta, y, rows, cols, eps, st);
   return ln_fwd_t<float>(x, gamma, beta, y, rows, cols, eps, st);
+}
+
+cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,
+                               int acc_dx, float* dgamma, float* dbeta, int acc_params, void* workspace,
+                               long long rows, int cols, float eps, cudaStream_t st) {
+  if (dtype == OASES_BF16)
+    return ln_bwd_t<__nv_bfloat16>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st,
+                                   which);
+  return ln_bwd_t<float>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st, which);
 }
 
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,

@@ -38,6 +38,9 @@ Context::~Context() {
   if (nccl) ncclCommDestroy(nccl);
   if (compute) cudaStreamDestroy(compute);
   if (comm) cudaStreamDestroy(comm);
+  if (side) cudaStreamDestroy(side);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  if (join_ev) cudaEventDestroy(join_ev);
 }
 
 static void check_nccl(ncclResult_t r, const char* what) {
@@ -71,6 +74,9 @@ std::unique_ptr<Context> make_context(const oases_ctx_desc& d) {
   // The comm stream gets the highest priority so NCCL's CTAs are scheduled as
   // soon as the overlapped GEMM frees SMs.
   check_cuda(cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi), "comm stream");
+  check_cuda(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, lo), "side stream");
+  check_cuda(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming), "fork event");
+  check_cuda(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming), "join event");
   ctx->comm_disabled = d.comm_disabled != 0;
   // tp == 1 with an id: a single-rank NCCL communicator (AllReduce is the
   // identity) -- exercises the NCCL path, including graph capture, on one GPU.
@@ -260,6 +266,8 @@ void Stack::alloc_all() {
     w.ln_ws = arena_.alloc(layernorm_bwd_workspace(Ts, static_cast<int>(h)));
     w.col_ws = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
                                      colsum_workspace(Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
+    w.col_ws2 = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
+                                     colsum_workspace(Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
     w.loss = static_cast<double*>(arena_.alloc(sizeof(double)));
     w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
   }
@@ -348,6 +356,19 @@ void Stack::gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1) {
     ++timed_;
   }
   launches_ += 1;
+}
+
+void Stack::fork_side() {
+  check_cuda(cudaEventRecord(ctx_.fork_ev, ctx_.compute), "fork record");
+  check_cuda(cudaStreamWaitEvent(ctx_.side, ctx_.fork_ev, 0), "fork wait");
+  side_forked_ = true;
+}
+
+void Stack::join_side() {
+  if (!side_forked_) return;
+  check_cuda(cudaEventRecord(ctx_.join_ev, ctx_.side), "join record");
+  check_cuda(cudaStreamWaitEvent(ctx_.compute, ctx_.join_ev, 0), "join wait");
+  side_forked_ = false;
 }
 
 void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y) {
@@ -767,10 +788,15 @@ void Stack::backward(int wi, int block, int sb) {
     const void* dln = w.bwd_ar[(block + 1) % 2][usb];
     if (cfg_.ln) {
       const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
-      check_cuda(layernorm_bwd(dtype(), w.xs[static_cast<size_t>(block + 1)][usb], nxt.p[OASES_P_LN_GAMMA], dln, g,
-                               cfg_.residual ? 1 : 0, nxt.g[OASES_P_LN_GAMMA], nxt.g[OASES_P_LN_BETA], acc ? 1 : 0,
-                               w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute),
+      const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
+      check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
+                                    nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute),
                  "layernorm_bwd");
+      // dgamma/dbeta: side stream, under this op's GEMMs (joined at the op's end)
+      fork_side();
+      check_cuda(layernorm_bwd_part(2, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, nullptr, 0, nxt.g[OASES_P_LN_GAMMA],
+                                    nxt.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.side),
+                 "layernorm_bwd params");
       launches_ += 3;
     } else {
       check_cuda(bias_dropout_residual_fwd(dtype(), dln, nullptr, cfg_.residual ? g : nullptr, g, Ts, hi, 0.f, 0, 0,
@@ -782,13 +808,21 @@ void Stack::backward(int wi, int block, int sb) {
   // 2. through bias-dropout: g_ar = dropout'(g), dbias_row += colsum(g_ar)
   BlockParams& bp = w.params[static_cast<size_t>(block)];
   const void* gar = g;
-  if (cfg_.p_hidden > 0.f || cfg_.bias) {
-    const bool acc = cfg_.bias ? touch(w, block, OASES_P_B_ROW) : false;
-    check_cuda(col_pass(dtype(), g, cfg_.p_hidden > 0.f ? w.gar : nullptr, cfg_.bias ? bp.g[OASES_P_B_ROW] : nullptr,
-                        acc ? 1 : 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0), ctx_.compute),
-               "bdr_bwd");
+  if (cfg_.p_hidden > 0.f) {
+    check_cuda(col_pass(dtype(), g, w.gar, nullptr, 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed,
+                        drop_offset(block, sb, 0), ctx_.compute),
+               "dropout bwd");
+    ++launches_;
+    gar = w.gar;
+  }
+  if (cfg_.bias) {
+    // row-bias gradient = column sums of g_ar: side stream, under the row GEMMs
+    const bool acc = touch(w, block, OASES_P_B_ROW);
+    fork_side();
+    check_cuda(col_pass(dtype(), gar, nullptr, bp.g[OASES_P_B_ROW], acc ? 1 : 0, w.col_ws, Ts, hi, 0.f, 0, 0,
+                        ctx_.side),
+               "row bias grad");
     launches_ += 2;
-    if (cfg_.p_hidden > 0.f) gar = w.gar;
   }
   Workspace& ws = ws_for(w, block, sb);
   const bool att = is_attention(block);
@@ -822,9 +856,11 @@ void Stack::backward(int wi, int block, int sb) {
   }
   // 4. column bias
   if (cfg_.bias) {
+    // the column-bias gradient only feeds the step's result: side stream, under the column GEMMs
     const bool acc = touch(w, block, OASES_P_B_COL);
-    check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws, Ts,
-                        static_cast<int>(ncol), 0.f, 0, 0, ctx_.compute),
+    fork_side();
+    check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, Ts,
+                        static_cast<int>(ncol), 0.f, 0, 0, ctx_.side),
                "colsum");
     launches_ += 2;
   }
@@ -847,6 +883,7 @@ void Stack::backward(int wi, int block, int sb) {
   d.c = w.bwd_ar[block % 2][usb]; d.ldc = h;
   d.alpha = 1.f;
   gemm2(dw, d);
+  join_side();
 }
 
 void Stack::tail(int wi, int sb) {

@@ -28,6 +28,10 @@ struct Context {
   bool comm_disabled = false;  // calibration: one rank's shard, no collectives
   cudaStream_t compute = nullptr;
   cudaStream_t comm = nullptr;
+  // side compute stream: parameter-gradient reductions forked off the compute
+  // stream inside an op and joined before the op ends (off the critical path)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   ncclComm_t nccl = nullptr;
   ~Context();
 };
@@ -91,6 +95,7 @@ struct Worker {
   void* y = nullptr;     // [T_sub, h] final output for the loss head
   void* ln_ws = nullptr;
   void* col_ws = nullptr;
+  void* col_ws2 = nullptr;  // side-stream column sums (bias gradients)
   double* loss = nullptr;     // device scalar (f64)
   double* loss_ws = nullptr;  // partials
 };
@@ -141,6 +146,9 @@ class Stack {
   void alloc_all();
   void gemm(const oases_gemm_desc& d);
   void gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1);
+  void fork_side();  // side stream waits for the compute stream's current tail
+  void join_side();  // compute stream waits for the side stream's current tail
+  bool side_forked_ = false;
   void ln_fwd(const void* x, const void* g, const void* b, void* y);
   oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);
