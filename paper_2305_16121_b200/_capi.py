@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboases.so")
+LIB_PATH = os.environ.get("OASES_LIB") or os.path.join(_HERE, "liboases.so")
 
 OK, ERR_CONFIG, ERR_INFEASIBLE, ERR_IO, ERR_CUDA, ERR_NCCL = 0, 2, 3, 4, 5, 6
 F32, BF16 = 0, 1

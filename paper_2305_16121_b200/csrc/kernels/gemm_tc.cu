@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -99,23 +100,35 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, int t, TileInfo& 
 }
 
 // ----------------------------------------------------------------- epilogue
-// E elements (E = 8 bf16 / 4 f32, one 16-byte vector) of one output row.
-template <typename OutT, int E>
-__device__ __forceinline__ void ld_vec(const OutT* p, float (&v)[E]) {
-  if constexpr (sizeof(OutT) == 2) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
-      v[2 * j] = f.x;
-      v[2 * j + 1] = f.y;
-    }
-  } else {
-    const float4 f = *reinterpret_cast<const float4*>(p);
-    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-  }
+// erf-GeLU and its derivative for the bf16 tensor-core epilogues. The normal
+// CDF uses Abramowitz & Stegun 7.1.26 (|erf error| <= 1.5e-7, four orders of
+// magnitude below the bf16 output's resolution): one rcp and one ex2 on the
+// SFU, shared between Phi(x) and phi(x), ~16 instructions instead of erff +
+// expf (~45). The f32 parity path (gemm_simt) and the standalone GeLU kernels
+// keep the exact erff of numerics.cpp:50-55.
+__device__ __forceinline__ void norm_cdf_pdf(float x, float& cdf, float& pdf) {
+  const float u = fabsf(x) * 0.70710678118654752f;
+  float t, e;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, u, 1.0f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-0.72134752044448170f * x * x));  // exp(-x^2/2)
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+  const float half_erf = fmaf(-0.5f * poly, e, 0.5f);  // erf(|x|/sqrt2) / 2
+  cdf = 0.5f + copysignf(half_erf, x);
+  pdf = 0.39894228040143268f * e;
 }
+__device__ __forceinline__ float gelu_fast(float x) {
+  float c, d;
+  norm_cdf_pdf(x, c, d);
+  return x * c;
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  float c, d;
+  norm_cdf_pdf(x, c, d);
+  return fmaf(x, d, c);
+}
+
+// E elements (E = 8 bf16 / 4 f32, one 16-byte vector) of one output row.
 template <typename OutT, int E>
 __device__ __forceinline__ void st_vec(OutT* p, const float (&v)[E]) {
   if constexpr (sizeof(OutT) == 2) {
@@ -148,101 +161,175 @@ __device__ __forceinline__ void ld_bias(const __nv_bfloat16* b, int n, int valid
   }
 }
 
-// One warp's 32-row x ncols stripe of an accumulator tile (ncols % 32 == 0).
-// TMEM -> registers (thread = row) -> 128B-swizzled smem staging -> each lane
-// takes one 16-byte column group of a row, so a warp's global access covers
-// 32/LPR full row segments -> fused epilogue -> global.
+// 16-byte vector (E elements) -> floats.
+template <typename OutT, int E>
+__device__ __forceinline__ void unpack_vec(const uint4 u, float (&v)[E]) {
+  if constexpr (sizeof(OutT) == 2) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
+  } else {
+    v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y); v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+  }
+}
+
+// Geometry of one warp's epilogue stripe: lane (lr, lc) owns 16-byte column
+// group lc of rows lr, lr + RPI, ... of each 32-column chunk.
+template <typename OutT>
+struct StripeGeo {
+  static constexpr int E = 16 / sizeof(OutT);  // elements per lane per row
+  static constexpr int LPR = 32 / E;           // lanes per row (4 | 8)
+  static constexpr int RPI = 32 / LPR;         // rows per iteration (8 | 4)
+  static constexpr int IT = 32 / RPI;          // row iterations per chunk
+};
+
+// Loads of the global operands an epilogue reads (dGeLU pre-activation,
+// f32 accumulate of C) for chunk c into registers.
 template <typename OutT, int EPI, bool ACC>
-__device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_base, int nbeg, int ncols,
-                                                uint32_t taddr, float4* stg, int lane) {
-  constexpr int E = 16 / sizeof(OutT);  // elements per lane per row
-  constexpr int LPR = 32 / E;           // lanes per row (4 | 8)
-  constexpr int RPI = 32 / LPR;         // rows per iteration (8 | 4)
+__device__ __forceinline__ void epi_prefetch(const TcParams& p, int c, int nbeg, int lc, int lr, int rows_left,
+                                             long long lane_base, long long step,
+                                             uint4 (&pa)[StripeGeo<OutT>::IT], uint4 (&pc)[StripeGeo<OutT>::IT]) {
+  using G = StripeGeo<OutT>;
+  const int n = nbeg + c * 32 + lc * G::E;
+  const bool full = n + G::E <= p.N;  // partial groups use the scalar tail path
+  // every element gets a value (zero where not loaded): no merge with stale
+  // register contents, so the buffers never need to live in local memory
+#pragma unroll
+  for (int it = 0; it < G::IT; ++it) {
+    const bool ok = full && it * G::RPI + lr < rows_left;
+    const long long off = lane_base + nbeg + c * 32 + it * step;
+    if constexpr (EPI == OASES_EPI_DGELU) {
+      pa[it] = make_uint4(0u, 0u, 0u, 0u);
+      if (ok) pa[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const OutT*>(p.aux) + off));
+    }
+    if constexpr (ACC) {
+      pc[it] = make_uint4(0u, 0u, 0u, 0u);
+      if (ok) pc[it] = *reinterpret_cast<const uint4*>(reinterpret_cast<const OutT*>(p.c) + off);
+    }
+  }
+}
+
+// One 32-column chunk of a stripe: TMEM -> swizzled smem -> fused epilogue -> global.
+template <typename OutT, int EPI, bool ACC>
+__device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, long long row0, long long col0, int lr,
+                                          int lc, int rows_left, long long step, long long lane_base, uint32_t taddr,
+                                          float4* stg, int lane) {
+  using G = StripeGeo<OutT>;
+  constexpr int E = G::E, RPI = G::RPI, IT = G::IT;
   constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU;
-  const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
-  const long long row0 = p.c_row_off[0] * zo + p.c_row_off[1] * zi + m_base;
-  const long long col0 = p.c_col_off[0] * zo + p.c_col_off[1] * zi;
-  const int lr = lane / LPR, lc = lane % LPR;
-  const int rows_left = p.M - m_base;  // rows of this stripe inside the problem
-  const long long step = static_cast<long long>(RPI) * p.ldc;
-  const bool scale = p.alpha != 1.f;
-#pragma unroll 1
-  for (int c = 0; c < ncols / 32; ++c) {
-    const int nc = nbeg + c * 32;
+  constexpr bool DG = EPI == OASES_EPI_DGELU;
+  const int nc = nbeg + c * 32;
+  // All of the chunk's global operand loads are in flight at once (one DRAM
+  // latency per chunk instead of one per row pair). bf16 operands (4 vectors)
+  // are issued before the TMEM drain so their latency overlaps it; f32 ones
+  // (8 vectors) after it, once the 32 TMEM registers are free again.
+  constexpr bool EARLY = true;
+  uint4 pa[IT], pc[IT];
+  if constexpr ((DG || ACC) && EARLY)
+    epi_prefetch<OutT, EPI, ACC>(p, c, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
+  {
     uint32_t r[32];
     tmem_ld32(taddr + static_cast<uint32_t>(c * 32), r);
     tmem_wait_ld();
-    if (nc >= p.N) continue;  // warp-uniform
+    if (nc >= p.N) return;  // warp-uniform
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       stg[lane * 8 + (j ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                                      __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-    __syncwarp();
-    const int n = nc + lc * E;
-    const int valid = p.N - n;  // elements of this lane's group inside the problem
-    if (valid > 0) {
-      float b[E];
-      if constexpr (BIAS) {
-        if (p.bias) ld_bias<E>(reinterpret_cast<const __nv_bfloat16*>(p.bias), n, valid, b);
-        else
+  }
+  if constexpr ((DG || ACC) && !EARLY)
+    epi_prefetch<OutT, EPI, ACC>(p, c, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
+  __syncwarp();
+  const int n = nc + lc * E;
+  const int valid = p.N - n;  // elements of this lane's group inside the problem
+  if (valid > 0) {
+    float b[E];
+    if constexpr (BIAS) {
+      if (p.bias) ld_bias<E>(reinterpret_cast<const __nv_bfloat16*>(p.bias), n, valid, b);
+      else
 #pragma unroll
-          for (int i = 0; i < E; ++i) b[i] = 0.f;
+        for (int i = 0; i < E; ++i) b[i] = 0.f;
+    }
+    OutT* cp = reinterpret_cast<OutT*>(p.c) + (row0 + lr) * p.ldc + col0 + n;
+    const bool scale = p.alpha != 1.f;
+#pragma unroll
+    for (int it = 0; it < IT; ++it, cp += step) {
+      const int row = it * RPI + lr;
+      if (row >= rows_left) break;
+      float v[E];
+#pragma unroll
+      for (int q = 0; q < E / 4; ++q) {
+        const int ch = lc * (E / 4) + q;
+        const float4 a = stg[row * 8 + (ch ^ (row & 7))];
+        v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
       }
-      OutT* cp = reinterpret_cast<OutT*>(p.c) + (row0 + lr) * p.ldc + col0 + n;
-#pragma unroll 2
-      for (int it = 0; it < 32 / RPI; ++it, cp += step) {
-        const int row = it * RPI + lr;
-        if (row >= rows_left) break;
-        float v[E];
+      if (scale)
 #pragma unroll
-        for (int q = 0; q < E / 4; ++q) {
-          const int ch = lc * (E / 4) + q;
-          const float4 a = stg[row * 8 + (ch ^ (row & 7))];
-          v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+        for (int i = 0; i < E; ++i) v[i] *= p.alpha;
+      if constexpr (BIAS)
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] += b[i];
+      const long long rel = cp - reinterpret_cast<OutT*>(p.c);
+      if (valid >= E) {
+        if constexpr (DG) {
+          float x[E];
+          unpack_vec<OutT, E>(pa[it], x);
+#pragma unroll
+          for (int i = 0; i < E; ++i) v[i] *= gelu_grad_fast(x[i]);
         }
-        if (scale)
+        if constexpr (ACC) {
+          float o[E];
+          unpack_vec<OutT, E>(pc[it], o);
 #pragma unroll
-          for (int i = 0; i < E; ++i) v[i] *= p.alpha;
-        if constexpr (BIAS)
+          for (int i = 0; i < E; ++i) v[i] += o[i];
+        }
+        st_vec<OutT, E>(cp, v);
+        if constexpr (EPI == OASES_EPI_BIAS_GELU) {
 #pragma unroll
-          for (int i = 0; i < E; ++i) v[i] += b[i];
-        const long long rel = cp - reinterpret_cast<OutT*>(p.c);
-        if (valid >= E) {
-          if constexpr (EPI == OASES_EPI_DGELU) {
-            float x[E];
-            ld_vec<OutT, E>(reinterpret_cast<const OutT*>(p.aux) + rel, x);
+          for (int i = 0; i < E; ++i) v[i] = gelu_fast(v[i]);
+          st_vec<OutT, E>(reinterpret_cast<OutT*>(p.c2) + rel, v);
+        }
+      } else {
 #pragma unroll
-            for (int i = 0; i < E; ++i) v[i] *= gelu_grad_f(x[i]);
-          }
-          if constexpr (ACC) {
-            float o[E];
-            ld_vec<OutT, E>(cp, o);
-#pragma unroll
-            for (int i = 0; i < E; ++i) v[i] += o[i];
-          }
-          st_vec<OutT, E>(cp, v);
-          if constexpr (EPI == OASES_EPI_BIAS_GELU) {
-#pragma unroll
-            for (int i = 0; i < E; ++i) v[i] = gelu_f(v[i]);
-            st_vec<OutT, E>(reinterpret_cast<OutT*>(p.c2) + rel, v);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < E; ++i) {  // compile-time indices keep v[] in registers
-            if (i >= valid) break;
-            float x = v[i];
-            if constexpr (EPI == OASES_EPI_DGELU)
-              x *= gelu_grad_f(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
-            if constexpr (ACC) x += to_f(cp[i]);
-            cp[i] = from_f<OutT>(x);
-            if constexpr (EPI == OASES_EPI_BIAS_GELU)
-              reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_f(x));
-          }
+        for (int i = 0; i < E; ++i) {  // compile-time indices keep v[] in registers
+          if (i >= valid) break;
+          float x = v[i];
+          if constexpr (DG) x *= gelu_grad_fast(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
+          if constexpr (ACC) x += to_f(cp[i]);
+          cp[i] = from_f<OutT>(x);
+          if constexpr (EPI == OASES_EPI_BIAS_GELU)
+            reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_fast(x));
         }
       }
     }
-    __syncwarp();
   }
+  __syncwarp();
+}
+
+// One warp's 32-row x (32*NCH)-column stripe of an accumulator tile.
+// TMEM -> registers (thread = row) -> 128B-swizzled smem staging -> each lane
+// takes one 16-byte column group of a row, so a warp's global access covers
+// 32/LPR full row segments -> fused epilogue -> global.
+// Epilogues that READ global memory (the dGeLU pre-activation, the f32
+// accumulate of C) issue every load of a chunk before draining TMEM.
+template <typename OutT, int EPI, bool ACC, int NCH>
+__device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_base, int nbeg, uint32_t taddr,
+                                                float4* stg, int lane) {
+  using G = StripeGeo<OutT>;
+  const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
+  const long long row0 = p.c_row_off[0] * zo + p.c_row_off[1] * zi + m_base;
+  const long long col0 = p.c_col_off[0] * zo + p.c_col_off[1] * zi;
+  const int lr = lane / G::LPR, lc = lane % G::LPR;
+  const int rows_left = p.M - m_base;  // rows of this stripe inside the problem
+  const long long step = static_cast<long long>(G::RPI) * p.ldc;
+  const long long lane_base = (row0 + lr) * p.ldc + col0 + lc * G::E;  // element offset of (row lr, column 0)
+#pragma unroll 1
+  for (int c = 0; c < NCH; ++c)
+    epi_chunk<OutT, EPI, ACC>(p, c, nbeg, row0, col0, lr, lc, rows_left, step, lane_base, taddr, stg, lane);
 }
 
 // Calls BODY(OutT, EPI, ACC) for the runtime mode of p (compile-time specialised).
@@ -251,21 +338,13 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
     const int mode_ = ((p).c_f32 ? 8 : 0) + (p).epilogue * 2 + ((p).accumulate ? 1 : 0); \
     switch (mode_) {                                                                     \
       case 0: BODY(__nv_bfloat16, 0, false); break;                                      \
-      case 1: BODY(__nv_bfloat16, 0, true); break;                                       \
       case 2: BODY(__nv_bfloat16, 1, false); break;                                      \
-      case 3: BODY(__nv_bfloat16, 1, true); break;                                       \
       case 4: BODY(__nv_bfloat16, 2, false); break;                                      \
-      case 5: BODY(__nv_bfloat16, 2, true); break;                                       \
       case 6: BODY(__nv_bfloat16, 3, false); break;                                      \
-      case 7: BODY(__nv_bfloat16, 3, true); break;                                       \
       case 8: BODY(float, 0, false); break;                                              \
       case 9: BODY(float, 0, true); break;                                               \
       case 10: BODY(float, 1, false); break;                                             \
-      case 11: BODY(float, 1, true); break;                                              \
-      case 12: BODY(float, 2, false); break;                                             \
-      case 13: BODY(float, 2, true); break;                                              \
-      case 14: BODY(float, 3, false); break;                                             \
-      default: BODY(float, 3, true); break;                                              \
+      default: BODY(float, 1, true); break;                                              \
     }                                                                                    \
   } while (0)
 
@@ -285,7 +364,7 @@ __device__ __forceinline__ void epilogue_role_single(const TcParams& p, uint64_t
     tc_fence_after();
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                            static_cast<uint32_t>(acc * BN + half * (BN / 2));
-    epilogue_stripe<OutT, EPI, ACC>(p, ti.z, ti.m0 + q * 32, ti.n0 + half * (BN / 2), BN / 2, taddr, stg, lane);
+    epilogue_stripe<OutT, EPI, ACC, BN / 64>(p, ti.z, ti.m0 + q * 32, ti.n0 + half * (BN / 2), taddr, stg, lane);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -469,7 +548,7 @@ __device__ __forceinline__ void pair_tile_epilogue(const TcParams& p, int lt, ui
   int z, m0, n0;
   pair_decode(p, lt, z, m0, n0);
   const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
-  epilogue_stripe<OutT, EPI, ACC>(p, z, mb, n0 + half * (PAIR_BN / 2), PAIR_BN / 2, taddr, stg, lane);
+  epilogue_stripe<OutT, EPI, ACC, PAIR_BN / 64>(p, z, mb, n0 + half * (PAIR_BN / 2), taddr, stg, lane);
 }
 
 // Producer: TMA of one k-block of a tile (compile-time operand layout).
@@ -788,6 +867,16 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
   }
   if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_DGELU) {
     *err = "gemm_tc: unknown epilogue";
+    return false;
+  }
+  // Instantiated epilogue modes (OASES_EPI_DISPATCH): bf16 output without
+  // accumulation (any epilogue); f32 output with NONE or BIAS, +-accumulate.
+  if (d.c_dtype != OASES_F32 && d.accumulate) {
+    *err = "gemm_tc: accumulate needs an f32 output";
+    return false;
+  }
+  if (d.c_dtype == OASES_F32 && d.epilogue != OASES_EPI_NONE && d.epilogue != OASES_EPI_BIAS) {
+    *err = "gemm_tc: f32 output supports the NONE and BIAS epilogues only";
     return false;
   }
   const int BN = (d.N <= 128) ? 128 : 256;

@@ -9,6 +9,7 @@
 // fraction, exposed communication by the same interval algebra as
 // simulate() (sim.cpp:178-199), and the device bytes of the stack.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <set>
 
@@ -161,7 +162,11 @@ bool Executor::capture_graph() {
     throw;
   }
   check_cuda(cudaStreamEndCapture(c.compute, &graph_), "end capture");
-  check_cuda(cudaGraphInstantiate(&graph_exec_, graph_, 0), "instantiate");
+  // Keep the per-node stream priorities of the capture (comm stream highest)
+  // instead of running every node at the launching stream's priority.
+  const char* np = std::getenv("OASES_GRAPH_NODE_PRIO");
+  const unsigned long long flags = (np && np[0] == '0') ? 0ull : static_cast<unsigned long long>(cudaGraphInstantiateFlagUseNodePriority);
+  check_cuda(cudaGraphInstantiateWithFlags(&graph_exec_, graph_, flags), "instantiate");
   return true;
 }
 
