@@ -162,6 +162,13 @@ SchedulePlan schedule_intra_pass(const ModelGraph& graph);
 SchedulePlan schedule_cross_pass(const ModelGraph& graph);
 SchedulePlan schedule_oases(const ModelGraph& graph);
 SchedulePlan make_schedule(const ModelGraph& graph, ScheduleVariant variant);
+// Extension (fine-grained recomputation): per layer unit,
+// keep[u] keeps the unit's interior post-AllReduce tensors (Oases: recompute
+// from them, no collective) or replays the unit from its input with its
+// recompute AllReduces (CrossPass). All-true == schedule_oases, all-false ==
+// schedule_cross_pass; a mixed plan carries variant CrossPass.
+SchedulePlan schedule_oases_policy(const ModelGraph& graph, const std::vector<bool>& keep);
+int layer_unit_count(const ModelGraph& graph);
 
 struct Violation {
   std::string code;
@@ -207,6 +214,15 @@ Breakdown breakdown(const SimResult& result);
 // measured-trace path of execute().
 double exposed_comm_time(std::vector<std::pair<double, double>> compute,
                          std::vector<std::pair<double, double>> comm);
+
+// Extension: the policy choosing keep[] under an HBM budget (host/policy.cpp).
+struct RecomputePolicy {
+  std::vector<bool> keep;
+  double predicted_time = 0.0;
+  double predicted_memory = 0.0;
+};
+RecomputePolicy choose_recompute_policy(const ModelGraph& graph, const CostVectors& costs, const Strategy& strategy,
+                                        double budget_bytes, SimOptions options = {});
 
 // ------------------------------------------------------------- planner.hpp:18-82
 struct EdgeCostMatrix {

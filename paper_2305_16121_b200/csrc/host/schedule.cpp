@@ -260,42 +260,55 @@ void save_per_unit(Emitter& e, const std::vector<std::pair<int, int>>& units, in
   }
 }
 
-SchedulePlan build_pipelined(const ModelGraph& g, ScheduleVariant v) {
+// `keep[u]` (per layer unit, Oases/CrossPass only): the unit's interior
+// post-AllReduce tensors stay in HBM, so its recompute starts from them and
+// replays no collective (Oases, Eq. 1); otherwise the unit is replayed from
+// its input with the recompute AllReduces (CrossPass). All-true is Oases,
+// all-false CrossPass; a mixed vector is the fine-grained memory policy
+// (SURVEY.md 8(f) F4), built with the same weave and dependency rules.
+SchedulePlan build_pipelined(const ModelGraph& g, ScheduleVariant v, const std::vector<bool>* keep_in = nullptr) {
   Emitter e(g, v, /*split=*/true);
   if (g.block_count() == 0) return e.plan();
-  const bool oases = v == ScheduleVariant::Oases;
   const bool rec = g.recompute_enabled;
   const auto units = layer_units(g);
+  std::vector<bool> keep(units.size(), v == ScheduleVariant::Oases);
+  if (keep_in) keep = *keep_in;
+  std::vector<int> unit_of(static_cast<std::size_t>(g.block_count()));
+  for (std::size_t u = 0; u < units.size(); ++u)
+    for (int b = units[u].first; b <= units[u].second; ++b) unit_of[static_cast<std::size_t>(b)] = static_cast<int>(u);
+  auto kept = [&](int b) { return static_cast<bool>(keep[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(b)])]); };
 
   DataDeps deps{g, e, [&](int b, int sb) -> int {
-                  if (oases) return b > 0 ? e.comm(Pass::Forward, b - 1, sb) : kNone;  // stored post-AR tensor
-                  for (const auto& [first, last] : units) {
-                    (void)last;
-                    if (b == first) return first > 0 ? e.comm(Pass::Forward, first - 1, sb) : kNone;
-                  }
+                  const auto& unit = units[static_cast<std::size_t>(unit_of[static_cast<std::size_t>(b)])];
+                  // stored post-AR tensor (kept unit, or the unit's own input)
+                  if (kept(b) || b == unit.first) return b > 0 ? e.comm(Pass::Forward, b - 1, sb) : kNone;
                   return e.comm(Pass::Recompute, b - 1, sb);  // replayed comm inside the unit
                 }};
 
   e.weave(forward_steps(g), 0, deps);
   if (rec) {
-    if (oases) {
-      for (int b = 0; b < g.block_count(); ++b)
-        for (int sb = 0; sb < 2; ++sb) e.plan().saved_sequences.push_back(e.forward_ids(b, sb));
-    } else {
-      save_per_unit(e, units, 2);
+    for (std::size_t u = 0; u < units.size(); ++u) {
+      if (keep[u]) {
+        for (int b = units[u].first; b <= units[u].second; ++b)
+          for (int sb = 0; sb < 2; ++sb) e.plan().saved_sequences.push_back(e.forward_ids(b, sb));
+      } else {
+        save_per_unit(e, {units[u]}, 2);
+      }
     }
   }
 
   e.enter_backward();
-  if (oases || v == ScheduleVariant::CrossPass || !rec) {
+  if (keep_in || v == ScheduleVariant::Oases || v == ScheduleVariant::CrossPass || !rec) {
     Program bwd;
-    if (oases || !rec) {
-      for (int b = g.block_count() - 1; b >= 0; --b) {
-        if (rec) add_recompute(g, b, /*replay_comm=*/false, bwd);
-        add_backward(g, b, bwd);
-      }
-    } else {
-      for (auto it = units.rbegin(); it != units.rend(); ++it) {
+    for (auto it = units.rbegin(); it != units.rend(); ++it) {
+      if (!rec) {
+        for (int b = it->second; b >= it->first; --b) add_backward(g, b, bwd);
+      } else if (kept(it->first)) {
+        for (int b = it->second; b >= it->first; --b) {
+          add_recompute(g, b, /*replay_comm=*/false, bwd);
+          add_backward(g, b, bwd);
+        }
+      } else {
         for (int b = it->first; b <= it->second; ++b) add_recompute(g, b, true, bwd);
         for (int b = it->second; b >= it->first; --b) add_backward(g, b, bwd);
       }
@@ -351,6 +364,19 @@ SchedulePlan schedule_default(const ModelGraph& g) {
 SchedulePlan schedule_intra_pass(const ModelGraph& g) { return build_pipelined(g, ScheduleVariant::IntraPass); }
 SchedulePlan schedule_cross_pass(const ModelGraph& g) { return build_pipelined(g, ScheduleVariant::CrossPass); }
 SchedulePlan schedule_oases(const ModelGraph& g) { return build_pipelined(g, ScheduleVariant::Oases); }
+
+SchedulePlan schedule_oases_policy(const ModelGraph& g, const std::vector<bool>& keep) {
+  const auto units = layer_units(g);
+  if (keep.size() != units.size())
+    throw ConfigError("schedule_oases_policy: keep has " + std::to_string(keep.size()) + " entries, the model has " +
+                      std::to_string(units.size()) + " layer units");
+  const bool all = std::all_of(keep.begin(), keep.end(), [](bool k) { return k; });
+  // a plan that replays any collective is labelled CrossPass (validate_plan
+  // forbids recompute comms only in Oases plans)
+  return build_pipelined(g, all ? ScheduleVariant::Oases : ScheduleVariant::CrossPass, &keep);
+}
+
+int layer_unit_count(const ModelGraph& g) { return static_cast<int>(layer_units(g).size()); }
 
 SchedulePlan make_schedule(const ModelGraph& g, ScheduleVariant v) {
   switch (v) {

@@ -80,6 +80,14 @@ Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stac
     e.waits.assign(waits.begin(), waits.end());
     ops_.push_back(std::move(e));
   }
+  // Residual-stream storage: x_b stays in its own HBM buffer unless the plan
+  // rebuilds it from a replayed AllReduce (interior of a CrossPass unit).
+  {
+    std::vector<bool> stored(static_cast<size_t>(stack.num_blocks()), true);
+    for (const ExecOp& e : ops_)
+      if (e.kind == OpKind::RecomputeCompute && e.rebuild_x) stored[static_cast<size_t>(e.block)] = false;
+    stack.bind_storage(stored);
+  }
   // LN_0 backward tail: after the last backward comm (or compute) of block 0.
   for (int id = 0; id < n; ++id) {
     const auto& op = plan.op(id);

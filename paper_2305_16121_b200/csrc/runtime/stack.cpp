@@ -228,11 +228,11 @@ void Stack::alloc_all() {
     }
     w.input = arena_.alloc(static_cast<size_t>(T * h) * es);
     w.grad = arena_.alloc(static_cast<size_t>(T * h) * es);
-    w.xs.resize(static_cast<size_t>(nblocks_));
-    for (int b = 0; b < nblocks_; ++b) {
-      void* base = b == 0 ? w.input : arena_.alloc(static_cast<size_t>(T * h) * es);
-      w.xs[static_cast<size_t>(b)] = {half(base, 0, h), half(base, 1, h)};
-    }
+    // x_0 aliases the input; the other residual-stream buffers are placed by
+    // bind_storage (all dedicated until a plan is bound)
+    w.xs.assign(static_cast<size_t>(nblocks_), {nullptr, nullptr});
+    w.x_own.assign(static_cast<size_t>(nblocks_), {nullptr, nullptr});
+    if (nblocks_ > 0) w.xs[0] = w.x_own[0] = {half(w.input, 0, h), half(w.input, 1, h)};
     for (int par = 0; par < 2; ++par) {
       void* f = arena_.alloc(static_cast<size_t>(T * h) * es);
       void* bb = arena_.alloc(static_cast<size_t>(T * h) * es);
@@ -272,6 +272,35 @@ void Stack::alloc_all() {
     w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
   }
   check_cuda(cudaDeviceSynchronize(), "stack allocation");
+  // residual-stream buffers of blocks > 0 are placed when a plan is bound
+  x_stored_.assign(static_cast<size_t>(nblocks_), false);
+  if (nblocks_ > 0) x_stored_[0] = true;
+}
+
+void Stack::bind_storage(const std::vector<bool>& stored) {
+  if (static_cast<int>(stored.size()) != nblocks_) throw ConfigError("bind_storage: one flag per block");
+  const int64_t T = 2 * tokens_sub(), h = cfg_.h;
+  const size_t bytes = static_cast<size_t>(T * h) * esize();
+  for (Worker& w : workers_) {
+    for (int b = 1; b < nblocks_; ++b) {
+      auto& own = w.x_own[static_cast<size_t>(b)];
+      if (stored[static_cast<size_t>(b)]) {
+        if (!own[0]) {
+          void* base = arena_.alloc(bytes);
+          own = {half(base, 0, h), half(base, 1, h)};
+        }
+        w.xs[static_cast<size_t>(b)] = own;
+      } else {
+        if (!w.x_scratch[0]) {
+          void* base = arena_.alloc(bytes);
+          w.x_scratch = {half(base, 0, h), half(base, 1, h)};
+        }
+        w.xs[static_cast<size_t>(b)] = w.x_scratch;
+      }
+    }
+  }
+  x_stored_ = stored;
+  if (nblocks_ > 0) x_stored_[0] = true;
 }
 
 Workspace& Stack::ws_for(Worker& w, int block, int sb) {
@@ -501,6 +530,9 @@ void download(const void* dev, int dtype, int64_t n, double* host) {
 void Stack::get_input_grad(double* host) { download(workers_[0].grad, dtype(), 2 * tokens_sub() * cfg_.h, host); }
 
 void Stack::get_activation(int worker, int block, int sb, double* host) {
+  if (block >= 0 && block < nblocks_ && !x_stored_[static_cast<size_t>(block)])
+    throw ConfigError("activation: x_" + std::to_string(block) +
+                      " is not kept by the bound plan (rebuilt in recompute; bind an Oases plan to read it)");
   if (worker < 0 || worker >= num_workers() || block < 0 || block > nblocks_ || sb < 0 || sb > 1)
     throw ConfigError("get_activation: index out of range");
   Worker& w = workers_[static_cast<size_t>(worker)];

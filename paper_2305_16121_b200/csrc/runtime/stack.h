@@ -80,8 +80,13 @@ struct Workspace {
 struct Worker {
   int rank = 0;
   std::vector<BlockParams> params;
-  // saved residual stream x_b per sub-batch (b = 0..nblocks-1), x_0 aliases input
+  // residual stream x_b per sub-batch (b = 0..nblocks-1), x_0 aliases input.
+  // Blocks whose x_b the bound plan keeps until backward own a buffer; the
+  // others (interior tensors of CrossPass-replayed layer units) share
+  // x_scratch, rebuilt by their recompute (Stack::bind_storage).
   std::vector<std::array<void*, 2>> xs;
+  std::vector<std::array<void*, 2>> x_own;  // dedicated buffers, allocated on first need
+  std::array<void*, 2> x_scratch = {};
   std::array<void*, 2> fwd_ar[2] = {}, rec_ar[2] = {}, bwd_ar[2] = {};  // [block parity][sb]
   std::vector<std::array<Workspace, 2>> ws;  // [slot][sb]
   void* input = nullptr;                     // [T, h]
@@ -122,6 +127,10 @@ class Stack {
   void set_input(const void* host, int host_dtype, cudaStream_t st);
   void get_input_grad(double* host);
   void get_activation(int worker, int block, int sb, double* host);
+  // Residual-stream storage for a plan: stored[b] (b > 0) keeps x_b in its own
+  // HBM buffer from forward to backward; false maps it onto a scratch buffer
+  // (the plan rebuilds it in recompute). Called by plan_bind.
+  void bind_storage(const std::vector<bool>& stored);
 
   // ---- per-op kernel lists (issued on ctx.compute for every worker) ----
   void forward(int worker, int block, int sb, bool with_bdr, bool with_row);
@@ -166,6 +175,7 @@ class Stack {
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;
+  std::vector<bool> x_stored_;  // [block] x_b readable after a step (bind_storage)
   int64_t launches_ = 0;
   bool timing_ = false;
   size_t timed_ = 0;

@@ -87,8 +87,23 @@ def graph_for(cfg: ModelConfig):
     return t.build_block_graph(ops, spec)
 
 
-def plan_for(cfg: ModelConfig, variant="Oases"):
+def plan_for(cfg: ModelConfig, variant="Oases", keep=None):
+    """Schedule for `cfg`. keep: per layer unit, keep its interior post-AllReduce
+    tensors (Oases) or replay the unit with its AllReduces (CrossPass); the
+    fine-grained recomputation policy (tmpsim.schedule_oases_policy)."""
+    if keep is not None:
+        return t.schedule_oases_policy(graph_for(cfg), [bool(k) for k in keep])
     return t.make_schedule(graph_for(cfg), VARIANTS[variant] if isinstance(variant, str) else variant)
+
+
+def recompute_policy(cfg: ModelConfig, budget_bytes: float, *, tp: int = 1, costs=None, profile=None):
+    """Per-layer keep/replay choice under an HBM budget (tmpsim.choose_recompute_policy)
+    on `costs` (analytic build_cost_vectors of `profile` unless given, e.g. calibrated
+    rows loaded with load_measured_costs)."""
+    graph = graph_for(cfg)
+    if costs is None:
+        costs = t.build_cost_vectors(graph, cfg.spec(), profile or t.b200_profile(max(tp, 1)))
+    return t.choose_recompute_policy(graph, costs, t.Strategy([tp] * graph.block_count()), float(budget_bytes))
 
 
 class _FlatPlan:
