@@ -179,6 +179,18 @@ oases_status oases_bias_dropout_residual_fwd(int dtype, const void* x, const voi
                                              const void* residual, void* out, int64_t rows,
                                              int64_t cols, float dropout_p, uint64_t seed,
                                              uint64_t offset, void* stream);
+/* Fused: x_out = residual + dropout(x + bias) (as oases_bias_dropout_residual_fwd)
+ * and y = LayerNorm(x_out) (bit-identical to oases_layernorm_fwd of x_out), one
+ * HBM pass. The block-boundary step of the layer (SURVEY.md 8(a) block
+ * partition: bias-dropout-residual on AR_{b-1}, then LN_b). Shapes the fused
+ * kernel does not cover (cols % 16, or cols/16 not a multiple of 32 up to
+ * 4*256) return OASES_ERR_CONFIG; callers then issue the two kernels. */
+oases_status oases_bias_dropout_residual_layernorm_fwd(int dtype, const void* x, const void* bias,
+                                                       const void* residual, void* x_out,
+                                                       const void* gamma, const void* beta, void* y,
+                                                       int64_t rows, int64_t cols, float eps,
+                                                       float dropout_p, uint64_t seed, uint64_t offset,
+                                                       void* stream);
 /* dx = dropout'(dout); dbias (+)= column sums of dx (deterministic). */
 oases_status oases_bias_dropout_residual_bwd(int dtype, const void* dout, void* dx, float* dbias,
                                              int acc_bias, float* workspace, int64_t rows,

@@ -197,6 +197,9 @@ _SIGNATURES = [
                                      C.c_float, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     ("oases_softmax_bwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_float,
                                      C.c_float, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+    ("oases_bias_dropout_residual_layernorm_fwd", C.c_int,
+     [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+      C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint64, C.c_void_p]),
     ("oases_bias_dropout_residual_fwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                    C.c_int64, C.c_float, C.c_uint64, C.c_uint64, C.c_void_p]),
     ("oases_bias_dropout_residual_bwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,

@@ -39,8 +39,10 @@ namespace oases {
 namespace {
 
 constexpr int kTile = 128;
-constexpr int kRowWarps = 8;                    // two warps per TMEM lane quarter, 64 columns each
+constexpr int kRowWarps = 8;                    // backward: two warps per TMEM lane quarter, 64 columns each
 constexpr int kThreads = 64 + 32 * kRowWarps;  // + TMA warp + MMA warp
+constexpr int kFwdRowWarps = 16;                      // forward: four warps per lane quarter, 32 columns each
+constexpr int kFwdThreads = 64 + 32 * kFwdRowWarps;  // 18 warps: 4-5 per scheduler hide the softmax latency
 constexpr float kLog2e = 1.44269504088896341f;
 
 struct AttnParams {
@@ -96,6 +98,42 @@ __device__ __forceinline__ void philox_init(const AttnParams& p, PhiloxState& ps
   ps.o1 = static_cast<uint32_t>(p.offset >> 32);
   ps.thr4 = p.thr * 0x01010101u;
 }
+// Same Philox with the round keys derived on the fly (two adds per round
+// instead of 20 live registers) for the register-tight forward row warps.
+struct PhiloxLite {
+  uint32_t s0, s1, o0, o1, thr4;
+};
+__device__ __forceinline__ void philox_init(const AttnParams& p, PhiloxLite& ps) {
+  ps.s0 = static_cast<uint32_t>(p.seed);
+  ps.s1 = static_cast<uint32_t>(p.seed >> 32);
+  ps.o0 = static_cast<uint32_t>(p.offset);
+  ps.o1 = static_cast<uint32_t>(p.offset >> 32);
+  ps.thr4 = p.thr * 0x01010101u;
+}
+__device__ __forceinline__ void keep_masks16(const PhiloxLite& ps, unsigned long long ctr, uint32_t (&m)[8]) {
+  uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = ps.o0, c3 = ps.o1;
+  uint32_t k0 = ps.s0, k1 = ps.s1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = static_cast<unsigned long long>(0xD2511F53u) * c0;
+    const unsigned long long p1 = static_cast<unsigned long long>(0xCD9E8D57u) * c2;
+    const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ k1;
+    c1 = static_cast<uint32_t>(p1);
+    c3 = static_cast<uint32_t>(p0);
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint32_t u[4] = {c0, c1, c2, c3};
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t k = __vcmpgeu4(u[w], ps.thr4);
+    m[2 * w] = __byte_perm(k, 0, 0x1100);
+    m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
+  }
+}
 // Keep masks of 16 consecutive elements (Philox counter ctr) as 8 bf16x2 lane
 // masks: m[k] covers elements 2k (low half) and 2k+1.
 __device__ __forceinline__ void keep_masks16(const PhiloxState& ps, unsigned long long ctr, uint32_t (&m)[8]) {
@@ -135,8 +173,8 @@ struct FwdCfg {
   static constexpr int K_OFF = 2 * TILE_BYTES;           // [2]
   static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;   // [2]
   static constexpr int P_OFF = V_OFF + 2 * TILE_BYTES;
-  static constexpr int RED_OFF = P_OFF + kTile * kTile * 2;  // row-sum exchange [2][128]
-  static constexpr int BAR_OFF = RED_OFF + 1024;
+  static constexpr int RED_OFF = P_OFF + kTile * kTile * 2;  // row max / row sum exchange [4 parts][128 rows]
+  static constexpr int BAR_OFF = RED_OFF + 4 * kTile * 4;
   static constexpr int SMEM = BAR_OFF + 256;
   static constexpr uint32_t TMEM_COLS = 512;  // S x2 (256) + O x2 (2*DH)
 };
@@ -147,7 +185,7 @@ struct FwdCfg {
 // item's loads and first QK^T run under the current item's last softmax and
 // epilogue.
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, const AttnParams p) {
   using C = FwdCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -183,10 +221,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], kRowWarps);
-      mbar_init(&o_free[s], kRowWarps);
+      mbar_init(&s_empty[s], kFwdRowWarps);
+      mbar_init(&o_free[s], kFwdRowWarps);
     }
-    mbar_init(p_full, kRowWarps);
+    mbar_init(p_full, kFwdRowWarps);
     mbar_init(pv_done, 1);
     fence_barrier_init();
   }
@@ -306,14 +344,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ row warps: query row r, key columns [c0, c0 + 64)
-    const int q = warp & 3, hf = (warp - 2) >> 2;
+    // ------------------------------------------------ row warps
+    // Warp w owns TMEM lane quarter q = w % 4 (query rows 32q .. 32q+31 of the
+    // tile; one row per thread), key columns [32 part, 32 part + 32) of every
+    // S tile and O columns [part DH/4, (part+1) DH/4). The four warps of a
+    // quarter combine their partial row maxima / sums through smem.
+    const int q = warp & 3, part = (warp - 2) >> 2;
     const int rr = q * 32 + lane;
-    const int c0 = hf * 64;
+    const int c0 = part * 32;
+    constexpr int OC = DH / 4;  // O columns per warp
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
     uint8_t* pbuf = smem + C::P_OFF;
-    float* xsum = reinterpret_cast<float*>(smem + C::RED_OFF);  // [half][row]
-    PhiloxState ph;
+    float* red = reinterpret_cast<float*>(smem + C::RED_OFF);  // [part][row]
+    PhiloxLite ph;
     philox_init(p, ph);
     int g = 0;
     for (int r = 0, k = 0;; ++r, ++k) {
@@ -324,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
       const int i = qt * kTile + rr;
       const int ob = k & 1;
-      const uint32_t to = tl + 2 * kTile + ob * DH + hf * (DH / 2);  // this warp's half of O
+      const uint32_t to = tl + 2 * kTile + ob * DH + part * OC;  // this warp's columns of O
       const unsigned long long ebase =
           (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i) *
               static_cast<unsigned long long>(p.seq) +
@@ -334,36 +377,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = g & 1;
         mbar_wait(&s_full[st], (g >> 1) & 1);
         tc_fence_after();
-        // the row max needs all 128 keys: read the partner half too (TMEM reads are cheap)
-        uint32_t u[2][32], w[2][32];
-        tmem_ld32(tl + st * kTile + c0, u[0]);
-        tmem_ld32(tl + st * kTile + c0 + 32, u[1]);
-        tmem_ld32(tl + st * kTile + (c0 ^ 64), w[0]);
-        tmem_ld32(tl + st * kTile + (c0 ^ 64) + 32, w[1]);
+        uint32_t u[32];
+        tmem_ld32(tl + st * kTile + c0, u);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[st]);
         if (j == qt) {
-          int lim = rr - c0, limw = rr - (c0 ^ 64);  // keys > row are masked
-          asm volatile("" : "+r"(lim), "+r"(limw));  // keep the comparisons inside the (rare) diagonal branch
+          int lim = rr - c0;                   // keys > row are masked
+          asm volatile("" : "+r"(lim));        // keep the comparisons inside the (rare) diagonal branch
 #pragma unroll
-          for (int kk = 0; kk < 64; ++kk) {
-            if (kk > lim) u[kk >> 5][kk & 31] = __float_as_uint(-INFINITY);
-            if (kk > limw) w[kk >> 5][kk & 31] = __float_as_uint(-INFINITY);
-          }
+          for (int kk = 0; kk < 32; ++kk)
+            if (kk > lim) u[kk] = __float_as_uint(-INFINITY);
         }
-        float mloc;
-        {  // 8 independent partial maxima (short dependency chains)
-          float mp[8];
+        float mpart;
+        {  // 4 independent partial maxima (short dependency chains)
+          float mp[4];
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mp[kk] = fmaxf(__uint_as_float(u[0][kk]), __uint_as_float(w[0][kk]));
+          for (int kk = 0; kk < 4; ++kk) mp[kk] = __uint_as_float(u[kk]);
 #pragma unroll
-          for (int kk = 8; kk < 64; ++kk)
-            mp[kk & 7] =
-                fmaxf(mp[kk & 7], fmaxf(__uint_as_float(u[kk >> 5][kk & 31]), __uint_as_float(w[kk >> 5][kk & 31])));
-          mloc = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+          for (int kk = 4; kk < 32; ++kk) mp[kk & 3] = fmaxf(mp[kk & 3], __uint_as_float(u[kk]));
+          mpart = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
         }
+        named_bar_sync(1 + q, 128);  // the quarter's previous partials are consumed
+        red[part * kTile + rr] = mpart;
+        named_bar_sync(1 + q, 128);
+        const float mloc = fmaxf(fmaxf(red[rr], red[kTile + rr]), fmaxf(red[2 * kTile + rr], red[3 * kTile + rr]));
         // Conditional rescaling: keep the running max unless the row max grew by
         // more than 8 (log2 units). P = exp2(s - m) then stays <= 256 (exact in
         // bf16's range) and O, l are rescaled only when it pays; the result is
@@ -372,21 +411,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mx = cand > m + 8.f ? cand : m;
         const float alpha = ex2(m - mx);
         const float nmx = -mx;
-        float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[32];
+        float sp[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[16];
 #pragma unroll
-        for (int kk = 0; kk < 64; kk += 2) {
-          const float a = ex2(fmaf(__uint_as_float(u[kk >> 5][kk & 31]), p.sl2, nmx));
-          const float b = ex2(fmaf(__uint_as_float(u[kk >> 5][(kk & 31) + 1]), p.sl2, nmx));
-          sp[(kk >> 1) & 7] += a + b;
+        for (int kk = 0; kk < 32; kk += 2) {
+          const float a = ex2(fmaf(__uint_as_float(u[kk]), p.sl2, nmx));
+          const float b = ex2(fmaf(__uint_as_float(u[kk + 1]), p.sl2, nmx));
+          sp[(kk >> 1) & 3] += a + b;
           pk[kk >> 1] = pack_bf16(a, b);
         }
-        const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
+        const float sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
         l = l * alpha + sum;
         m = mx;
         if (p.thr) {
 #pragma unroll
-          for (int gq = 0; gq < 4; ++gq) {
+          for (int gq = 0; gq < 2; ++gq) {
             uint32_t km[8];
             keep_masks16(ph, (ebase + static_cast<unsigned long long>(j) * kTile + gq * 16) >> 4, km);
 #pragma unroll
@@ -400,51 +439,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           // O holds P_{j-1} V_{j-1}: rescale it to the new reference max
-#pragma unroll
-          for (int c = 0; c < DH / 64; ++c) {
+          if constexpr (OC == 32) {
             uint32_t o[32];
-            tmem_ld32(to + c * 32, o);
+            tmem_ld32(to, o);
             tmem_wait_ld();
 #pragma unroll
             for (int kk = 0; kk < 32; ++kk) o[kk] = __float_as_uint(__uint_as_float(o[kk]) * alpha);
-            tmem_st32(to + c * 32, o);
+            tmem_st32(to, o);
+          } else {
+            uint32_t o[16];
+            tmem_ld16(to, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) o[kk] = __float_as_uint(__uint_as_float(o[kk]) * alpha);
+            tmem_st16(to, o);
           }
           tmem_wait_st();
         }
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
-          *tile_chunk(pbuf, rr, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        for (int ch = 0; ch < 4; ++ch)
+          *tile_chunk(pbuf, rr, part * 4 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
         fence_proxy_async();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
       }
       // ---- item epilogue: O / l -> ctx, lse
-      xsum[hf * 128 + rr] = l;
-      named_bar_sync(1 + q, 64);
-      const float lt = l + xsum[(hf ^ 1) * 128 + rr];
+      named_bar_sync(1 + q, 128);
+      red[part * kTile + rr] = l;
+      named_bar_sync(1 + q, 128);
+      const float lt = (red[rr] + red[kTile + rr]) + (red[2 * kTile + rr] + red[3 * kTile + rr]);
       mbar_wait(pv_done, (g - 1) & 1);
       tc_fence_after();
       const float inv = p.ks / lt;
       __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + i) * p.ld_out +
-                            p.do_col + jl * DH + hf * (DH / 2);
+                            p.do_col + jl * DH + part * OC;
+      uint32_t o[OC];
+      if constexpr (OC == 32) tmem_ld32(to, o);
+      else tmem_ld16(to, o);
+      tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < DH / 64; ++c) {
-        uint32_t o[32];
-        tmem_ld32(to + c * 32, o);
-        tmem_wait_ld();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const float* f = reinterpret_cast<const float*>(o + 8 * kk);
-          *reinterpret_cast<uint4*>(orow + c * 32 + kk * 8) =
-              make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
-                         pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
-        }
+      for (int kk = 0; kk < OC / 8; ++kk) {
+        const float* f = reinterpret_cast<const float*>(o + 8 * kk);
+        *reinterpret_cast<uint4*>(orow + kk * 8) =
+            make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                       pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[ob]);
-      if (hf == 0) p.lse[static_cast<long long>(z) * p.seq + i] = m + log2f(lt);
+      if (part == 0) p.lse[static_cast<long long>(z) * p.seq + i] = m + log2f(lt);
     }
   }
   tc_fence_before();
@@ -850,13 +894,13 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
   if (d.head_dim == 128) {
     static cudaError_t once = set_smem(attn_fwd_kernel<128>, FwdCfg<128>::SMEM);
     if ((e = once) == cudaSuccess) {
-      attn_fwd_kernel<128><<<grid, kThreads, FwdCfg<128>::SMEM, stream>>>(tqkv, p);
+      attn_fwd_kernel<128><<<grid, kFwdThreads, FwdCfg<128>::SMEM, stream>>>(tqkv, p);
       e = cudaGetLastError();
     }
   } else {
     static cudaError_t once = set_smem(attn_fwd_kernel<64>, FwdCfg<64>::SMEM);
     if ((e = once) == cudaSuccess) {
-      attn_fwd_kernel<64><<<grid, kThreads, FwdCfg<64>::SMEM, stream>>>(tqkv, p);
+      attn_fwd_kernel<64><<<grid, kFwdThreads, FwdCfg<64>::SMEM, stream>>>(tqkv, p);
       e = cudaGetLastError();
     }
   }

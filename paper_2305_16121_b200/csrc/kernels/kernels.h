@@ -8,6 +8,14 @@
 
 namespace oases {
 
+// Fused bias-dropout-residual + LayerNorm forward: xout = res + dropout(in + bias)
+// (as bias_dropout_residual_fwd), y = LN(xout) (bit-identical to layernorm_fwd
+// of xout). cudaErrorNotSupported when bdr_layernorm_supported() is false.
+bool bdr_layernorm_supported(long long rows, int cols);
+cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
+                                                void* xout, const void* gamma, const void* beta, void* y,
+                                                long long rows, int cols, float eps, float p, uint64_t seed,
+                                                uint64_t offset, cudaStream_t st);
 cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, long long rows,
                           int cols, float eps, cudaStream_t st);
 size_t layernorm_bwd_workspace(long long rows, int cols);

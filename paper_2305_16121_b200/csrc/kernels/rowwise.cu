@@ -807,6 +807,132 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   return cudaGetLastError();
 }
 
+// Row-group LayerNorm forward: TPR = cols / (16 NV) threads per row, 16 NV
+// consecutive-by-16 elements per thread (one Philox dropout counter per 16),
+// RB = 256 / TPR rows per 256-thread block; exact two-pass f32 statistics with
+// fixed-order reductions. BDR fuses the producing bias-dropout-residual
+// (x = res + dropout(in + bias), the bdr_fwd16 arithmetic in the same order)
+// and stores x: HBM traffic read in+res / write x+y instead of a separate
+// bias-dropout-residual pass plus a re-read of x. The plain and fused variants
+// share every f32 operation of the normalisation, so LN(x) is bit-identical
+// whichever kernel produced x (Oases recompute == CrossPass replay).
+template <typename T, int NV, bool BDR>
+__global__ void __launch_bounds__(256) ln_rows_kernel(const T* __restrict__ in, const T* __restrict__ bias,
+                                                      const T* __restrict__ res, T* __restrict__ xout,
+                                                      const T* __restrict__ gamma, const T* __restrict__ beta,
+                                                      T* __restrict__ y, long long rows, int cols, float eps,
+                                                      uint32_t thr, float ks, int drop, uint64_t seed,
+                                                      uint64_t offset) {
+  __shared__ float sm[2][8][8];  // [statistic][row of the block][warp of the row]
+  const int tpr = cols / (16 * NV), rb = 256 / tpr, wpr = tpr / 32;
+  const int sub = threadIdx.x / tpr, t = threadIdx.x - sub * tpr, wi = t >> 5;
+  const long long row = static_cast<long long>(blockIdx.x) * rb + sub;
+  const bool ok = row < rows;
+  const long long base = row * cols;
+  float v[NV][16];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * tpr + t) * 16;
+    if (!ok) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[k][e] = 0.f;
+      continue;
+    }
+    load16(in + base + c, v[k]);
+    if constexpr (BDR) {
+      if (bias) {
+        float b[16];
+        load16(bias + c, b);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[k][e] += b[e];
+      }
+      if (drop) apply_dropout16(v[k], static_cast<unsigned long long>(base + c), seed, offset, thr, ks);
+      if (res) {
+        float r[16];
+        load16(res + base + c, r);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[k][e] += r[e];
+      }
+      store16(xout + base + c, v[k]);
+      if constexpr (sizeof(T) == 2) {  // normalise the stored (rounded) x, exactly what a re-read would see
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[k][e] = __bfloat162float(__float2bfloat16_rn(v[k][e]));
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) s += v[k][e];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sm[0][sub][wi] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int w = 0; w < wpr; ++w) s += sm[0][sub][w];
+  const float mean = s / static_cast<float>(cols);
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) q += (v[k][e] - mean) * (v[k][e] - mean);
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) sm[1][sub][wi] = q;
+  __syncthreads();
+  q = 0.f;
+  for (int w = 0; w < wpr; ++w) q += sm[1][sub][w];
+  if (!ok) return;
+  const float rstd = rsqrtf(q / static_cast<float>(cols) + eps);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * tpr + t) * 16;
+    float g[16], b[16];
+    load16(gamma + c, g);
+    load16(beta + c, b);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[k][e] = (v[k][e] - mean) * rstd * g[e] + b[e];
+    store16(y + base + c, v[k]);
+  }
+}
+
+// NV for the row-group kernel (0: shape not covered -> older kernels).
+inline int ln_rows_nv(int cols) {
+  if (cols % 16) return 0;
+  for (int nv = 1; nv <= 4; nv *= 2) {
+    const int v = cols / 16;
+    if (v % nv) return 0;
+    const int tpr = v / nv;
+    if (tpr <= 256 && tpr >= 32 && tpr % 32 == 0) return nv;
+  }
+  return 0;
+}
+
+template <typename T, bool BDR>
+cudaError_t ln_rows_launch(const void* in, const void* bias, const void* res, void* xout, const void* gamma,
+                           const void* beta, void* y, long long rows, int cols, float eps, float p, uint64_t seed,
+                           uint64_t offset, cudaStream_t st) {
+  const int nv = ln_rows_nv(cols);
+  if (!nv || rows >= (1LL << 31) * 4) return cudaErrorNotSupported;
+  const int rb = 256 / (cols / (16 * nv));
+  const unsigned grid = static_cast<unsigned>((rows + rb - 1) / rb);
+  const uint32_t thr = dropout_threshold(p);
+  const float ks = dropout_keep_scale(p);
+  const int drop = p > 0.f;
+  auto I = static_cast<const T*>(in);
+  auto Bi = static_cast<const T*>(bias);
+  auto R = static_cast<const T*>(res);
+  auto X = static_cast<T*>(xout);
+  auto G = static_cast<const T*>(gamma);
+  auto Be = static_cast<const T*>(beta);
+  auto Y = static_cast<T*>(y);
+  switch (nv) {
+    case 1: ln_rows_kernel<T, 1, BDR><<<grid, 256, 0, st>>>(I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+    case 2: ln_rows_kernel<T, 2, BDR><<<grid, 256, 0, st>>>(I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+    default: ln_rows_kernel<T, 4, BDR><<<grid, 256, 0, st>>>(I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+  }
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y, long long rows, int cols, float eps,
                      cudaStream_t st) {
@@ -814,6 +940,8 @@ cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y
   auto G = static_cast<const T*>(gamma);
   auto B = static_cast<const T*>(beta);
   auto Y = static_cast<T*>(y);
+  if (ln_rows_nv(cols) && rows < (1LL << 31))
+    return ln_rows_launch<T, false>(x, nullptr, nullptr, nullptr, gamma, beta, y, rows, cols, eps, 0.f, 0, 0, st);
   const int nvec = block_nvec<T>(cols);
   if (nvec && rows < (1LL << 31)) {
     if (nvec == 1)
@@ -843,6 +971,19 @@ cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const voi
                           int cols, float eps, cudaStream_t st) {
   if (dtype == OASES_BF16) return ln_fwd_t<__nv_bfloat16>(x, gamma, beta, y, rows, cols, eps, st);
   return ln_fwd_t<float>(x, gamma, beta, y, rows, cols, eps, st);
+}
+
+bool bdr_layernorm_supported(long long rows, int cols) { return ln_rows_nv(cols) && rows < (1LL << 31); }
+
+cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
+                                                void* xout, const void* gamma, const void* beta, void* y,
+                                                long long rows, int cols, float eps, float p, uint64_t seed,
+                                                uint64_t offset, cudaStream_t st) {
+  if (!bdr_layernorm_supported(rows, cols)) return cudaErrorNotSupported;
+  if (dtype == OASES_BF16)
+    return ln_rows_launch<__nv_bfloat16, true>(in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset,
+                                               st);
+  return ln_rows_launch<float, true>(in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset, st);
 }
 
 cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,

@@ -124,6 +124,23 @@ oases_status oases_layernorm_fwd(int dtype, const void* x, const void* gamma, co
   });
 }
 
+oases_status oases_bias_dropout_residual_layernorm_fwd(int dtype, const void* x, const void* bias,
+                                                       const void* residual, void* x_out, const void* gamma,
+                                                       const void* beta, void* y, int64_t rows, int64_t cols,
+                                                       float eps, float dropout_p, uint64_t seed, uint64_t offset,
+                                                       void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    need_device();
+    if (!oases::bdr_layernorm_supported(rows, static_cast<int>(cols)))
+      throw tmpsim::ConfigError("bias_dropout_residual_layernorm_fwd: shape not covered by the fused kernel");
+    check_cuda(oases::bias_dropout_residual_layernorm_fwd(dtype, x, bias, residual, x_out, gamma, beta, y, rows,
+                                                          static_cast<int>(cols), eps, dropout_p, seed, offset,
+                                                          S(stream)),
+               "bias_dropout_residual_layernorm_fwd");
+  });
+}
+
 size_t oases_layernorm_bwd_workspace(int64_t rows, int64_t cols) {
   return oases::layernorm_bwd_workspace(rows, static_cast<int>(cols));
 }

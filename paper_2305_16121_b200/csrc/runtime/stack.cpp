@@ -156,6 +156,11 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
     if (cfg.attention && (cfg.s % 128 || dh_ % 64 || nrow_attn_ % 64))
       throw ConfigError("stack: bf16 attention needs seq % 128 == 0 and head dim % 64 == 0");
   }
+  // Fused bias-dropout-residual + LayerNorm unless OASES_FUSED_BDR_LN=0 (A/B runs).
+  {
+    const char* e = std::getenv("OASES_FUSED_BDR_LN");
+    fuse_bdr_ln_ = !(e && e[0] == '0');
+  }
   // Fused tcgen05 attention unless OASES_FUSED_ATTN=0 (A/B runs of the unfused chain).
   {
     const char* e = std::getenv("OASES_FUSED_ATTN");
@@ -398,6 +403,31 @@ void Stack::join_side() {
   check_cuda(cudaEventRecord(ctx_.join_ev, ctx_.side), "join record");
   check_cuda(cudaStreamWaitEvent(ctx_.compute, ctx_.join_ev, 0), "join wait");
   side_forked_ = false;
+}
+
+// x_b = x_{b-1} + dropout(ar + bias_row_{b-1}), then LN_b(x_b) -> ln: one
+// fused HBM pass where the row-group kernel covers the shape (its LN is
+// bit-identical to ln_fwd of the stored x_b), else the two kernels.
+void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln) {
+  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
+  const BlockParams& bp = w.params[static_cast<size_t>(block)];
+  const void* bias = cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr;
+  const void* res = cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr;
+  if (cfg_.ln && fuse_bdr_ln_ && bdr_layernorm_supported(Ts, static_cast<int>(h))) {
+    check_cuda(bias_dropout_residual_layernorm_fwd(dtype(), ar, bias, res, x, bp.p[OASES_P_LN_GAMMA],
+                                                   bp.p[OASES_P_LN_BETA], ln, Ts, static_cast<int>(h), cfg_.eps,
+                                                   cfg_.p_hidden, cfg_.seed, drop_offset(block - 1, sb, 0),
+                                                   ctx_.compute),
+               "bdr + layernorm");
+    ++launches_;
+    return;
+  }
+  check_cuda(bias_dropout_residual_fwd(dtype(), ar, bias, res, x, Ts, static_cast<int>(h), cfg_.p_hidden, cfg_.seed,
+                                       drop_offset(block - 1, sb, 0), ctx_.compute),
+             "bdr_fwd");
+  ++launches_;
+  if (cfg_.ln) ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ln);
 }
 
 void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y) {
@@ -690,25 +720,17 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
   Worker& w = workers_[static_cast<size_t>(wi)];
   const int64_t Ts = tokens_sub(), h = cfg_.h;
   void* x = w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)];
-  if (block > 0 && with_bdr) {
-    const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
-    check_cuda(bias_dropout_residual_fwd(dtype(), w.fwd_ar[(block - 1) % 2][static_cast<size_t>(sb)],
-                                         cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr,
-                                         cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr,
-                                         x, Ts, static_cast<int>(h), cfg_.p_hidden, cfg_.seed,
-                                         drop_offset(block - 1, sb, 0), ctx_.compute),
-               "bdr_fwd");
-    ++launches_;
-  }
   Workspace& ws = ws_for(w, block, sb);
   const BlockParams& bp = w.params[static_cast<size_t>(block)];
   const bool att = is_attention(block);
   const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
   const void* ln = x;
-  if (cfg_.ln) {
+  if (block > 0 && with_bdr) {
+    bdr_then_ln(w, block, sb, w.fwd_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln);
+  } else if (cfg_.ln) {
     ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
-    ln = ws.ln;
   }
+  if (cfg_.ln) ln = ws.ln;
   oases_gemm_desc d{};
   d.c_dtype = dtype();
   d.M = Ts; d.N = ncol; d.K = h;
@@ -745,27 +767,20 @@ void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) 
   Worker& w = workers_[static_cast<size_t>(wi)];
   const int64_t Ts = tokens_sub(), h = cfg_.h;
   void* x = w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)];
-  if (rebuild_x && block > 0) {
-    const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
-    check_cuda(bias_dropout_residual_fwd(dtype(), w.rec_ar[(block - 1) % 2][static_cast<size_t>(sb)],
-                                         cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr,
-                                         cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr,
-                                         x, Ts, static_cast<int>(h), cfg_.p_hidden, cfg_.seed,
-                                         drop_offset(block - 1, sb, 0), ctx_.compute),
-               "bdr_fwd (replay)");
-    ++launches_;
-  }
-  // Same kernels as the forward from the stored x_b; the row GEMM only when
-  // this variant replays the block's AllReduce.
+  // Same kernels as the forward from the stored x_b (or x_b rebuilt from the
+  // replayed AllReduce); the row GEMM only when this variant replays the
+  // block's AllReduce.
   Workspace& ws = ws_for(w, block, sb);
   const BlockParams& bp = w.params[static_cast<size_t>(block)];
   const bool att = is_attention(block);
   const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
   const void* ln = x;
-  if (cfg_.ln) {
+  if (rebuild_x && block > 0) {
+    bdr_then_ln(w, block, sb, w.rec_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln);
+  } else if (cfg_.ln) {
     ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
-    ln = ws.ln;
   }
+  if (cfg_.ln) ln = ws.ln;
   oases_gemm_desc d{};
   d.c_dtype = dtype();
   d.M = Ts; d.N = ncol; d.K = h;

@@ -159,6 +159,7 @@ class Stack {
   void join_side();  // compute stream waits for the side stream's current tail
   bool side_forked_ = false;
   void ln_fwd(const void* x, const void* g, const void* b, void* y);
+  void bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln);
   oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);
   void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
@@ -171,7 +172,8 @@ class Stack {
   DeviceArena arena_;
   std::vector<Worker> workers_;
   int nblocks_ = 0;
-  bool fused_attn_ = false;  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
+  bool fused_attn_ = false;
+  bool fuse_bdr_ln_ = true;  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;

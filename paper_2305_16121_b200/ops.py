@@ -155,6 +155,14 @@ def bias_dropout_residual_fwd(x, bias, residual, out, dropout_p=0.0, seed=0, off
                                                      cols, dropout_p, seed, offset, _stream(stream)))
 
 
+def bias_dropout_residual_layernorm_fwd(x, bias, residual, x_out, gamma, beta, y, dropout_p=0.0, seed=0, offset=0,
+                                        eps=1e-5, stream=None):
+    rows, cols = x.shape
+    check(capi.lib().oases_bias_dropout_residual_layernorm_fwd(
+        _dtype(x), _ptr(x), _ptr(bias), _ptr(residual), _ptr(x_out), _ptr(gamma), _ptr(beta), _ptr(y), rows, cols,
+        eps, dropout_p, seed, offset, _stream(stream)))
+
+
 def bias_dropout_residual_bwd(dout, dx, dbias, acc_bias=False, dropout_p=0.0, seed=0, offset=0, stream=None):
     rows, cols = dout.shape
     ws = torch.empty(capi.lib().oases_colsum_workspace(rows, cols) // 4 + 64, dtype=torch.float32,

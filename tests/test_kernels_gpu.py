@@ -119,3 +119,39 @@ def test_loss_head_and_local_allreduce(cuda):
     torch.cuda.synchronize()
     for b in bufs:
         assert rel(b, ref) < 1e-6
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,cols", [(4096, 2048), (1000, 1024), (257, 4096), (64, 8192), (33, 512)])
+@pytest.mark.parametrize("p,use_bias,use_res", [(0.1, True, True), (0.0, False, True), (0.1, True, False)])
+def test_fused_bdr_layernorm_bit_identical(cuda, dt, rows, cols, p, use_bias, use_res):
+    """The fused block-boundary kernel equals bias_dropout_residual_fwd followed by
+    layernorm_fwd BIT FOR BIT (x and LN(x)); LN checked against float64 too."""
+    torch.manual_seed(rows * 7 + cols)
+    x = torch.randn(rows, cols, device=cuda).to(dt)
+    b = torch.randn(cols, device=cuda).to(dt) if use_bias else None
+    r = torch.randn(rows, cols, device=cuda).to(dt) if use_res else None
+    g = (1 + 0.1 * torch.randn(cols, device=cuda)).to(dt)
+    be = (0.1 * torch.randn(cols, device=cuda)).to(dt)
+    x1, y1 = torch.empty_like(x), torch.empty_like(x)
+    ops.bias_dropout_residual_fwd(x, b, r, x1, dropout_p=p, seed=3, offset=17)
+    ops.layernorm_fwd(x1, g, be, y1)
+    x2, y2 = torch.empty_like(x), torch.empty_like(x)
+    ops.bias_dropout_residual_layernorm_fwd(x, b, r, x2, g, be, y2, dropout_p=p, seed=3, offset=17)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2)
+    assert torch.equal(y1, y2)
+    xd = x2.double()
+    ref = (xd - xd.mean(1, keepdim=True)) / torch.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-5)
+    ref = ref * g.double() + be.double()
+    assert rel(y2, ref) < (1e-5 if dt == torch.float32 else 2e-2)
+
+
+def test_fused_bdr_layernorm_rejects_uncovered_shape(cuda):
+    from paper_2305_16121_b200 import _capi as capi
+
+    x = torch.randn(8, 40, device=cuda)
+    g, be = torch.ones(40, device=cuda), torch.zeros(40, device=cuda)
+    with pytest.raises(capi.OasesError) as e:
+        ops.bias_dropout_residual_layernorm_fwd(x, None, x, torch.empty_like(x), g, be, torch.empty_like(x))
+    assert e.value.status == capi.ERR_CONFIG

@@ -60,6 +60,22 @@ def main():
                              "simulated_oases_s": t.simulate(t.schedule_oases(graph), costs, pr.strategy).makespan}
         except t.InfeasibleError as e:
             entry["plan"] = {"infeasible": str(e)}
+        # fine-grained recomputation policy at the uniform degree n:
+        # which layers keep their mid-layer post-AllReduce tensor under budgets
+        # between full recomputation (CrossPass) and Oases
+        s_n = t.Strategy([n] * graph.block_count())
+        lo = t.simulate(t.schedule_cross_pass(graph), costs, s_n)
+        hi = t.simulate(t.schedule_oases(graph), costs, s_n)
+        pol = {"crosspass": {"s": lo.makespan, "memory": lo.peak_memory, "exposed_comm_s": lo.comm_exposed},
+               "oases": {"s": hi.makespan, "memory": hi.peak_memory, "exposed_comm_s": hi.comm_exposed},
+               "budgets": []}
+        for frac in (0.0, 0.25, 0.5, 0.75, 1.0):
+            budget_p = lo.peak_memory + frac * (hi.peak_memory - lo.peak_memory)
+            rp = t.choose_recompute_policy(graph, costs, s_n, budget_p)
+            pol["budgets"].append({"budget_bytes": budget_p, "kept_layers": sum(rp.keep),
+                                   "keep": "".join("K" if k else "r" for k in rp.keep),
+                                   "predicted_s": rp.predicted_time, "memory": rp.predicted_memory})
+        entry["recompute_policy"] = pol
         report["gpus"][n] = entry
         print(n, json.dumps(entry["plan"]), flush=True)
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
