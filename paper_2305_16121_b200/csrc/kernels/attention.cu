@@ -42,9 +42,25 @@ constexpr int kTile = 128;
 constexpr int kRowWarps = 8;                    // backward: two warps per TMEM lane quarter, 64 columns each
 constexpr int kThreads = 64 + 32 * kRowWarps;  // + TMA warp + MMA warp
 constexpr int kFwdRowWarps = 16;                      // forward: four warps per lane quarter, 32 columns each
-constexpr int kFwdThreads = 64 + 32 * kFwdRowWarps;  // 18 warps: 4-5 per scheduler hide the softmax latency
+constexpr int kFwdThreads = 96 + 32 * kFwdRowWarps;  // + Q/K producer, MMA, V producer: 19 warps
 constexpr float kLog2e = 1.44269504088896341f;
 
+#ifdef OASES_EXP_TRACE
+__device__ unsigned long long g_attn_trace[8][64];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATRACE(ev, g) \
+  do {                 \
+    if (blockIdx.x == 0 && (g) < 64) g_attn_trace[ev][g] = gtime(); \
+  } while (0)
+#else
+#define ATRACE(ev, g) \
+  do {                 \
+  } while (0)
+#endif
 struct AttnParams {
   int seq, hl, hg, hoff, Z, nq;
   int q_col, k_col, v_col;  // columns of head 0 of Q / K / V in the qkv (and dqkv) rows
@@ -58,6 +74,7 @@ struct AttnParams {
   uint32_t thr;             // dropout byte threshold (0 = no dropout)
   float ks;                 // keep scale
   uint64_t seed, offset;
+  uint32_t rk0[10], rk1[10];  // Philox round keys of `seed` (constant-bank operands of the round LOP3s)
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -80,26 +97,9 @@ __device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int r, int ch) {
 // Philox4x32-10 (common.cuh) with the round keys and
 // the offset words hoisted out of the per-call path: they are the same for
 // every call of a launch.
-struct PhiloxState {
-  uint32_t k0[10], k1[10];
-  uint32_t o0, o1;
-  uint32_t thr4;
-};
-__device__ __forceinline__ void philox_init(const AttnParams& p, PhiloxState& ps) {
-  uint32_t a = static_cast<uint32_t>(p.seed), b = static_cast<uint32_t>(p.seed >> 32);
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    ps.k0[r] = a;
-    ps.k1[r] = b;
-    a += 0x9E3779B9u;
-    b += 0xBB67AE85u;
-  }
-  ps.o0 = static_cast<uint32_t>(p.offset);
-  ps.o1 = static_cast<uint32_t>(p.offset >> 32);
-  ps.thr4 = p.thr * 0x01010101u;
-}
-// Same Philox with the round keys derived on the fly (two adds per round
-// instead of 20 live registers) for the register-tight forward row warps.
+// Philox4x32-10 (common.cuh): the offset words live
+// in registers, the round keys of the seed in the kernel parameters
+// (AttnParams::rk0/rk1, constant-bank operands of the round LOP3s).
 struct PhiloxLite {
   uint32_t s0, s1, o0, o1, thr4;
 };
@@ -110,40 +110,17 @@ __device__ __forceinline__ void philox_init(const AttnParams& p, PhiloxLite& ps)
   ps.o1 = static_cast<uint32_t>(p.offset >> 32);
   ps.thr4 = p.thr * 0x01010101u;
 }
-__device__ __forceinline__ void keep_masks16(const PhiloxLite& ps, unsigned long long ctr, uint32_t (&m)[8]) {
-  uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = ps.o0, c3 = ps.o1;
-  uint32_t k0 = ps.s0, k1 = ps.s1;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const unsigned long long p0 = static_cast<unsigned long long>(0xD2511F53u) * c0;
-    const unsigned long long p1 = static_cast<unsigned long long>(0xCD9E8D57u) * c2;
-    const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ k0;
-    const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ k1;
-    c1 = static_cast<uint32_t>(p1);
-    c3 = static_cast<uint32_t>(p0);
-    c0 = n0;
-    c2 = n2;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  const uint32_t u[4] = {c0, c1, c2, c3};
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const uint32_t k = __vcmpgeu4(u[w], ps.thr4);
-    m[2 * w] = __byte_perm(k, 0, 0x1100);
-    m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
-  }
-}
 // Keep masks of 16 consecutive elements (Philox counter ctr) as 8 bf16x2 lane
 // masks: m[k] covers elements 2k (low half) and 2k+1.
-__device__ __forceinline__ void keep_masks16(const PhiloxState& ps, unsigned long long ctr, uint32_t (&m)[8]) {
+__device__ __forceinline__ void keep_masks16(const PhiloxLite& ps, const AttnParams& prm, unsigned long long ctr,
+                                             uint32_t (&m)[8]) {
   uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = ps.o0, c3 = ps.o1;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
     const unsigned long long p0 = static_cast<unsigned long long>(0xD2511F53u) * c0;
     const unsigned long long p1 = static_cast<unsigned long long>(0xCD9E8D57u) * c2;
-    const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ ps.k0[r];
-    const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ ps.k1[r];
+    const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ prm.rk0[r];
+    const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ prm.rk1[r];
     c1 = static_cast<uint32_t>(p1);
     c3 = static_cast<uint32_t>(p0);
     c0 = n0;
@@ -157,7 +134,6 @@ __device__ __forceinline__ void keep_masks16(const PhiloxState& ps, unsigned lon
     m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
   }
 }
-
 // Static zigzag schedule of work items over a persistent grid. Items are
 // numbered heaviest first; round r hands CTA c item r*G + c (r even) or
 // r*G + G-1-c (r odd), which balances the decreasing item sizes.
@@ -172,11 +148,17 @@ struct FwdCfg {
   static constexpr int Q_OFF = 0;                        // [2] double-buffered across items
   static constexpr int K_OFF = 2 * TILE_BYTES;           // [2]
   static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;   // [2]
-  static constexpr int P_OFF = V_OFF + 2 * TILE_BYTES;
-  static constexpr int RED_OFF = P_OFF + kTile * kTile * 2;  // row max / row sum exchange [4 parts][128 rows]
+  static constexpr int RED_OFF = V_OFF + 2 * TILE_BYTES;  // row max / row sum exchange [4 parts][128 rows]
   static constexpr int BAR_OFF = RED_OFF + 4 * kTile * 4;
   static constexpr int SMEM = BAR_OFF + 256;
-  static constexpr uint32_t TMEM_COLS = 512;  // S x2 (256) + O x2 (2*DH)
+  // TMEM: NS S/P buffers of 128 columns + NO O accumulators of DH columns.
+  // Three S buffers give the S MMA of iteration g+3 the slack of a whole
+  // iteration after PV_g (which reads P_g from the buffer) completes.
+  static constexpr int NS = 3;
+  static constexpr int NO = DH == 64 ? 2 : 1;
+  static constexpr uint32_t O_COL = NS * kTile;
+  static constexpr uint32_t TMEM_COLS = 512;
+  static_assert(NS * kTile + NO * DH <= 512, "TMEM budget");
 };
 
 // Persistent flash forward: each CTA walks its zigzag item list as one flat
@@ -196,12 +178,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* k_empty = bars + 6;   // [2] freed by the S MMA
   uint64_t* v_full = bars + 8;    // [2]
   uint64_t* v_empty = bars + 10;  // [2] freed by the PV MMA
-  uint64_t* s_full = bars + 12;   // [2]
-  uint64_t* s_empty = bars + 14;  // [2]
-  uint64_t* o_free = bars + 16;   // [2] row warps drained the O buffer
-  uint64_t* p_full = bars + 18;
-  uint64_t* pv_done = bars + 19;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* s_full = bars + 12;   // [NS] S_g in TMEM buffer g % NS
+  uint64_t* p_full = bars + 15;   // [NS] P_g (bf16) written over S_g by the row warps
+  uint64_t* pv_done = bars + 18;  // [NS] PV_g done: buffer g % NS reusable
+  uint64_t* o_free = bars + 21;   // [NO] row warps drained the O buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 23);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = static_cast<int>(gridDim.x);
@@ -220,12 +201,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], kFwdRowWarps);
-      mbar_init(&o_free[s], kFwdRowWarps);
     }
-    mbar_init(p_full, kFwdRowWarps);
-    mbar_init(pv_done, 1);
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], kFwdRowWarps);
+      mbar_init(&pv_done[s], 1);
+    }
+    for (int s = 0; s < C::NO; ++s) mbar_init(&o_free[s], kFwdRowWarps);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -234,9 +216,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2) {
+    // TMA producers: warp 0 streams Q and K, warp 2 streams V. Separate
+    // threads so a K load never queues behind the wait for a V stage (freed
+    // only by the PV MMA at the end of a softmax): K gets a full extra
+    // iteration of latency slack.
     if (lane == 0) {
-      tma_prefetch(&tqkv);
+      const bool kq = warp == 0;
+      if (kq) tma_prefetch(&tqkv);
       int g = 0;  // global kv iteration
       for (int r = 0, k = 0;; ++r, ++k) {
         const int t = zigzag_item(r, G);
@@ -245,102 +232,126 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         item_of(t, qt, z);
         const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
         const int qb = k & 1;
-        mbar_wait(&q_empty[qb], ((k >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[qb], C::TILE_BYTES);
+        if (kq) {
+          mbar_wait(&q_empty[qb], ((k >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qb], C::TILE_BYTES);
 #pragma unroll
-        for (int gg = 0; gg < DH / 64; ++gg)
-          tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + gg * 16384, &tqkv, &q_full[qb],
-                      p.q_col + jl * DH + gg * 64, row0 + qt * kTile);
+          for (int gg = 0; gg < DH / 64; ++gg)
+            tma_load_2d(smem + C::Q_OFF + qb * C::TILE_BYTES + gg * 16384, &tqkv, &q_full[qb],
+                        p.q_col + jl * DH + gg * 64, row0 + qt * kTile);
+        }
         for (int j = 0; j <= qt; ++j, ++g) {
           const int st = g & 1, ph = ((g >> 1) & 1) ^ 1;
-          mbar_wait(&k_empty[st], ph);
-          mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
+          uint64_t* empty = kq ? &k_empty[st] : &v_empty[st];
+          uint64_t* full = kq ? &k_full[st] : &v_full[st];
+          const int off = kq ? C::K_OFF : C::V_OFF, col = kq ? p.k_col : p.v_col;
+          mbar_wait(empty, ph);
+          ATRACE(kq ? 6 : 7, g);
+#ifdef OASES_EXP_NOLOAD
+          mbar_arrive(full);
+          (void)off; (void)col;
+#else
+          mbar_arrive_expect_tx(full, C::TILE_BYTES);
 #pragma unroll
           for (int gg = 0; gg < DH / 64; ++gg)
-            tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + gg * 16384, &tqkv, &k_full[st],
-                        p.k_col + jl * DH + gg * 64, row0 + j * kTile);
-          mbar_wait(&v_empty[st], ph);
-          mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
-#pragma unroll
-          for (int gg = 0; gg < DH / 64; ++gg)
-            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + gg * 16384, &tqkv, &v_full[st],
-                        p.v_col + jl * DH + gg * 64, row0 + j * kTile);
+            tma_load_2d(smem + off + st * C::TILE_BYTES + gg * 16384, &tqkv, full, col + jl * DH + gg * 64,
+                        row0 + j * kTile);
+#endif
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id_s = umma_idesc_bf16(kTile, kTile, 0, 0);
-      constexpr uint32_t id_o = umma_idesc_bf16(kTile, DH, 0, 1);
+      constexpr uint32_t id_o = umma_idesc_bf16(kTile, DH, 0, 1);  // A = P in TMEM (K-major), B = V (MN-major)
       const uint32_t sb = smem_u32(smem);
-      // S for flat iteration (item k, kv tile j, global g); commits q_empty after the item's last tile.
+      // S for flat iteration (item k, kv tile j, global g) into TMEM buffer g&1,
+      // once PV_{g-2} (which read P_{g-2} from that buffer) is done; commits
+      // q_empty after the item's last tile.
       auto issue_s = [&](int k, int j, int g, bool last) {
-        const int st = g & 1, qb = k & 1;
+        ATRACE(0, g);
+        const int st = g % C::NS, kv = g & 1, qb = k & 1;
         if (j == 0) mbar_wait(&q_full[qb], (k >> 1) & 1);
-        mbar_wait(&k_full[st], (g >> 1) & 1);
-        mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
+        mbar_wait(&k_full[kv], (g >> 1) & 1);
+        if (g >= C::NS) mbar_wait(&pv_done[st], ((g - C::NS) / C::NS) & 1);
+        ATRACE(1, g);
         tc_fence_after();
-        const uint32_t qa = sb + C::Q_OFF + qb * C::TILE_BYTES, kb = sb + C::K_OFF + st * C::TILE_BYTES;
+        const uint32_t qa = sb + C::Q_OFF + qb * C::TILE_BYTES, kb = sb + C::K_OFF + kv * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+#ifndef OASES_EXP_NOMMA
           umma_bf16(tmem + st * kTile, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
                     id_s, kk > 0 ? 1u : 0u);
+#ifdef OASES_EXP_DOUBLEMMA
+          umma_bf16(tmem + st * kTile, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
+                    id_s, 1u);
+#endif
+#endif
         }
         umma_commit(&s_full[st]);
-        umma_commit(&k_empty[st]);
+        umma_commit(&k_empty[kv]);
         if (last) umma_commit(&q_empty[qb]);
       };
+      // O += P_g V_g with P_g read from TMEM (bf16, 64 columns over S_g).
       auto issue_pv = [&](int k, int j, int g) {
-        const int st = g & 1, ob = k & 1;
-        if (j == 0) mbar_wait(&o_free[ob], ((k >> 1) & 1) ^ 1);
-        mbar_wait(p_full, g & 1);
-        mbar_wait(&v_full[st], (g >> 1) & 1);
+        ATRACE(2, g);
+        const int st = g % C::NS, kv = g & 1, ob = k % C::NO;
+        if (j == 0) mbar_wait(&o_free[ob], ((k / C::NO) & 1) ^ 1);
+        mbar_wait(&p_full[st], (g / C::NS) & 1);
+        mbar_wait(&v_full[kv], (g >> 1) & 1);
+        ATRACE(3, g);
         tc_fence_after();
-        const uint32_t pa = sb + C::P_OFF, vb = sb + C::V_OFF + st * C::TILE_BYTES;
+        const uint32_t vb = sb + C::V_OFF + kv * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = umma_desc_sw128(vb + kk * 2048, 16384, 1024);
-          umma_bf16(tmem + 2 * kTile + ob * DH, ad, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+#ifndef OASES_EXP_NOMMA
+          umma_bf16_ts(tmem + C::O_COL + ob * DH, tmem + st * kTile + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+#endif
         }
-        umma_commit(&v_empty[st]);
-        umma_commit(pv_done);
+        umma_commit(&v_empty[kv]);
+        umma_commit(&pv_done[st]);
       };
-      // flat iteration cursor: (round r -> item t, k), kv tile j, global g
-      int r = 0, k = 0, j = 0, g = 0, qt = -1;
-      {
-        const int t = zigzag_item(0, G);
-        if (t < total) {
+      // Flat iteration cursors (round r -> item k, kv tile j, global g). The S
+      // MMAs run two iterations ahead of the PV MMAs (three S/P buffers), so
+      // the commit -> mbarrier -> softmax latency of S_{g+1}, S_{g+2} hides
+      // under the softmax of g.
+      struct Cur {
+        int r, k, j, qt, g;
+        bool valid;
+      };
+      auto cur_load = [&](Cur& c) {
+        const int t = zigzag_item(c.r, G);
+        c.valid = t < total;
+        if (c.valid) {
           int z;
-          item_of(t, qt, z);
+          item_of(t, c.qt, z);
         }
+      };
+      auto cur_next = [&](Cur& c) {
+        ++c.g;
+        if (++c.j > c.qt) {
+          ++c.r;
+          ++c.k;
+          c.j = 0;
+          cur_load(c);
+        }
+      };
+      Cur sc{0, 0, 0, 0, 0, false}, pc{0, 0, 0, 0, 0, false};
+      cur_load(sc);
+      cur_load(pc);
+      for (int a = 0; a < C::NS - 1 && sc.valid; ++a) {
+        issue_s(sc.k, sc.j, sc.g, sc.j == sc.qt);
+        cur_next(sc);
       }
-      if (qt >= 0) {
-        issue_s(0, 0, 0, qt == 0);
-        for (;;) {
-          // successor of (k, j)
-          int k2 = k, j2 = j + 1, qt2 = qt;
-          if (j2 > qt) {
-            const int t2 = zigzag_item(r + 1, G);
-            if (t2 < total) {
-              int z2;
-              item_of(t2, qt2, z2);
-              k2 = k + 1;
-              j2 = 0;
-            } else {
-              qt2 = -1;
-            }
-          }
-          if (qt2 >= 0) issue_s(k2, j2, g + 1, j2 == qt2);
-          issue_pv(k, j, g);
-          if (qt2 < 0) break;
-          if (k2 != k) ++r;
-          k = k2;
-          j = j2;
-          qt = qt2;
-          ++g;
+      while (pc.valid) {
+        if (sc.valid) {
+          issue_s(sc.k, sc.j, sc.g, sc.j == sc.qt);
+          cur_next(sc);
         }
+        issue_pv(pc.k, pc.j, pc.g);
+        cur_next(pc);
       }
     }
   } else {
@@ -349,12 +360,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // tile; one row per thread), key columns [32 part, 32 part + 32) of every
     // S tile and O columns [part DH/4, (part+1) DH/4). The four warps of a
     // quarter combine their partial row maxima / sums through smem.
-    const int q = warp & 3, part = (warp - 2) >> 2;
+    const int q = warp & 3, part = (warp - 3) >> 2;  // row warps 3 .. 18
     const int rr = q * 32 + lane;
     const int c0 = part * 32;
     constexpr int OC = DH / 4;  // O columns per warp
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    uint8_t* pbuf = smem + C::P_OFF;
     float* red = reinterpret_cast<float*>(smem + C::RED_OFF);  // [part][row]
     PhiloxLite ph;
     philox_init(p, ph);
@@ -366,23 +376,34 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       item_of(t, qt, z);
       const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
       const int i = qt * kTile + rr;
-      const int ob = k & 1;
-      const uint32_t to = tl + 2 * kTile + ob * DH + part * OC;  // this warp's columns of O
+      const int ob = k % C::NO;
+      const uint32_t to = tl + C::O_COL + ob * DH + part * OC;  // this warp's columns of O
       const unsigned long long ebase =
           (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i) *
               static_cast<unsigned long long>(p.seq) +
           c0;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j <= qt; ++j, ++g) {
-        const int st = g & 1;
-        mbar_wait(&s_full[st], (g >> 1) & 1);
+        const int st = g % C::NS;
+#ifdef OASES_EXP_ONESPIN
+        if (part == 0) mbar_wait(&s_full[st], (g / C::NS) & 1);
+        named_bar_sync(1 + q, 128);
+#else
+        mbar_wait(&s_full[st], (g / C::NS) & 1);
+#endif
+        if (warp == 3 && lane == 0) ATRACE(4, g);
         tc_fence_after();
+#ifdef OASES_EXP_NOSOFT
+        {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[st]);
+          continue;
+        }
+#endif
         uint32_t u[32];
         tmem_ld32(tl + st * kTile + c0, u);
         tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[st]);
         if (j == qt) {
           int lim = rr - c0;                   // keys > row are masked
           asm volatile("" : "+r"(lim));        // keep the comparisons inside the (rare) diagonal branch
@@ -399,10 +420,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int kk = 4; kk < 32; ++kk) mp[kk & 3] = fmaxf(mp[kk & 3], __uint_as_float(u[kk]));
           mpart = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
         }
+#ifdef OASES_EXP_NOBAR
+        const float mloc = mpart;
+#else
+        tc_fence_before();           // this warp's S loads precede the barrier (P overwrites S below)
         named_bar_sync(1 + q, 128);  // the quarter's previous partials are consumed
         red[part * kTile + rr] = mpart;
         named_bar_sync(1 + q, 128);
+        tc_fence_after();
         const float mloc = fmaxf(fmaxf(red[rr], red[kTile + rr]), fmaxf(red[2 * kTile + rr], red[3 * kTile + rr]));
+#endif
         // Conditional rescaling: keep the running max unless the row max grew by
         // more than 8 (log2 units). P = exp2(s - m) then stays <= 256 (exact in
         // bf16's range) and O, l are rescaled only when it pays; the result is
@@ -415,8 +442,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int kk = 0; kk < 32; kk += 2) {
+#ifdef OASES_EXP_NOEXP
+          const float a = fmaf(__uint_as_float(u[kk]), p.sl2, nmx);
+          const float b = fmaf(__uint_as_float(u[kk + 1]), p.sl2, nmx);
+#else
           const float a = ex2(fmaf(__uint_as_float(u[kk]), p.sl2, nmx));
           const float b = ex2(fmaf(__uint_as_float(u[kk + 1]), p.sl2, nmx));
+#endif
           sp[(kk >> 1) & 3] += a + b;
           pk[kk >> 1] = pack_bf16(a, b);
         }
@@ -427,18 +459,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int gq = 0; gq < 2; ++gq) {
             uint32_t km[8];
-            keep_masks16(ph, (ebase + static_cast<unsigned long long>(j) * kTile + gq * 16) >> 4, km);
+            keep_masks16(ph, p, (ebase + static_cast<unsigned long long>(j) * kTile + gq * 16) >> 4, km);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) pk[gq * 8 + kk] &= km[kk];
           }
         }
-        // the P buffer must be free (previous PV done, possibly the previous item's)
-        if (g > 0) {
-          mbar_wait(pv_done, (g - 1) & 1);
-          tc_fence_after();
-        }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          // O holds P_{j-1} V_{j-1}: rescale it to the new reference max
+          // O holds P_{j-1} V_{j-1} once PV_{g-1} is done: rescale it to the new
+          // reference max (rare: only when the row max grew by more than 8)
+          mbar_wait(&pv_done[(g - 1) % C::NS], ((g - 1) / C::NS) & 1);
+          tc_fence_after();
           if constexpr (OC == 32) {
             uint32_t o[32];
             tmem_ld32(to, o);
@@ -456,20 +486,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
           tmem_wait_st();
         }
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-          *tile_chunk(pbuf, rr, part * 4 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-        fence_proxy_async();
+        // P_g (bf16 pairs) over this warp's S_g columns: the quarter's S loads all
+        // precede the max exchange above, so no warp still needs them
+        tmem_st16(tl + st * kTile + c0 / 2, pk);
+        tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (warp == 3 && lane == 0) ATRACE(5, g);
+        if (lane == 0) mbar_arrive(&p_full[st]);
       }
       // ---- item epilogue: O / l -> ctx, lse
       named_bar_sync(1 + q, 128);
       red[part * kTile + rr] = l;
       named_bar_sync(1 + q, 128);
       const float lt = (red[rr] + red[kTile + rr]) + (red[2 * kTile + rr] + red[3 * kTile + rr]);
-      mbar_wait(pv_done, (g - 1) & 1);
+      mbar_wait(&pv_done[(g - 1) % C::NS], ((g - 1) / C::NS) & 1);
       tc_fence_after();
       const float inv = p.ks / lt;
       __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + i) * p.ld_out +
@@ -688,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
     uint8_t* buf = smem + C::BUF_OFF;
     const bool leader = threadIdx.x == 64;
-    PhiloxState ph;
+    PhiloxLite ph;
     philox_init(p, ph);
     for (int it = 0; it < ni; ++it) {
       const int st = it & 1, i = kt + it;
@@ -728,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint32_t km[8];
-          keep_masks16(ph, (ebase + g * 16) >> 4, km);
+          keep_masks16(ph, p, (ebase + g * 16) >> 4, km);
 #pragma unroll
           for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
         }
@@ -851,10 +882,23 @@ bool fill_common(AttnParams& p, const oases_attn_desc& d, std::string* err) {
   p.ks = dropout_keep_scale(d.dropout_p);
   p.seed = d.seed;
   p.offset = d.offset;
+  uint32_t a = static_cast<uint32_t>(d.seed), b = static_cast<uint32_t>(d.seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    p.rk0[r] = a;
+    p.rk1[r] = b;
+    a += 0x9E3779B9u;
+    b += 0xBB67AE85u;
+  }
   return true;
 }
 
 }  // namespace
+
+#ifdef OASES_EXP_TRACE
+extern "C" int oases_attn_trace_dump(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(unsigned long long) * 8 * 64));
+}
+#endif
 
 bool attention_supported(int dtype, int head_dim, int seq) {
   return dtype == OASES_BF16 && (head_dim == 64 || head_dim == 128) && seq > 0 && seq % kTile == 0;
