@@ -512,13 +512,23 @@ constexpr int PAIR_STAGE_BYTES = 2 * PAIR_HALF_BYTES;  // A half + B half
 constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 256 + 1024;  // + 32 KB static staging
 constexpr uint32_t PAIR_TMEM_COLS = 512;
 
+// Tile order: groups of PAIR_GROUP_M m-tiles walked n-major inside the group,
+// so the ~74 tiles in flight at once share a few A and B panels (a wave
+// touches ~8 A + ~9 B panels instead of 2-3 A + every B panel). Keeps the
+// operand panels L2-resident across waves: DRAM traffic stays near A + B + C
+// once even when B is larger than the L2 share it gets (wgrad: B = 64 MB).
+constexpr int PAIR_GROUP_M = 8;
 __device__ __forceinline__ void pair_decode(const TcParams& p, int t, int& z, int& m0, int& n0) {
   const int per_z = p.tiles_m * p.tiles_n;
   z = t / per_z;
   const int r = t - z * per_z;
-  const int mt = r / p.tiles_n;
-  m0 = mt * PAIR_BM;
-  n0 = (r - mt * p.tiles_n) * PAIR_BN;
+  const int group = PAIR_GROUP_M * p.tiles_n;
+  const int grp = r / group;
+  const int first_m = grp * PAIR_GROUP_M;
+  const int gm = min(PAIR_GROUP_M, p.tiles_m - first_m);
+  const int idx = r - grp * group;
+  m0 = (first_m + idx % gm) * PAIR_BM;
+  n0 = (idx / gm) * PAIR_BN;
 }
 
 // Up to two independent GEMM problems in one persistent launch (a "group"):

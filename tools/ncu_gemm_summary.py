@@ -1,8 +1,9 @@
 """Summarise `ncu --set full` captures of single GEMM / attention launches into
 profiles/ncu_summary.json (the `traffic` field of bench.py's roofline object).
 
-usage: python tools/ncu_gemm_summary.py OUT.json NAME=REP:M,N,K,OUT_BYTES [...]
-  REP        an .ncu-rep holding one launch of the kernel (tools/gemm_one.py)
+usage: python tools/ncu_gemm_summary.py OUT.json NAME=REP[#i]:M,N,K,OUT_BYTES [...]
+  REP        an .ncu-rep holding one launch of the kernel (tools/gemm_one.py);
+             REP#i selects launch i of a multi-launch capture
   M,N,K      GEMM shape; algorithmic bytes = 2*(M*K + N*K) + OUT_BYTES*M*N
 The first entry is the dominant kernel bench.py reports.
 """
@@ -49,7 +50,12 @@ def main():
         name, rest = arg.split("=", 1)
         rep, shape = rest.split(":")
         M, N, K, ob = (int(x) for x in shape.split(","))
-        for d in raw(rep):
+        idx = None
+        if "#" in rep:  # REP#i: the i-th launch of a multi-launch capture
+            rep, i = rep.split("#")
+            idx = int(i)
+        launches = raw(rep)
+        for d in (launches if idx is None else [launches[idx]]):
             alg = 2 * (M * K + N * K) + ob * M * N
             traffic = d.get("dram_read", 0) + d.get("dram_write", 0)
             e = {"name": name, "shape": [M, N, K], "out_bytes_per_elem": ob, "algorithmic_bytes": alg,
