@@ -23,9 +23,13 @@ cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const voi
                           float* dgamma, float* dbeta, int acc_params, void* workspace, long long rows, int cols,
                           float eps, cudaStream_t st);
 // which: 1 = dx and row statistics (into workspace), 2 = dgamma/dbeta from those statistics
+// gout (optional, part 1 only): also write dropout'(dx) under (drop_p, seed,
+// offset) -- the bias-dropout-residual backward fused into the LN backward
+// pass; cudaErrorNotSupported for shapes the row-group kernel does not cover.
 cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,
                                int acc_dx, float* dgamma, float* dbeta, int acc_params, void* workspace,
-                               long long rows, int cols, float eps, cudaStream_t st);
+                               long long rows, int cols, float eps, cudaStream_t st, void* gout = nullptr,
+                               float drop_p = 0.f, uint64_t seed = 0, uint64_t offset = 0);
 // batch = n_samples * heads_local; rows are (sample, local head, query).
 cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,
                         float dropout_p, uint64_t seed, uint64_t offset, int heads_local, int heads_total,

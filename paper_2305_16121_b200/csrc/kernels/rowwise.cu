@@ -758,10 +758,125 @@ int block_nvec(int cols) {
 // which: 1 = dx (+ row statistics into the workspace), 2 = dgamma/dbeta from
 // those statistics, 3 = both. Splitting lets the parameter reduction run on a
 // side stream under the next GEMMs (its outputs are only needed at step end).
+// NV for the row-group kernel (0: shape not covered -> older kernels).
+inline int ln_rows_nv(int cols) {
+  if (cols % 16) return 0;
+  for (int nv = 1; nv <= 4; nv *= 2) {
+    const int v = cols / 16;
+    if (v % nv) return 0;
+    const int tpr = v / nv;
+    if (tpr <= 256 && tpr >= 32 && tpr % 32 == 0) return nv;
+  }
+  return 0;
+}
+
+// Row-group LayerNorm backward (same geometry as ln_rows_kernel): dx (+)=
+// rstd * (g - mean(g) - xhat * mean(g xhat)), g = dy * gamma, row statistics
+// to `stats` for the parameter pass. DROP also writes the gradient through the
+// preceding hidden dropout, gout = dropout'(dx) (the bias-dropout-residual
+// backward, numerically the col_pass of the stored bf16 dx), so the dropout
+// pass does not re-read dx from HBM.
+template <typename T, int NV, bool DROP>
+__global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
+                                                          const T* __restrict__ dy, T* __restrict__ dx, int acc,
+                                                          float2* __restrict__ stats, T* __restrict__ gout,
+                                                          long long rows, int cols, float eps, uint32_t thr, float ks,
+                                                          uint64_t seed, uint64_t offset) {
+  __shared__ float sm[4][8][8];  // [statistic][row of the block][warp of the row]
+  const int tpr = cols / (16 * NV), rb = 256 / tpr, wpr = tpr / 32;
+  const int sub = threadIdx.x / tpr, t = threadIdx.x - sub * tpr, wi = t >> 5;
+  const long long row = static_cast<long long>(blockIdx.x) * rb + sub;
+  const bool ok = row < rows;
+  const long long base = row * cols;
+  float xv[NV][16], gv[NV][16];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * tpr + t) * 16;
+    if (!ok) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) xv[k][e] = gv[k][e] = 0.f;
+      continue;
+    }
+    float d[16], g[16];
+    load16(x + base + c, xv[k]);
+    load16(dy + base + c, d);
+    load16(gamma + c, g);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      gv[k][e] = d[e] * g[e];
+      s += xv[k][e];
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sm[0][sub][wi] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int w = 0; w < wpr; ++w) s += sm[0][sub][w];
+  const float mean = s / static_cast<float>(cols);
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) q += (xv[k][e] - mean) * (xv[k][e] - mean);
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) sm[1][sub][wi] = q;
+  __syncthreads();
+  q = 0.f;
+  for (int w = 0; w < wpr; ++w) q += sm[1][sub][w];
+  const float rstd = rsqrtf(q / static_cast<float>(cols) + eps);
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      xv[k][e] = (xv[k][e] - mean) * rstd;  // xhat
+      s1 += gv[k][e];
+      s2 += gv[k][e] * xv[k][e];
+    }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if ((threadIdx.x & 31) == 0) {
+    sm[2][sub][wi] = s1;
+    sm[3][sub][wi] = s2;
+  }
+  __syncthreads();
+  s1 = 0.f;
+  s2 = 0.f;
+  for (int w = 0; w < wpr; ++w) {
+    s1 += sm[2][sub][w];
+    s2 += sm[3][sub][w];
+  }
+  if (!ok) return;
+  const float m1 = s1 / static_cast<float>(cols), m2 = s2 / static_cast<float>(cols);
+  if (t == 0) stats[row] = make_float2(mean, rstd);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = (k * tpr + t) * 16;
+    float o[16];
+    if (acc) load16(dx + base + c, o);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float r = rstd * (gv[k][e] - m1 - xv[k][e] * m2);
+      o[e] = acc ? o[e] + r : r;
+    }
+    store16(dx + base + c, o);
+    if constexpr (DROP) {
+      if constexpr (sizeof(T) == 2) {  // what a re-read of the stored dx sees
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(o[e]));
+      }
+      apply_dropout16(o, static_cast<unsigned long long>(base + c), seed, offset, thr, ks);
+      store16(gout + base + c, o);
+    }
+  }
+}
+
 template <typename T>
 cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx, int acc_dx, float* dgamma,
                      float* dbeta, int acc_params, void* workspace, long long rows, int cols, float eps,
-                     cudaStream_t st, int which = 3) {
+                     cudaStream_t st, int which = 3, void* gout = nullptr, float drop_p = 0.f, uint64_t seed = 0,
+                     uint64_t offset = 0) {
   float2* stats = static_cast<float2*>(workspace);
   float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) +
                                          ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)));
@@ -771,8 +886,28 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   auto DX = static_cast<T*>(dx);
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
   const int nvec = block_nvec<T>(cols);
+  const int rnv = ln_rows_nv(cols);
   if (!(which & 1)) {
     // parameter pass only
+  } else if (rnv && rows < (1LL << 31)) {
+    const unsigned g2 = static_cast<unsigned>((rows + 256 / (cols / (16 * rnv)) - 1) / (256 / (cols / (16 * rnv))));
+    T* GO = static_cast<T*>(gout);
+    const uint32_t thr = dropout_threshold(drop_p);
+    const float ks = dropout_keep_scale(drop_p);
+#define OASES_LNB(NV, D) \
+  ln_bwd_rows_kernel<T, NV, D><<<g2, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, GO, rows, cols, eps, thr, ks, seed, offset)
+    if (GO) {
+      if (rnv == 1) OASES_LNB(1, true);
+      else if (rnv == 2) OASES_LNB(2, true);
+      else OASES_LNB(4, true);
+    } else {
+      if (rnv == 1) OASES_LNB(1, false);
+      else if (rnv == 2) OASES_LNB(2, false);
+      else OASES_LNB(4, false);
+    }
+#undef OASES_LNB
+  } else if (gout) {
+    return cudaErrorNotSupported;  // the fused dropout output needs the row-group kernel
   } else if (nvec && rows < (1LL << 31)) {
     // one row per block (measured faster than 2 for the backward)
     if (nvec == 1)
@@ -895,18 +1030,6 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const T* __restrict__ in, 
   }
 }
 
-// NV for the row-group kernel (0: shape not covered -> older kernels).
-inline int ln_rows_nv(int cols) {
-  if (cols % 16) return 0;
-  for (int nv = 1; nv <= 4; nv *= 2) {
-    const int v = cols / 16;
-    if (v % nv) return 0;
-    const int tpr = v / nv;
-    if (tpr <= 256 && tpr >= 32 && tpr % 32 == 0) return nv;
-  }
-  return 0;
-}
-
 template <typename T, bool BDR>
 cudaError_t ln_rows_launch(const void* in, const void* bias, const void* res, void* xout, const void* gamma,
                            const void* beta, void* y, long long rows, int cols, float eps, float p, uint64_t seed,
@@ -988,11 +1111,13 @@ cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const
 
 cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,
                                int acc_dx, float* dgamma, float* dbeta, int acc_params, void* workspace,
-                               long long rows, int cols, float eps, cudaStream_t st) {
+                               long long rows, int cols, float eps, cudaStream_t st, void* gout, float drop_p,
+                               uint64_t seed, uint64_t offset) {
   if (dtype == OASES_BF16)
     return ln_bwd_t<__nv_bfloat16>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st,
-                                   which);
-  return ln_bwd_t<float>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st, which);
+                                   which, gout, drop_p, seed, offset);
+  return ln_bwd_t<float>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st, which,
+                         gout, drop_p, seed, offset);
 }
 
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,

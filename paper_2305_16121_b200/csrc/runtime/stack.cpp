@@ -819,7 +819,9 @@ void Stack::backward(int wi, int block, int sb) {
   const int hi = static_cast<int>(h);
   void* g = half(w.grad, sb, h);
   const size_t usb = static_cast<size_t>(sb);
-  // 1. gradient arriving at x_{b+1}
+  // 1. gradient arriving at x_{b+1}; with LayerNorm the same pass also writes
+  //    g_ar = dropout'(g) (step 2) when the row-group kernel covers the width
+  bool gar_done = false;
   if (block == nblocks_ - 1) {
     const BlockParams& bp = w.params[static_cast<size_t>(block)];
     check_cuda(bias_dropout_residual_fwd(dtype(), w.fwd_ar[block % 2][usb], cfg_.bias ? bp.p[OASES_P_B_ROW] : nullptr,
@@ -836,9 +838,12 @@ void Stack::backward(int wi, int block, int sb) {
     if (cfg_.ln) {
       const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
       const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
+      const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && bdr_layernorm_supported(Ts, hi);
       check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
-                                    nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute),
+                                    nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute, fuse ? w.gar : nullptr,
+                                    cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0)),
                  "layernorm_bwd");
+      gar_done = fuse;
       // dgamma/dbeta: side stream, under this op's GEMMs (joined at the op's end)
       fork_side();
       check_cuda(layernorm_bwd_part(2, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, nullptr, 0, nxt.g[OASES_P_LN_GAMMA],
@@ -856,10 +861,12 @@ void Stack::backward(int wi, int block, int sb) {
   BlockParams& bp = w.params[static_cast<size_t>(block)];
   const void* gar = g;
   if (cfg_.p_hidden > 0.f) {
-    check_cuda(col_pass(dtype(), g, w.gar, nullptr, 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed,
-                        drop_offset(block, sb, 0), ctx_.compute),
-               "dropout bwd");
-    ++launches_;
+    if (!gar_done) {
+      check_cuda(col_pass(dtype(), g, w.gar, nullptr, 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed,
+                          drop_offset(block, sb, 0), ctx_.compute),
+                 "dropout bwd");
+      ++launches_;
+    }
     gar = w.gar;
   }
   if (cfg_.bias) {
