@@ -68,7 +68,8 @@ typedef struct {
 typedef enum {
   OASES_EPI_NONE = 0,      /* C = alpha*acc (+ C if accumulate) */
   OASES_EPI_BIAS = 1,      /* C = alpha*acc + bias[n] */
-  OASES_EPI_BIAS_GELU = 2, /* C = v = alpha*acc + bias[n];  C2 = gelu(v)  (erf GeLU, numerics.cpp:50) */
+  OASES_EPI_BIAS_GELU = 2, /* C = v = alpha*acc + bias[n];  C2 = gelu(v)  (erf GeLU, numerics.cpp:50);
+                              C2 == NULL: C = gelu(v) only (the pre-activation is not stored) */
   OASES_EPI_DGELU = 3      /* C = alpha*acc * gelu'(AUX[m,n])  (hadamard+gelu_grad, numerics.cpp:204) */
 } oases_epilogue;
 

@@ -94,8 +94,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
       if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias) v += p.bias[n];
       if (p.epilogue == OASES_EPI_DGELU) v *= gelu_grad_f(p.aux[off]);
       if (p.accumulate) v += p.c[off];
-      p.c[off] = v;
-      if (p.epilogue == OASES_EPI_BIAS_GELU) p.c2[off] = gelu_f(v);
+      if (p.epilogue == OASES_EPI_BIAS_GELU && !p.c2) {
+        p.c[off] = gelu_f(v);  // activation only
+      } else {
+        p.c[off] = v;
+        if (p.epilogue == OASES_EPI_BIAS_GELU) p.c2[off] = gelu_f(v);
+      }
     }
   }
 }

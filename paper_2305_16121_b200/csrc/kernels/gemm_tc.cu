@@ -287,11 +287,14 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
 #pragma unroll
           for (int i = 0; i < E; ++i) v[i] += o[i];
         }
-        st_vec<OutT, E>(cp, v);
         if constexpr (EPI == OASES_EPI_BIAS_GELU) {
+          // C2 == null: only the activation is wanted (pre-activation dead), into C
+          if (p.c2) st_vec<OutT, E>(cp, v);
 #pragma unroll
           for (int i = 0; i < E; ++i) v[i] = gelu_fast(v[i]);
-          st_vec<OutT, E>(reinterpret_cast<OutT*>(p.c2) + rel, v);
+          st_vec<OutT, E>(p.c2 ? reinterpret_cast<OutT*>(p.c2) + rel : cp, v);
+        } else {
+          st_vec<OutT, E>(cp, v);
         }
       } else {
 #pragma unroll
@@ -300,9 +303,16 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
           float x = v[i];
           if constexpr (DG) x *= gelu_grad_fast(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
           if constexpr (ACC) x += to_f(cp[i]);
-          cp[i] = from_f<OutT>(x);
-          if constexpr (EPI == OASES_EPI_BIAS_GELU)
-            reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_fast(x));
+          if constexpr (EPI == OASES_EPI_BIAS_GELU) {
+            if (p.c2) {
+              cp[i] = from_f<OutT>(x);
+              reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_fast(x));
+            } else {
+              cp[i] = from_f<OutT>(gelu_fast(x));
+            }
+          } else {
+            cp[i] = from_f<OutT>(x);
+          }
         }
       }
     }

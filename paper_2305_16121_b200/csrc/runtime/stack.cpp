@@ -746,7 +746,14 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
     attention_fwd(w, block, sb, ws);
   } else {
     d.epilogue = OASES_EPI_BIAS_GELU;
-    d.c2 = ws.act;
+    if (cfg_.recompute) {
+      // the recompute pass regenerates the pre-activation the backward needs
+      // (dGeLU); here only the activation feeding FC2 is live
+      d.c = ws.act;
+      d.c2 = nullptr;
+    } else {
+      d.c2 = ws.act;
+    }
     gemm(d);
   }
   if (with_row) {

@@ -177,3 +177,22 @@ def test_gemm_grouped_dgrad_wgrad_bitwise(cuda, T, h, n):
     ref_w = 0.5 + g.double().t() @ act.double()
     assert relerr(outs[1][0], ref_d) < 1e-2
     assert relerr(outs[1][1], ref_w) < 1e-5
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_gemm_gelu_activation_only(cuda, dt):
+    """EPI_BIAS_GELU with no C2 stores only gelu(acc + bias) into C (the forward FC1
+    under recomputation, whose pre-activation is dead)."""
+    torch.manual_seed(9)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = capi.BF16 if dt == "bf16" else capi.F32
+    M, N, K = 384, 512, 256
+    A = torch.randn(M, K, device=cuda).to(tdt)
+    B = (torch.randn(N, K, device=cuda) / math.sqrt(K)).to(tdt)
+    bias = torch.randn(N, device=cuda).to(tdt)
+    pre, act = torch.empty(M, N, device=cuda, dtype=tdt), torch.empty(M, N, device=cuda, dtype=tdt)
+    ops.gemm(M, N, K, ops.operand(A), ops.operand(B), pre, epilogue=capi.EPI_BIAS_GELU, bias=bias, c2=act, dtype=kdt)
+    only = torch.empty(M, N, device=cuda, dtype=tdt)
+    ops.gemm(M, N, K, ops.operand(A), ops.operand(B), only, epilogue=capi.EPI_BIAS_GELU, bias=bias, dtype=kdt)
+    torch.cuda.synchronize()
+    assert torch.equal(only, act)
