@@ -169,6 +169,7 @@ struct FwdCfg {
 template <int DH>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, const AttnParams p) {
+  pdl_trigger();
   using C = FwdCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
 
   if (warp == 0 || warp == 2) {
     // TMA producers: warp 0 streams Q and K, warp 2 streams V. Separate
@@ -537,6 +539,8 @@ __global__ void __launch_bounds__(256) attn_dsum_kernel(const __nv_bfloat16* __r
                                                         const __nv_bfloat16* __restrict__ out, long long ld,
                                                         float* __restrict__ dsum, int seq, int hl, int col0,
                                                         long long rows) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int TPR = DH / 8;  // threads per row (power of two <= 32)
   const long long row = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) / TPR;
   const int sub = threadIdx.x % TPR;
@@ -575,6 +579,7 @@ template <int DH>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_dkdv_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
                      const __grid_constant__ CUtensorMap tds, const AttnParams p) {
+  pdl_trigger();
   using C = BwdCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -623,6 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -938,14 +944,12 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
   if (d.head_dim == 128) {
     static cudaError_t once = set_smem(attn_fwd_kernel<128>, FwdCfg<128>::SMEM);
     if ((e = once) == cudaSuccess) {
-      attn_fwd_kernel<128><<<grid, kFwdThreads, FwdCfg<128>::SMEM, stream>>>(tqkv, p);
-      e = cudaGetLastError();
+      e = launch_pdl(attn_fwd_kernel<128>, dim3(grid), dim3(kFwdThreads), FwdCfg<128>::SMEM, stream, tqkv, p);
     }
   } else {
     static cudaError_t once = set_smem(attn_fwd_kernel<64>, FwdCfg<64>::SMEM);
     if ((e = once) == cudaSuccess) {
-      attn_fwd_kernel<64><<<grid, kFwdThreads, FwdCfg<64>::SMEM, stream>>>(tqkv, p);
-      e = cudaGetLastError();
+      e = launch_pdl(attn_fwd_kernel<64>, dim3(grid), dim3(kFwdThreads), FwdCfg<64>::SMEM, stream, tqkv, p);
     }
   }
   if (e != cudaSuccess) {
@@ -989,15 +993,13 @@ GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream) {
   }
   const long long drows = static_cast<long long>(p.Z) * d.seq;
   const unsigned dgrid = static_cast<unsigned>((drows * (d.head_dim / 8) + 255) / 256);
-  if (d.head_dim == 128)
-    attn_dsum_kernel<128><<<dgrid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(d.dout),
-                                                      static_cast<const __nv_bfloat16*>(d.out), d.ld_dout, dsum,
-                                                      d.seq, d.heads_local, 0, drows);
-  else
-    attn_dsum_kernel<64><<<dgrid, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(d.dout),
-                                                     static_cast<const __nv_bfloat16*>(d.out), d.ld_dout, dsum,
-                                                     d.seq, d.heads_local, 0, drows);
-  cudaError_t e = cudaGetLastError();
+  const auto* dO = static_cast<const __nv_bfloat16*>(d.dout);
+  const auto* O = static_cast<const __nv_bfloat16*>(d.out);
+  cudaError_t e = d.head_dim == 128
+                      ? launch_pdl(attn_dsum_kernel<128>, dim3(dgrid), dim3(256), 0, stream, dO, O, d.ld_dout, dsum,
+                                   d.seq, d.heads_local, 0, drows)
+                      : launch_pdl(attn_dsum_kernel<64>, dim3(dgrid), dim3(256), 0, stream, dO, O, d.ld_dout, dsum,
+                                   d.seq, d.heads_local, 0, drows);
   if (e == cudaSuccess) {
     p.out = d.dqkv;
     p.ld_out = d.ld_dqkv;
@@ -1007,14 +1009,14 @@ GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream) {
     if (d.head_dim == 128) {
       static cudaError_t once = set_smem(attn_dkdv_kernel<128>, BwdCfg<128>::SMEM);
       if ((e = once) == cudaSuccess) {
-        attn_dkdv_kernel<128><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tqkv, tdo, tds, p);
-        e = cudaGetLastError();
+        e = launch_pdl(attn_dkdv_kernel<128>, dim3(grid), dim3(kThreads), BwdCfg<128>::SMEM, stream, tqkv, tdo,
+                       tds, p);
       }
     } else {
       static cudaError_t once = set_smem(attn_dkdv_kernel<64>, BwdCfg<64>::SMEM);
       if ((e = once) == cudaSuccess) {
-        attn_dkdv_kernel<64><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tqkv, tdo, tds, p);
-        e = cudaGetLastError();
+        e = launch_pdl(attn_dkdv_kernel<64>, dim3(grid), dim3(kThreads), BwdCfg<64>::SMEM, stream, tqkv, tdo,
+                       tds, p);
       }
     }
   }

@@ -2,6 +2,7 @@
 // Philox dropout, erf-GeLU. Inline PTX only (no CUTLASS/CuTe dependency).
 #pragma once
 
+#include <utility>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -190,6 +191,31 @@ __device__ __forceinline__ float dropout_one(float v, unsigned long long e, uint
   uint32_t u[4];
   Philox::gen(seed, offset, e >> 4, u);
   return keep_byte(u, static_cast<unsigned>(e & 15), thr) ? v * ks : 0.f;
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels launched with launch_pdl may start while the previous kernel of the
+// stream is still running (its tail SMs pick up this grid's prologue: barrier
+// init, TMEM alloc, descriptor prefetch); pdl_wait() blocks until that kernel
+// has completed and its memory is visible, so it precedes every global access.
+// pdl_trigger() lets this grid's own dependents launch early. Both are no-ops
+// for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------- mbarrier

@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kThreads) bdr_fwd16_kernel(const T* __restrict
                                                              const T* __restrict__ res, T* __restrict__ out, IDX n,
                                                              IDX cols, uint32_t thr, float ks, int drop, uint64_t seed,
                                                              uint64_t offset) {
+  pdl_trigger();
+  pdl_wait();
   const IDX stride = static_cast<IDX>(gridDim.x) * blockDim.x * 16;
   for (IDX i = (static_cast<IDX>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; i < n; i += stride) {
     float v[16];
@@ -169,6 +171,8 @@ __global__ void __launch_bounds__(32) col_pass16_kernel(const T* __restrict__ in
                                                         float* __restrict__ part, long long rows, int cols,
                                                         int rows_per_chunk, uint32_t thr, float ks, int drop,
                                                         uint64_t seed, uint64_t offset) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x;
   const int c = blockIdx.x * 512 + lane * 16;
   if (c >= cols) return;
@@ -210,6 +214,8 @@ __global__ void __launch_bounds__(32) col_pass16_kernel(const T* __restrict__ in
 // bit-reproducible.
 __global__ void __launch_bounds__(kThreads) col_finalize_fast_kernel(const float* __restrict__ part, int chunks,
                                                                      int cols, float* __restrict__ out, int acc) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sm[8][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -274,6 +280,8 @@ __global__ void __launch_bounds__(kThreads) gelu_bwd_kernel(const T* __restrict_
 template <typename T>
 __global__ void __launch_bounds__(kThreads) gelu_sq_loss_kernel(const T* __restrict__ z, T* __restrict__ dz,
                                                                 double* __restrict__ part, long long n) {
+  pdl_trigger();
+  pdl_wait();
   double acc = 0.0;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -296,6 +304,8 @@ __global__ void __launch_bounds__(kThreads) gelu_sq_loss_kernel(const T* __restr
 // Deterministic tree over the block partials (fixed order).
 __global__ void __launch_bounds__(kThreads) loss_finalize_kernel(const double* __restrict__ part, int nparts,
                                                                  double* __restrict__ out, int acc) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sm[kThreads];
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += kThreads) s += part[i];
@@ -391,12 +401,12 @@ void bdr16(const T* X, const T* B, const T* R, T* O, long long n, int cols, uint
   if (g > 148LL * 8) g = 148LL * 8;
   if (g < 1) g = 1;
   if (n < (1LL << 31))  // 32-bit index arithmetic cannot wrap
-    bdr_fwd16_kernel<T, uint32_t><<<static_cast<unsigned>(g), kThreads, 0, st>>>(
-        X, B, R, O, static_cast<uint32_t>(n), static_cast<uint32_t>(cols), thr, ks, drop, seed, offset);
+    launch_pdl(bdr_fwd16_kernel<T, uint32_t>, dim3(static_cast<unsigned>(g)), dim3(kThreads), 0, st, X, B, R, O,
+               static_cast<uint32_t>(n), static_cast<uint32_t>(cols), thr, ks, drop, seed, offset);
   else
-    bdr_fwd16_kernel<T, unsigned long long><<<static_cast<unsigned>(g), kThreads, 0, st>>>(
-        X, B, R, O, static_cast<unsigned long long>(n), static_cast<unsigned long long>(cols), thr, ks, drop, seed,
-        offset);
+    launch_pdl(bdr_fwd16_kernel<T, unsigned long long>, dim3(static_cast<unsigned>(g)), dim3(kThreads), 0, st, X, B,
+               R, O, static_cast<unsigned long long>(n), static_cast<unsigned long long>(cols), thr, ks, drop, seed,
+               offset);
 }
 
 }  // namespace
@@ -457,9 +467,8 @@ static bool col_pass_t(const void* in, void* dx, float* part, long long rows, in
   constexpr int V = 16 / sizeof(T);
   if (cols % 16 == 0 && vec_ok<T>(in, dx, rows * cols, cols) && vec_ok<T>(part, nullptr, cols, cols)) {
     const ColSplit sp = col_split16(rows, cols);
-    col_pass16_kernel<T><<<dim3((cols + 511) / 512, sp.chunks), 32, 0, st>>>(
-        static_cast<const T*>(in), static_cast<T*>(dx), part, rows, cols, sp.rows_per_chunk, thr, ks, drop, seed,
-        offset);
+    launch_pdl(col_pass16_kernel<T>, dim3((cols + 511) / 512, sp.chunks), dim3(32), 0, st, static_cast<const T*>(in),
+               static_cast<T*>(dx), part, rows, cols, sp.rows_per_chunk, thr, ks, drop, seed, offset);
     *chunks_out = sp.chunks;
     return true;
   }
@@ -495,7 +504,8 @@ cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, v
     fast = col_pass_t<float>(in, dx, part, rows, cols, thr, ks, drop, seed, offset, &chunks, st);
   if (out) {
     if (fast)
-      col_finalize_fast_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
+      launch_pdl(col_finalize_fast_kernel, dim3((cols + 31) / 32), dim3(kThreads), 0, st,
+                 static_cast<const float*>(part), chunks, cols, out, acc);
     else
       col_finalize_kernel<<<(cols + 31) / 32, kThreads, 0, st>>>(part, chunks, cols, out, acc);
   }
@@ -529,12 +539,13 @@ cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int a
   unsigned g = grid_for(n, kThreads * 4);
   if (g > 1024) g = 1024;
   if (dtype == OASES_BF16)
-    gelu_sq_loss_kernel<<<g, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(z), static_cast<__nv_bfloat16*>(dz),
-                                                ws, n);
+    launch_pdl(gelu_sq_loss_kernel<__nv_bfloat16>, dim3(g), dim3(kThreads), 0, st, static_cast<const __nv_bfloat16*>(z),
+               static_cast<__nv_bfloat16*>(dz), ws, n);
   else
-    gelu_sq_loss_kernel<<<g, kThreads, 0, st>>>(static_cast<const float*>(z), static_cast<float*>(dz), ws, n);
-  loss_finalize_kernel<<<1, kThreads, 0, st>>>(ws, static_cast<int>(g), loss, acc);
-  return cudaGetLastError();
+    launch_pdl(gelu_sq_loss_kernel<float>, dim3(g), dim3(kThreads), 0, st, static_cast<const float*>(z),
+               static_cast<float*>(dz), ws, n);
+  return launch_pdl(loss_finalize_kernel, dim3(1), dim3(kThreads), 0, st, static_cast<const double*>(ws),
+                    static_cast<int>(g), loss, acc);
 }
 
 cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cudaStream_t st) {

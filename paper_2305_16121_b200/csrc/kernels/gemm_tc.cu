@@ -386,6 +386,7 @@ template <int BN, int A_MN, int B_MN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const TcParams p) {
+  pdl_trigger();
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   // Statically shared staging so the compiler emits STS/LDS (a generic-pointer
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -618,6 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap tb0,
                     const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensorMap tb1,
                     const TcGroup g) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(16) float4 stg_all[STG_FLOAT4];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -656,6 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the previous kernel's outputs (our operands) are complete from here on
 
   if (warp == 0) {
     if (lane == 0) {
@@ -774,8 +778,7 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcPara
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_tc_kernel<BN, A_MN, B_MN><<<grid, THREADS, Cfg::SMEM, stream>>>(ma, mb, p);
-  return cudaGetLastError();
+  return launch_pdl(gemm_tc_kernel<BN, A_MN, B_MN>, dim3(grid), dim3(THREADS), Cfg::SMEM, stream, ma, mb, p);
 }
 
 template <int A0, int B0, int A1, int B1>
@@ -787,8 +790,8 @@ cudaError_t launch_group_t(const CUtensorMap (&maps)[4], const TcGroup& g, int g
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  gemm_tc2_kernel<A0, B0, A1, B1><<<grid, THREADS, PAIR_SMEM, stream>>>(maps[0], maps[1], maps[2], maps[3], g);
-  return cudaGetLastError();
+  return launch_pdl(gemm_tc2_kernel<A0, B0, A1, B1>, dim3(grid), dim3(THREADS), PAIR_SMEM, stream, maps[0], maps[1],
+                    maps[2], maps[3], g);
 }
 
 // false: no instantiation for this combination of operand layouts

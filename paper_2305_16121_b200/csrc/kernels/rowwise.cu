@@ -397,6 +397,8 @@ template <typename T>
 __global__ void __launch_bounds__(32) ln_param16_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                                                         const float2* __restrict__ stats, float* __restrict__ part,
                                                         long long rows, int cols, int rows_per_chunk) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x;
   const int c = blockIdx.x * 512 + lane * 16;
   if (c >= cols) return;
@@ -447,6 +449,8 @@ __global__ void __launch_bounds__(32) ln_param16_kernel(const T* __restrict__ x,
 __global__ void __launch_bounds__(256) colpair_finalize_fast_kernel(const float* __restrict__ part, int chunks,
                                                                     int cols, float* __restrict__ out0,
                                                                     float* __restrict__ out1, int acc) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sm[2][8][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -782,6 +786,8 @@ __global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const T* __restrict__ 
                                                           float2* __restrict__ stats, T* __restrict__ gout,
                                                           long long rows, int cols, float eps, uint32_t thr, float ks,
                                                           uint64_t seed, uint64_t offset) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sm[4][8][8];  // [statistic][row of the block][warp of the row]
   const int tpr = cols / (16 * NV), rb = 256 / tpr, wpr = tpr / 32;
   const int sub = threadIdx.x / tpr, t = threadIdx.x - sub * tpr, wi = t >> 5;
@@ -894,8 +900,9 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
     T* GO = static_cast<T*>(gout);
     const uint32_t thr = dropout_threshold(drop_p);
     const float ks = dropout_keep_scale(drop_p);
-#define OASES_LNB(NV, D) \
-  ln_bwd_rows_kernel<T, NV, D><<<g2, 256, 0, st>>>(X, G, DY, DX, acc_dx, stats, GO, rows, cols, eps, thr, ks, seed, offset)
+#define OASES_LNB(NV, D)                                                                                          \
+  launch_pdl(ln_bwd_rows_kernel<T, NV, D>, dim3(g2), dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, GO, rows, cols, \
+             eps, thr, ks, seed, offset)
     if (GO) {
       if (rnv == 1) OASES_LNB(1, true);
       else if (rnv == 2) OASES_LNB(2, true);
@@ -928,10 +935,10 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   if ((which & 2) && (dgamma || dbeta)) {
     if (cols % 16 == 0) {
       const ParamSplit sp = param_split16(rows, cols);
-      ln_param16_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 32, 0, st>>>(X, DY, stats, part, rows, cols,
-                                                                        sp.rows_per_chunk);
-      colpair_finalize_fast_kernel<<<(cols + 31) / 32, 256, 0, st>>>(part, sp.chunks, cols, dgamma, dbeta,
-                                                                     acc_params);
+      launch_pdl(ln_param16_kernel<T>, dim3(sp.col_blocks, sp.chunks), dim3(32), 0, st, X, DY,
+                 static_cast<const float2*>(stats), part, rows, cols, sp.rows_per_chunk);
+      launch_pdl(colpair_finalize_fast_kernel, dim3((cols + 31) / 32), dim3(256), 0, st,
+                 static_cast<const float*>(part), sp.chunks, cols, dgamma, dbeta, acc_params);
     } else {
       const ParamSplit sp = param_split<T>(rows, cols);
       ln_param_partial_kernel<T><<<dim3(sp.col_blocks, sp.chunks), 256, 0, st>>>(X, DY, stats, part, rows, cols,
@@ -958,6 +965,8 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const T* __restrict__ in, 
                                                       T* __restrict__ y, long long rows, int cols, float eps,
                                                       uint32_t thr, float ks, int drop, uint64_t seed,
                                                       uint64_t offset) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sm[2][8][8];  // [statistic][row of the block][warp of the row]
   const int tpr = cols / (16 * NV), rb = 256 / tpr, wpr = tpr / 32;
   const int sub = threadIdx.x / tpr, t = threadIdx.x - sub * tpr, wi = t >> 5;
@@ -1049,9 +1058,9 @@ cudaError_t ln_rows_launch(const void* in, const void* bias, const void* res, vo
   auto Be = static_cast<const T*>(beta);
   auto Y = static_cast<T*>(y);
   switch (nv) {
-    case 1: ln_rows_kernel<T, 1, BDR><<<grid, 256, 0, st>>>(I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
-    case 2: ln_rows_kernel<T, 2, BDR><<<grid, 256, 0, st>>>(I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
-    default: ln_rows_kernel<T, 4, BDR><<<grid, 256, 0, st>>>(I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+    case 1: launch_pdl(ln_rows_kernel<T, 1, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+    case 2: launch_pdl(ln_rows_kernel<T, 2, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+    default: launch_pdl(ln_rows_kernel<T, 4, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
   }
   return cudaGetLastError();
 }
