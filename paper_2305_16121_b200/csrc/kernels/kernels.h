@@ -25,7 +25,8 @@ cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const voi
 // which: 1 = dx and row statistics (into workspace), 2 = dgamma/dbeta from those statistics
 // gout (optional, part 1 only): also write dropout'(dx) under (drop_p, seed,
 // offset) -- the bias-dropout-residual backward fused into the LN backward
-// pass; cudaErrorNotSupported for shapes the row-group kernel does not cover.
+// pass; cudaErrorNotSupported unless ln_bwd_dropout_supported().
+bool ln_bwd_dropout_supported(int dtype, long long rows, int cols);
 cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,
                                int acc_dx, float* dgamma, float* dbeta, int acc_params, void* workspace,
                                long long rows, int cols, float eps, cudaStream_t st, void* gout = nullptr,

@@ -4,6 +4,7 @@
 // statistics. The reference restates none of these (its toy FFN has no LN and
 // no attention, numerics.hpp:37-44); the fp64 oracle (oracle/gpt_oracle.cpp)
 // defines their parity semantics.
+#include <cstdlib>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -306,11 +307,20 @@ __global__ void __launch_bounds__(256) ln_fwd_block_kernel(const T* __restrict__
   }
 }
 
-template <typename T, int NVEC, int R>
+// DROP: also writes gout = dropout'(dx) (the hidden-dropout gradient of the
+// bias-dropout-residual backward, computed from the stored bf16 dx exactly as
+// the separate column pass would), saving that pass's re-read of dx.
+template <typename T, int NVEC, int R, bool DROP = false>
 __global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
                                                            const T* __restrict__ dy, T* __restrict__ dx, int acc,
                                                            float2* __restrict__ stats, long long rows, int cols,
-                                                           float eps) {
+                                                           float eps, T* __restrict__ gout = nullptr,
+                                                           uint32_t thr = 0, float ks = 1.f, uint64_t seed = 0,
+                                                           uint64_t offset = 0) {
+  if constexpr (DROP) {
+    pdl_trigger();
+    pdl_wait();
+  }
   constexpr int V = Vec<T>::N;
   __shared__ float sm[16 * R];
   const long long row0 = static_cast<long long>(blockIdx.x) * R;
@@ -384,7 +394,16 @@ __global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__
         const float r = rstd[k] * (gv[k][t][e] - m1 - xv[k][t][e] * m2);
         o[k][t][e] = acc ? o[k][t][e] + r : r;
       }
-      vstore(dx + (row0 + k) * cols + (t * 256 + threadIdx.x) * V, o[k][t]);
+      const long long off = (row0 + k) * cols + (t * 256 + threadIdx.x) * V;
+      vstore(dx + off, o[k][t]);
+      if constexpr (DROP) {
+        if constexpr (sizeof(T) == 2) {  // what a re-read of the stored dx sees
+#pragma unroll
+          for (int e = 0; e < V; ++e) o[k][t][e] = __bfloat162float(__float2bfloat16_rn(o[k][t][e]));
+        }
+        apply_dropout<V>(o[k][t], static_cast<unsigned long long>(off), seed, offset, thr, ks);
+        vstore(gout + off, o[k][t]);
+      }
     }
   }
 }
@@ -774,110 +793,6 @@ inline int ln_rows_nv(int cols) {
   return 0;
 }
 
-// Row-group LayerNorm backward (same geometry as ln_rows_kernel): dx (+)=
-// rstd * (g - mean(g) - xhat * mean(g xhat)), g = dy * gamma, row statistics
-// to `stats` for the parameter pass. DROP also writes the gradient through the
-// preceding hidden dropout, gout = dropout'(dx) (the bias-dropout-residual
-// backward, numerically the col_pass of the stored bf16 dx), so the dropout
-// pass does not re-read dx from HBM.
-template <typename T, int NV, bool DROP>
-__global__ void __launch_bounds__(256) ln_bwd_rows_kernel(const T* __restrict__ x, const T* __restrict__ gamma,
-                                                          const T* __restrict__ dy, T* __restrict__ dx, int acc,
-                                                          float2* __restrict__ stats, T* __restrict__ gout,
-                                                          long long rows, int cols, float eps, uint32_t thr, float ks,
-                                                          uint64_t seed, uint64_t offset) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float sm[4][8][8];  // [statistic][row of the block][warp of the row]
-  const int tpr = cols / (16 * NV), rb = 256 / tpr, wpr = tpr / 32;
-  const int sub = threadIdx.x / tpr, t = threadIdx.x - sub * tpr, wi = t >> 5;
-  const long long row = static_cast<long long>(blockIdx.x) * rb + sub;
-  const bool ok = row < rows;
-  const long long base = row * cols;
-  float xv[NV][16], gv[NV][16];
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int c = (k * tpr + t) * 16;
-    if (!ok) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) xv[k][e] = gv[k][e] = 0.f;
-      continue;
-    }
-    float d[16], g[16];
-    load16(x + base + c, xv[k]);
-    load16(dy + base + c, d);
-    load16(gamma + c, g);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      gv[k][e] = d[e] * g[e];
-      s += xv[k][e];
-    }
-  }
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) sm[0][sub][wi] = s;
-  __syncthreads();
-  s = 0.f;
-  for (int w = 0; w < wpr; ++w) s += sm[0][sub][w];
-  const float mean = s / static_cast<float>(cols);
-  float q = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-#pragma unroll
-    for (int e = 0; e < 16; ++e) q += (xv[k][e] - mean) * (xv[k][e] - mean);
-  q = warp_sum(q);
-  if ((threadIdx.x & 31) == 0) sm[1][sub][wi] = q;
-  __syncthreads();
-  q = 0.f;
-  for (int w = 0; w < wpr; ++w) q += sm[1][sub][w];
-  const float rstd = rsqrtf(q / static_cast<float>(cols) + eps);
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      xv[k][e] = (xv[k][e] - mean) * rstd;  // xhat
-      s1 += gv[k][e];
-      s2 += gv[k][e] * xv[k][e];
-    }
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  if ((threadIdx.x & 31) == 0) {
-    sm[2][sub][wi] = s1;
-    sm[3][sub][wi] = s2;
-  }
-  __syncthreads();
-  s1 = 0.f;
-  s2 = 0.f;
-  for (int w = 0; w < wpr; ++w) {
-    s1 += sm[2][sub][w];
-    s2 += sm[3][sub][w];
-  }
-  if (!ok) return;
-  const float m1 = s1 / static_cast<float>(cols), m2 = s2 / static_cast<float>(cols);
-  if (t == 0) stats[row] = make_float2(mean, rstd);
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int c = (k * tpr + t) * 16;
-    float o[16];
-    if (acc) load16(dx + base + c, o);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float r = rstd * (gv[k][e] - m1 - xv[k][e] * m2);
-      o[e] = acc ? o[e] + r : r;
-    }
-    store16(dx + base + c, o);
-    if constexpr (DROP) {
-      if constexpr (sizeof(T) == 2) {  // what a re-read of the stored dx sees
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(o[e]));
-      }
-      apply_dropout16(o, static_cast<unsigned long long>(base + c), seed, offset, thr, ks);
-      store16(gout + base + c, o);
-    }
-  }
-}
-
 template <typename T>
 cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx, int acc_dx, float* dgamma,
                      float* dbeta, int acc_params, void* workspace, long long rows, int cols, float eps,
@@ -892,29 +807,25 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
   auto DX = static_cast<T*>(dx);
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
   const int nvec = block_nvec<T>(cols);
-  const int rnv = ln_rows_nv(cols);
   if (!(which & 1)) {
     // parameter pass only
-  } else if (rnv && rows < (1LL << 31)) {
-    const unsigned g2 = static_cast<unsigned>((rows + 256 / (cols / (16 * rnv)) - 1) / (256 / (cols / (16 * rnv))));
-    T* GO = static_cast<T*>(gout);
+  } else if (gout) {
+    // fused dropout output: the block-per-row kernel (one row of 256 threads, 8
+    // elements each; measured faster than the row-group geometry backward)
+    if (!nvec || rows >= (1LL << 31)) return cudaErrorNotSupported;
     const uint32_t thr = dropout_threshold(drop_p);
     const float ks = dropout_keep_scale(drop_p);
-#define OASES_LNB(NV, D)                                                                                          \
-  launch_pdl(ln_bwd_rows_kernel<T, NV, D>, dim3(g2), dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, GO, rows, cols, \
-             eps, thr, ks, seed, offset)
-    if (GO) {
-      if (rnv == 1) OASES_LNB(1, true);
-      else if (rnv == 2) OASES_LNB(2, true);
-      else OASES_LNB(4, true);
-    } else {
-      if (rnv == 1) OASES_LNB(1, false);
-      else if (rnv == 2) OASES_LNB(2, false);
-      else OASES_LNB(4, false);
-    }
-#undef OASES_LNB
-  } else if (gout) {
-    return cudaErrorNotSupported;  // the fused dropout output needs the row-group kernel
+    T* GO = static_cast<T*>(gout);
+    const dim3 gr(static_cast<unsigned>(rows));
+    if (nvec == 1)
+      launch_pdl(ln_bwd_block_kernel<T, 1, 1, true>, gr, dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, rows, cols,
+                 eps, GO, thr, ks, seed, offset);
+    else if (nvec == 2)
+      launch_pdl(ln_bwd_block_kernel<T, 2, 1, true>, gr, dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, rows, cols,
+                 eps, GO, thr, ks, seed, offset);
+    else
+      launch_pdl(ln_bwd_block_kernel<T, 4, 1, true>, gr, dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, rows, cols,
+                 eps, GO, thr, ks, seed, offset);
   } else if (nvec && rows < (1LL << 31)) {
     // one row per block (measured faster than 2 for the backward)
     if (nvec == 1)
@@ -1106,6 +1017,11 @@ cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const voi
 }
 
 bool bdr_layernorm_supported(long long rows, int cols) { return ln_rows_nv(cols) && rows < (1LL << 31); }
+
+bool ln_bwd_dropout_supported(int dtype, long long rows, int cols) {
+  const int nv = dtype == OASES_BF16 ? block_nvec<__nv_bfloat16>(cols) : block_nvec<float>(cols);
+  return nv && rows < (1LL << 31);
+}
 
 cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
                                                 void* xout, const void* gamma, const void* beta, void* y,

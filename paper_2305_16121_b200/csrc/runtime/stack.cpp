@@ -845,7 +845,7 @@ void Stack::backward(int wi, int block, int sb) {
     if (cfg_.ln) {
       const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
       const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
-      const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && bdr_layernorm_supported(Ts, hi);
+      const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && ln_bwd_dropout_supported(dtype(), Ts, hi);
       check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
                                     nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute, fuse ? w.gar : nullptr,
                                     cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0)),

@@ -48,6 +48,8 @@ timeit(lambda: ops.layernorm_bwd(x, g, r, y, dg, dbe, accumulate_dx=True), 6 * T
        "layernorm_bwd (+dgamma/dbeta)")
 timeit(lambda: ops.bias_dropout_residual_fwd(x, b, r, y, dropout_p=0.1, seed=1, offset=2), 3 * T * h * B,
        "bias_dropout_residual_fwd p=0.1")
+timeit(lambda: ops.bias_dropout_residual_layernorm_fwd(x, b, r, y, g, b, r, dropout_p=0.1, seed=1, offset=2),
+       4 * T * h * B, "fused bdr + layernorm_fwd p=0.1")
 timeit(lambda: ops.bias_dropout_residual_bwd(x, y, db, dropout_p=0.1, seed=1, offset=2), 2 * T * h * B,
        "dropout' + dbias (col_pass)")
 timeit(lambda: ops.colsum(big, dbf), T * f * B, "colsum [4096 x 8192]")
