@@ -70,7 +70,10 @@ typedef enum {
   OASES_EPI_BIAS = 1,      /* C = alpha*acc + bias[n] */
   OASES_EPI_BIAS_GELU = 2, /* C = v = alpha*acc + bias[n];  C2 = gelu(v)  (erf GeLU, numerics.cpp:50);
                               C2 == NULL: C = gelu(v) only (the pre-activation is not stored) */
-  OASES_EPI_DGELU = 3      /* C = alpha*acc * gelu'(AUX[m,n])  (hadamard+gelu_grad, numerics.cpp:204) */
+  OASES_EPI_DGELU = 3,     /* C = alpha*acc * gelu'(AUX[m,n])  (hadamard+gelu_grad, numerics.cpp:204) */
+  OASES_EPI_BIAS_GELU_GRAD = 4, /* v = alpha*acc + bias[n]; C = gelu'(v), C2 = gelu(v)  (the recompute FC1:
+                                   stores the factor the dgrad needs instead of the pre-activation) */
+  OASES_EPI_MUL = 5        /* C = alpha*acc * AUX[m,n]  (dgrad with a stored gelu'(pre)) */
 } oases_epilogue;
 
 typedef enum {

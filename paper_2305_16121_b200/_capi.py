@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("OASES_LIB") or os.path.join(_HERE, "liboases.so")
 
 OK, ERR_CONFIG, ERR_INFEASIBLE, ERR_IO, ERR_CUDA, ERR_NCCL = 0, 2, 3, 4, 5, 6
 F32, BF16 = 0, 1
-EPI_NONE, EPI_BIAS, EPI_BIAS_GELU, EPI_DGELU = 0, 1, 2, 3
+EPI_NONE, EPI_BIAS, EPI_BIAS_GELU, EPI_DGELU, EPI_BIAS_GELU_GRAD, EPI_MUL = 0, 1, 2, 3, 4, 5
 CAUSAL_NONE, CAUSAL_SKIP_UPPER, CAUSAL_K_UPTO_M, CAUSAL_K_FROM_M = 0, 1, 2, 3
 
 

@@ -91,8 +91,16 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtParams p) {
       if (n >= p.N) continue;
       const long long off = (crow + m) * p.ldc + ccol + n;
       float v = p.alpha * acc[i][j];
-      if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU) && p.bias) v += p.bias[n];
+      if ((p.epilogue == OASES_EPI_BIAS || p.epilogue == OASES_EPI_BIAS_GELU ||
+           p.epilogue == OASES_EPI_BIAS_GELU_GRAD) && p.bias)
+        v += p.bias[n];
       if (p.epilogue == OASES_EPI_DGELU) v *= gelu_grad_f(p.aux[off]);
+      if (p.epilogue == OASES_EPI_MUL) v *= p.aux[off];
+      if (p.epilogue == OASES_EPI_BIAS_GELU_GRAD) {
+        p.c[off] = gelu_grad_f(v);
+        p.c2[off] = gelu_f(v);
+        continue;
+      }
       if (p.accumulate) v += p.c[off];
       if (p.epilogue == OASES_EPI_BIAS_GELU && !p.c2) {
         p.c[off] = gelu_f(v);  // activation only

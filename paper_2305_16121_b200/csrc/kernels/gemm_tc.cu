@@ -202,7 +202,7 @@ __device__ __forceinline__ void epi_prefetch(const TcParams& p, int c, int nbeg,
   for (int it = 0; it < G::IT; ++it) {
     const bool ok = full && it * G::RPI + lr < rows_left;
     const long long off = lane_base + nbeg + c * 32 + it * step;
-    if constexpr (EPI == OASES_EPI_DGELU) {
+    if constexpr (EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL) {
       pa[it] = make_uint4(0u, 0u, 0u, 0u);
       if (ok) pa[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const OutT*>(p.aux) + off));
     }
@@ -220,8 +220,8 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
                                           float4* stg, int lane) {
   using G = StripeGeo<OutT>;
   constexpr int E = G::E, RPI = G::RPI, IT = G::IT;
-  constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU;
-  constexpr bool DG = EPI == OASES_EPI_DGELU;
+  constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU || EPI == OASES_EPI_BIAS_GELU_GRAD;
+  constexpr bool DG = EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL;  // epilogues reading AUX
   const int nc = nbeg + c * 32;
   // All of the chunk's global operand loads are in flight at once (one DRAM
   // latency per chunk instead of one per row pair). bf16 operands (4 vectors)
@@ -279,7 +279,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
           float x[E];
           unpack_vec<OutT, E>(pa[it], x);
 #pragma unroll
-          for (int i = 0; i < E; ++i) v[i] *= gelu_grad_fast(x[i]);
+          for (int i = 0; i < E; ++i) v[i] *= EPI == OASES_EPI_MUL ? x[i] : gelu_grad_fast(x[i]);
         }
         if constexpr (ACC) {
           float o[E];
@@ -293,6 +293,18 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
 #pragma unroll
           for (int i = 0; i < E; ++i) v[i] = gelu_fast(v[i]);
           st_vec<OutT, E>(p.c2 ? reinterpret_cast<OutT*>(p.c2) + rel : cp, v);
+        } else if constexpr (EPI == OASES_EPI_BIAS_GELU_GRAD) {
+          // C = gelu'(v) (what the dgrad epilogue multiplies by), C2 = gelu(v)
+          float d[E];
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            float cdf, pdf;
+            norm_cdf_pdf(v[i], cdf, pdf);
+            d[i] = fmaf(v[i], pdf, cdf);
+            v[i] *= cdf;
+          }
+          st_vec<OutT, E>(cp, d);
+          st_vec<OutT, E>(reinterpret_cast<OutT*>(p.c2) + rel, v);
         } else {
           st_vec<OutT, E>(cp, v);
         }
@@ -301,9 +313,13 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
         for (int i = 0; i < E; ++i) {  // compile-time indices keep v[] in registers
           if (i >= valid) break;
           float x = v[i];
-          if constexpr (DG) x *= gelu_grad_fast(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
+          if constexpr (EPI == OASES_EPI_DGELU) x *= gelu_grad_fast(to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]));
+          if constexpr (EPI == OASES_EPI_MUL) x *= to_f(reinterpret_cast<const OutT*>(p.aux)[rel + i]);
           if constexpr (ACC) x += to_f(cp[i]);
-          if constexpr (EPI == OASES_EPI_BIAS_GELU) {
+          if constexpr (EPI == OASES_EPI_BIAS_GELU_GRAD) {
+            cp[i] = from_f<OutT>(gelu_grad_fast(x));
+            reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_fast(x));
+          } else if constexpr (EPI == OASES_EPI_BIAS_GELU) {
             if (p.c2) {
               cp[i] = from_f<OutT>(x);
               reinterpret_cast<OutT*>(p.c2)[rel + i] = from_f<OutT>(gelu_fast(x));
@@ -343,19 +359,21 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
 }
 
 // Calls BODY(OutT, EPI, ACC) for the runtime mode of p (compile-time specialised).
-#define OASES_EPI_DISPATCH(p, BODY)                                                      \
-  do {                                                                                   \
-    const int mode_ = ((p).c_f32 ? 8 : 0) + (p).epilogue * 2 + ((p).accumulate ? 1 : 0); \
-    switch (mode_) {                                                                     \
-      case 0: BODY(__nv_bfloat16, 0, false); break;                                      \
-      case 2: BODY(__nv_bfloat16, 1, false); break;                                      \
-      case 4: BODY(__nv_bfloat16, 2, false); break;                                      \
-      case 6: BODY(__nv_bfloat16, 3, false); break;                                      \
-      case 8: BODY(float, 0, false); break;                                              \
-      case 9: BODY(float, 0, true); break;                                               \
-      case 10: BODY(float, 1, false); break;                                             \
-      default: BODY(float, 1, true); break;                                              \
-    }                                                                                    \
+#define OASES_EPI_DISPATCH(p, BODY)                                                       \
+  do {                                                                                    \
+    const int mode_ = ((p).c_f32 ? 16 : 0) + (p).epilogue * 2 + ((p).accumulate ? 1 : 0); \
+    switch (mode_) {                                                                      \
+      case 0: BODY(__nv_bfloat16, 0, false); break;                                       \
+      case 2: BODY(__nv_bfloat16, 1, false); break;                                       \
+      case 4: BODY(__nv_bfloat16, 2, false); break;                                       \
+      case 6: BODY(__nv_bfloat16, 3, false); break;                                       \
+      case 8: BODY(__nv_bfloat16, 4, false); break;                                       \
+      case 10: BODY(__nv_bfloat16, 5, false); break;                                      \
+      case 16: BODY(float, 0, false); break;                                              \
+      case 17: BODY(float, 0, true); break;                                               \
+      case 18: BODY(float, 1, false); break;                                              \
+      default: BODY(float, 1, true); break;                                               \
+    }                                                                                     \
   } while (0)
 
 // ----------------------------------------------------------------- single-CTA kernel
@@ -888,7 +906,7 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
     *err = "gemm_tc: empty problem";
     return false;
   }
-  if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_DGELU) {
+  if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_MUL) {
     *err = "gemm_tc: unknown epilogue";
     return false;
   }

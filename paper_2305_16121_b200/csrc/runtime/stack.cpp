@@ -745,13 +745,14 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
     gemm(d);
     attention_fwd(w, block, sb, ws);
   } else {
-    d.epilogue = OASES_EPI_BIAS_GELU;
     if (cfg_.recompute) {
-      // the recompute pass regenerates the pre-activation the backward needs
-      // (dGeLU); here only the activation feeding FC2 is live
+      // the recompute pass regenerates gelu'(pre) for the backward; here only
+      // the activation feeding FC2 is live
+      d.epilogue = OASES_EPI_BIAS_GELU;
       d.c = ws.act;
       d.c2 = nullptr;
     } else {
+      d.epilogue = OASES_EPI_BIAS_GELU_GRAD;  // ws.col = gelu'(pre) for the dgrad, ws.act = gelu(pre)
       d.c2 = ws.act;
     }
     gemm(d);
@@ -802,7 +803,8 @@ void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) 
     gemm(d);
     attention_fwd(w, block, sb, ws);
   } else {
-    d.epilogue = OASES_EPI_BIAS_GELU;
+    // ws.col = gelu'(pre) (the factor the FC2 dgrad epilogue multiplies by), ws.act = gelu(pre)
+    d.epilogue = OASES_EPI_BIAS_GELU_GRAD;
     d.c2 = ws.act;
     gemm(d);
   }
@@ -909,9 +911,10 @@ void Stack::backward(int wi, int block, int sb) {
     gemm2(dw, d);
     attention_bwd(w, block, sb, ws);
   } else {
-    // dpre = (g_ar W_row) o gelu'(pre)   (hadamard + gelu_grad fused, numerics.cpp:203-204)
+    // dpre = (g_ar W_row) o gelu'(pre)   (hadamard + gelu_grad, numerics.cpp:203-204; gelu'(pre)
+    // was stored by the FC1 epilogue that produced the activation)
     d.c = w.dcol; d.ldc = ncol;
-    d.epilogue = OASES_EPI_DGELU;
+    d.epilogue = OASES_EPI_MUL;
     d.aux = ws.col;
     gemm2(dw, d);
   }

@@ -196,3 +196,30 @@ def test_gemm_gelu_activation_only(cuda, dt):
     ops.gemm(M, N, K, ops.operand(A), ops.operand(B), only, epilogue=capi.EPI_BIAS_GELU, bias=bias, dtype=kdt)
     torch.cuda.synchronize()
     assert torch.equal(only, act)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_gemm_gelu_grad_and_mul_epilogues(cuda, dt):
+    """BIAS_GELU_GRAD stores gelu'(v) and gelu(v); MUL multiplies by AUX: together
+    they equal the DGELU epilogue on the pre-activation (the FFN backward)."""
+    torch.manual_seed(10)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    kdt = capi.BF16 if dt == "bf16" else capi.F32
+    M, N, K = 384, 512, 256
+    A = torch.randn(M, K, device=cuda).to(tdt)
+    B = (torch.randn(N, K, device=cuda) / math.sqrt(K)).to(tdt)
+    bias = torch.randn(N, device=cuda).to(tdt)
+    v = A.double() @ B.double().t() + bias.double()
+    dgl, act = torch.empty(M, N, device=cuda, dtype=tdt), torch.empty(M, N, device=cuda, dtype=tdt)
+    ops.gemm(M, N, K, ops.operand(A), ops.operand(B), dgl, epilogue=capi.EPI_BIAS_GELU_GRAD, bias=bias, c2=act,
+             dtype=kdt)
+    torch.cuda.synchronize()
+    tol = 1e-2 if dt == "bf16" else 1e-5
+    assert relerr(dgl, gelu_grad64(v)) < tol
+    assert relerr(act, gelu64(v)) < tol
+    G = torch.randn(M, K, device=cuda).to(tdt)
+    W = (torch.randn(N, K, device=cuda) / math.sqrt(K)).to(tdt)
+    out = torch.empty(M, N, device=cuda, dtype=tdt)
+    ops.gemm(M, N, K, ops.operand(G), ops.operand(W), out, epilogue=capi.EPI_MUL, aux=dgl, dtype=kdt)
+    torch.cuda.synchronize()
+    assert relerr(out, (G.double() @ W.double().t()) * dgl.double()) < tol
