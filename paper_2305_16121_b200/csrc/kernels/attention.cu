@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int it = 0; it < ni; ++it) {
         const int st = it & 1, i = kt + it;
         mbar_wait(&st_empty[st], ((it >> 1) & 1) ^ 1);
+        ATRACE(0, it);
         uint8_t* sp = smem + C::STAGE_OFF + st * C::STAGE_BYTES;
         mbar_arrive_expect_tx(&st_full[st], C::STAGE_BYTES);
 #pragma unroll
@@ -697,6 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t qa = stage_addr(it), da = qa + C::TILE_BYTES;
         // dV += (keep o P)^T dO   (A: keys x queries, MN-major view of the [query][key] buffer)
         mbar_wait(pd_full, it & 1);
+        ATRACE(1, it);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk)
@@ -706,6 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it + 1 < ni) issue_s(it + 1);
         // dK += dS^T Q
         mbar_wait(ds_full, it & 1);
+        ATRACE(2, it);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk)
@@ -741,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           static_cast<unsigned long long>(kt) * kTile + c0;
       // pass 1: P = exp2(S*sl2 - lse) (kept in registers as bf16), keep o P -> buffer
       mbar_wait(s_full, it & 1);
+      if (warp == 2 && lane == 0) ATRACE(3, it);
       tc_fence_after();
       uint32_t u[2][32];
       tmem_ld32(tl + t_s + c0, u[0]);
@@ -781,9 +785,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         *tile_chunk(buf, r, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
       fence_proxy_async();
       __syncwarp();
+      if (warp == 2 && lane == 0) ATRACE(4, it);
       if (lane == 0) mbar_arrive(pd_full);
       // pass 2: dS = scale * (ks * (keep o P) o dP_drop - P D) -> buffer (after the dV MMA read it)
       mbar_wait(dp_full, it & 1);
+      if (warp == 2 && lane == 0) ATRACE(5, it);
       tc_fence_after();
       uint32_t v[2][32];
       tmem_ld32(tl + t_dp + c0, v[0]);
@@ -802,12 +808,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[k] = pack_bf16(d0, d1);
       }
       mbar_wait(buf_free1, it & 1);
+      if (warp == 2 && lane == 0) ATRACE(6, it);
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch)
         *tile_chunk(buf, r, hf * 8 + ch) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
       fence_proxy_async();
       named_bar_sync(1, 32 * kRowWarps);
       if (leader) {
+        ATRACE(7, it);
         mbar_arrive(ds_full);
         const int y = z * p.seq + i * kTile;
         tma_store_2d(&tds, buf, kt * kTile, y);
