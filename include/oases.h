@@ -122,6 +122,11 @@ oases_status oases_gemm_grouped(const oases_gemm_desc* descs, int32_t count, voi
 /*   bwd:  dout like out; dqkv like qkv (all three blocks written);          */
 /*         ds [samples*heads_local*seq, seq] bf16 scratch (dS, causal band); */
 /*         workspace: oases_attention_bwd_workspace() bytes                  */
+/*   mask_bits (optional, dropout on): cache of the Philox keep bits, one    */
+/*         bit per causal-band element, oases_attention_mask_bytes() bytes.  */
+/*         mask_mode 0: generate (Philox); 1: generate and store (forward);  */
+/*         2: read (recompute forward, backward) -- the bits ARE the Philox  */
+/*         results, so every mode computes the same values.                  */
 /* ------------------------------------------------------------------------ */
 typedef struct {
   int32_t dtype; /* OASES_BF16 */
@@ -140,11 +145,15 @@ typedef struct {
   void* workspace;
   float scale, dropout_p;
   uint64_t seed, offset;
+  uint32_t* mask_bits;
+  int32_t mask_mode;
+  int32_t pad_;
 } oases_attn_desc;
 
 int32_t oases_attention_supported(int dtype, int32_t head_dim, int32_t seq);
 oases_status oases_attention_fwd(const oases_attn_desc* desc, void* stream);
 size_t oases_attention_bwd_workspace(const oases_attn_desc* desc);
+size_t oases_attention_mask_bytes(const oases_attn_desc* desc);
 oases_status oases_attention_bwd(const oases_attn_desc* desc, void* stream);
 
 /* ------------------------------------------------------------------------ */

@@ -75,7 +75,16 @@ struct AttnParams {
   float ks;                 // keep scale
   uint64_t seed, offset;
   uint32_t rk0[10], rk1[10];  // Philox round keys of `seed` (constant-bank operands of the round LOP3s)
+  uint32_t* mask_bits;        // keep-bit cache [Z][causal tile][128 rows][4 words] (null: always Philox)
+  int mask_mode;              // 0 generate, 1 generate + store, 2 load
 };
+
+// Word index of (row, 32-column group w) of causal tile (qt, kt) of head z in
+// the keep-bit cache: tiles of a head in row-major causal order.
+__device__ __forceinline__ long long mask_word(const AttnParams& p, int z, int qt, int kt, int row, int w) {
+  const long long tile = static_cast<long long>(z) * (p.nq * (p.nq + 1) / 2) + qt * (qt + 1) / 2 + kt;
+  return (tile * kTile + row) * 4 + w;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -134,6 +143,43 @@ __device__ __forceinline__ void keep_masks16(const PhiloxLite& ps, const AttnPar
     m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
   }
 }
+// keep_masks16 plus the 16 keep bits (bit e = element e of the group).
+__device__ __forceinline__ uint32_t keep_masks16_bits(const PhiloxLite& ps, const AttnParams& prm,
+                                                      unsigned long long ctr, uint32_t (&m)[8]) {
+  uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = ps.o0, c3 = ps.o1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = static_cast<unsigned long long>(0xD2511F53u) * c0;
+    const unsigned long long p1 = static_cast<unsigned long long>(0xCD9E8D57u) * c2;
+    const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ prm.rk0[r];
+    const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ prm.rk1[r];
+    c1 = static_cast<uint32_t>(p1);
+    c3 = static_cast<uint32_t>(p0);
+    c0 = n0;
+    c2 = n2;
+  }
+  const uint32_t u[4] = {c0, c1, c2, c3};
+  uint32_t bits = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t k = __vcmpgeu4(u[w], ps.thr4);
+    m[2 * w] = __byte_perm(k, 0, 0x1100);
+    m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
+    bits |= (((k & 0x01010101u) * 0x01020408u) >> 24) << (4 * w);  // 4 byte flags -> 4 bits
+  }
+  return bits;
+}
+// The 8 bf16x2 lane masks of 16 cached keep bits.
+__device__ __forceinline__ void masks16_from_bits(uint32_t bits, uint32_t (&m)[8]) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t nib = (bits >> (4 * w)) & 0xFu;
+    const uint32_t k = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;  // 4 bits -> 4 byte flags
+    m[2 * w] = __byte_perm(k, 0, 0x1100);
+    m[2 * w + 1] = __byte_perm(k, 0, 0x3322);
+  }
+}
+
 // Static zigzag schedule of work items over a persistent grid. Items are
 // numbered heaviest first; round r hands CTA c item r*G + c (r even) or
 // r*G + G-1-c (r odd), which balances the decreasing item sizes.
@@ -385,8 +431,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               static_cast<unsigned long long>(p.seq) +
           c0;
       float m = -INFINITY, l = 0.f;
+      // cached keep bits: the word of tile j + 1 is loaded while tile j is processed
+      const bool cached = p.thr && p.mask_mode == 2;
+      uint32_t mword = cached ? p.mask_bits[mask_word(p, z, qt, 0, rr, part)] : 0u;
       for (int j = 0; j <= qt; ++j, ++g) {
         const int st = g % C::NS;
+        const uint32_t bits_j = mword;
+        if (cached && j < qt) mword = p.mask_bits[mask_word(p, z, qt, j + 1, rr, part)];
 #ifdef OASES_EXP_ONESPIN
         if (part == 0) mbar_wait(&s_full[st], (g / C::NS) & 1);
         named_bar_sync(1 + q, 128);
@@ -458,12 +509,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         l = l * alpha + sum;
         m = mx;
         if (p.thr) {
+          if (cached) {  // keep bits stored by the forward pass
 #pragma unroll
-          for (int gq = 0; gq < 2; ++gq) {
-            uint32_t km[8];
-            keep_masks16(ph, p, (ebase + static_cast<unsigned long long>(j) * kTile + gq * 16) >> 4, km);
+            for (int gq = 0; gq < 2; ++gq) {
+              uint32_t km[8];
+              masks16_from_bits(bits_j >> (16 * gq), km);
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) pk[gq * 8 + kk] &= km[kk];
+              for (int kk = 0; kk < 8; ++kk) pk[gq * 8 + kk] &= km[kk];
+            }
+          } else {
+            uint32_t bits = 0;
+#pragma unroll
+            for (int gq = 0; gq < 2; ++gq) {
+              uint32_t km[8];
+              bits |= keep_masks16_bits(ph, p, (ebase + static_cast<unsigned long long>(j) * kTile + gq * 16) >> 4,
+                                        km)
+                      << (16 * gq);
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) pk[gq * 8 + kk] &= km[kk];
+            }
+            if (p.mask_mode == 1) p.mask_bits[mask_word(p, z, qt, j, rr, part)] = bits;
           }
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
@@ -730,8 +795,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = threadIdx.x == 64;
     PhiloxLite ph;
     philox_init(p, ph);
+    // cached keep bits: the two words of query tile it + 1 load while tile it is processed
+    const bool cached = p.thr && p.mask_mode == 2;
+    uint32_t mw0 = 0u, mw1 = 0u;
+    if (cached) {
+      mw0 = p.mask_bits[mask_word(p, z, kt, kt, r, hf * 2)];
+      mw1 = p.mask_bits[mask_word(p, z, kt, kt, r, hf * 2 + 1)];
+    }
     for (int it = 0; it < ni; ++it) {
       const int st = it & 1, i = kt + it;
+      const uint32_t bw0 = mw0, bw1 = mw1;
+      if (cached && it + 1 < ni) {
+        mw0 = p.mask_bits[mask_word(p, z, i + 1, kt, r, hf * 2)];
+        mw1 = p.mask_bits[mask_word(p, z, i + 1, kt, r, hf * 2 + 1)];
+      }
       const uint8_t* sp = smem + C::STAGE_OFF + st * C::STAGE_BYTES;
       mbar_wait(&st_full[st], (it >> 1) & 1);
       const float nlse = -reinterpret_cast<const float*>(sp + 2 * C::TILE_BYTES)[r];
@@ -766,12 +843,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int k = 0; k < 32; ++k) pk[k] = pp[k];
       if (p.thr) {
+        if (cached) {  // keep bits stored by the forward pass
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t km[8];
-          keep_masks16(ph, p, (ebase + g * 16) >> 4, km);
+          for (int g = 0; g < 4; ++g) {
+            uint32_t km[8];
+            masks16_from_bits(((g >> 1) ? bw1 : bw0) >> (16 * (g & 1)), km);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
+            for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
+          }
+        } else {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint32_t km[8];
+            keep_masks16(ph, p, (ebase + g * 16) >> 4, km);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) pk[g * 8 + k] &= km[k];
+          }
         }
       }
       // the previous dK MMA and dS store must be done with the buffer
@@ -896,6 +983,12 @@ bool fill_common(AttnParams& p, const oases_attn_desc& d, std::string* err) {
   p.ks = dropout_keep_scale(d.dropout_p);
   p.seed = d.seed;
   p.offset = d.offset;
+  p.mask_bits = d.mask_bits;
+  p.mask_mode = (d.mask_bits && p.thr) ? d.mask_mode : 0;
+  if (p.mask_mode < 0 || p.mask_mode > 2) {
+    *err = "attention: mask_mode must be 0, 1 or 2";
+    return false;
+  }
   uint32_t a = static_cast<uint32_t>(d.seed), b = static_cast<uint32_t>(d.seed >> 32);
   for (int r = 0; r < 10; ++r) {
     p.rk0[r] = a;
@@ -916,6 +1009,12 @@ extern "C" int oases_attn_trace_dump(unsigned long long* host) {
 
 bool attention_supported(int dtype, int head_dim, int seq) {
   return dtype == OASES_BF16 && (head_dim == 64 || head_dim == 128) && seq > 0 && seq % kTile == 0;
+}
+
+size_t attention_mask_bytes(const oases_attn_desc& d) {
+  if (d.seq <= 0 || d.seq % kTile) return 0;
+  const long long nq = d.seq / kTile;
+  return static_cast<size_t>(d.samples) * d.heads_local * (nq * (nq + 1) / 2) * kTile * 4 * sizeof(uint32_t);
 }
 
 size_t attention_bwd_workspace(const oases_attn_desc& d) {

@@ -33,6 +33,7 @@ bool make_tma_bf16_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t c
 bool attention_supported(int dtype, int head_dim, int seq);
 GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream);
 size_t attention_bwd_workspace(const oases_attn_desc& d);
+size_t attention_mask_bytes(const oases_attn_desc& d);
 GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream);
 
 }  // namespace oases

@@ -105,6 +105,8 @@ size_t oases_attention_bwd_workspace(const oases_attn_desc* d) {
   return d ? oases::attention_bwd_workspace(*d) : 0;
 }
 
+size_t oases_attention_mask_bytes(const oases_attn_desc* d) { return d ? oases::attention_mask_bytes(*d) : 0; }
+
 oases_status oases_attention_bwd(const oases_attn_desc* d, void* stream) {
   return guarded([&] {
     if (!d) throw tmpsim::ConfigError("oases_attention_bwd: null descriptor");

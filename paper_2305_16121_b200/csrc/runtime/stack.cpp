@@ -267,6 +267,17 @@ void Stack::alloc_all() {
     w.dcol = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
     if (prob) w.dp = arena_.alloc(static_cast<size_t>(prob) * es);
     if (prob && fused_attn_) w.attn_ws = arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float));
+    if (prob && fused_attn_ && cfg_.p_attn > 0.f) {
+      oases_attn_desc md{};
+      md.samples = static_cast<int>(bh);
+      md.heads_local = hl_;
+      md.seq = static_cast<int>(cfg_.s);
+      const size_t mbytes = attention_mask_bytes(md);
+      w.mask_bits.assign(static_cast<size_t>(nblocks_ / 2 + 1), {nullptr, nullptr});
+      for (int b = 0; b < nblocks_; b += 2)
+        for (int sb = 0; sb < 2; ++sb)
+          w.mask_bits[static_cast<size_t>(b / 2)][static_cast<size_t>(sb)] = static_cast<uint32_t*>(arena_.alloc(mbytes));
+    }
     w.y = arena_.alloc(static_cast<size_t>(Ts * h) * es);
     w.ln_ws = arena_.alloc(layernorm_bwd_workspace(Ts, static_cast<int>(h)));
     w.col_ws = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
@@ -601,6 +612,13 @@ oases_attn_desc Stack::attn_desc(Worker& w, int block, int sb, const Workspace& 
   a.ld_dqkv = ncol_attn_;
   a.ds = w.dp;
   a.workspace = w.attn_ws;
+  // keep-bit cache unless OASES_ATTN_MASK_CACHE=0 (A/B runs: Philox in every pass)
+  static const bool cache = [] {
+    const char* e = std::getenv("OASES_ATTN_MASK_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  if (cache && !w.mask_bits.empty())
+    a.mask_bits = w.mask_bits[static_cast<size_t>(block / 2)][static_cast<size_t>(sb)];
   a.scale = 1.f / std::sqrt(static_cast<float>(dh_));
   a.dropout_p = cfg_.p_attn;
   a.seed = cfg_.seed;
@@ -608,13 +626,14 @@ oases_attn_desc Stack::attn_desc(Worker& w, int block, int sb, const Workspace& 
   return a;
 }
 
-void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws) {
+void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int mask_mode) {
   const int64_t s = cfg_.s, Ts = tokens_sub(), bh = cfg_.b / 2, Z = bh * hl_, nc = ncol_attn_, nr = nrow_attn_;
   const int64_t hd = static_cast<int64_t>(hl_) * dh_;
   const char* qkv = static_cast<const char*>(ws.col);
   const size_t es = esize();
   if (fused_attn_) {
-    const oases_attn_desc a = attn_desc(w, block, sb, ws);
+    oases_attn_desc a = attn_desc(w, block, sb, ws);
+    a.mask_mode = mask_mode;
     const GemmStatus st = oases::attention_fwd(a, ctx_.compute);
     if (!st.ok) {
       if (st.cuda) throw CudaError(st.err);
@@ -658,7 +677,8 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   const char* qkv = static_cast<const char*>(ws.col);
   char* dqkv = static_cast<char*>(w.dcol);
   if (fused_attn_) {
-    const oases_attn_desc a = attn_desc(w, block, sb, ws);
+    oases_attn_desc a = attn_desc(w, block, sb, ws);
+    a.mask_mode = 2;  // the forward pass stored the keep bits
     const GemmStatus st = oases::attention_bwd(a, ctx_.compute);
     if (!st.ok) {
       if (st.cuda) throw CudaError(st.err);
@@ -743,7 +763,7 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
   if (att) {
     d.epilogue = OASES_EPI_BIAS;
     gemm(d);
-    attention_fwd(w, block, sb, ws);
+    attention_fwd(w, block, sb, ws, 1);  // generate + store the keep bits
   } else {
     if (cfg_.recompute) {
       // the recompute pass regenerates gelu'(pre) for the backward; here only
@@ -801,7 +821,7 @@ void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) 
   if (att) {
     d.epilogue = OASES_EPI_BIAS;
     gemm(d);
-    attention_fwd(w, block, sb, ws);
+    attention_fwd(w, block, sb, ws, 2);  // the forward pass stored the keep bits
   } else {
     // ws.col = gelu'(pre) (the factor the FC2 dgrad epilogue multiplies by), ws.act = gelu(pre)
     d.epilogue = OASES_EPI_BIAS_GELU_GRAD;

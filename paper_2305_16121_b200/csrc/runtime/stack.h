@@ -97,6 +97,9 @@ struct Worker {
   void* dcol = nullptr;  // [T_sub, ncol_max]
   void* dp = nullptr;    // [bh*Hl*s, s]  dP_drop then dS (fused attention: dS only)
   void* attn_ws = nullptr;  // fused attention backward workspace (rowsum(dO o O))
+  // attention-dropout keep bits per [attention block][sb], written by the
+  // forward pass, read by the recompute forward and the backward
+  std::vector<std::array<uint32_t*, 2>> mask_bits;
   void* y = nullptr;     // [T_sub, h] final output for the loss head
   void* ln_ws = nullptr;
   void* col_ws = nullptr;
@@ -161,7 +164,7 @@ class Stack {
   void ln_fwd(const void* x, const void* g, const void* b, void* y);
   void bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln);
   oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
-  void attention_fwd(Worker& w, int block, int sb, const Workspace& ws);
+  void attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int mask_mode);
   void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
   Workspace& ws_for(Worker& w, int block, int sb);
   bool touch(const Worker& w, int block, int p);  // true if the gradient must accumulate (written this step)

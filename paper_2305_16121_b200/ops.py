@@ -112,18 +112,28 @@ def _attn_desc(qkv, samples, heads, head_dim, seq, scale, dropout_p, seed, offse
     return d
 
 
+def attention_mask_bytes(samples, heads, seq):
+    """Bytes of the attention-dropout keep-bit cache (mask_bits) for this shape."""
+    d = capi.AttnDesc()
+    d.samples, d.heads_local, d.seq = samples, heads, seq
+    return capi.lib().oases_attention_mask_bytes(C.byref(d))
+
+
 def attention_fwd(qkv, out, lse, samples, heads, head_dim, seq, scale, dropout_p=0.0, seed=0, offset=0,
-                  heads_total=0, head_offset=0, stream=None):
-    """Fused causal attention: qkv [samples*seq, >=3*heads*head_dim] (Q|K|V blocks) -> out (ctx), lse (f32)."""
+                  heads_total=0, head_offset=0, stream=None, mask_bits=None, mask_mode=0):
+    """Fused causal attention: qkv [samples*seq, >=3*heads*head_dim] (Q|K|V blocks) -> out (ctx), lse (f32).
+    mask_bits/mask_mode: keep-bit cache (0 generate, 1 generate + store, 2 read)."""
     d = _attn_desc(qkv, samples, heads, head_dim, seq, scale, dropout_p, seed, offset, heads_total, head_offset)
     d.out, d.ld_out, d.lse = _ptr(out), out.stride(0), _ptr(lse)
+    d.mask_bits, d.mask_mode = _ptr(mask_bits), mask_mode
     check(capi.lib().oases_attention_fwd(C.byref(d), _stream(stream)))
 
 
 def attention_bwd(qkv, out, lse, dout, dqkv, samples, heads, head_dim, seq, scale, dropout_p=0.0, seed=0, offset=0,
-                  heads_total=0, head_offset=0, ds=None, stream=None):
+                  heads_total=0, head_offset=0, ds=None, stream=None, mask_bits=None, mask_mode=0):
     """Backward of attention_fwd: writes dQ | dK | dV into dqkv (dS scratch allocated when not given)."""
     d = _attn_desc(qkv, samples, heads, head_dim, seq, scale, dropout_p, seed, offset, heads_total, head_offset)
+    d.mask_bits, d.mask_mode = _ptr(mask_bits), mask_mode
     d.out, d.ld_out, d.lse = _ptr(out), out.stride(0), _ptr(lse)
     d.dout, d.ld_dout = _ptr(dout), dout.stride(0)
     d.dqkv, d.ld_dqkv = _ptr(dqkv), dqkv.stride(0)

@@ -95,3 +95,37 @@ def test_fused_attention_deterministic_and_rejects(cuda):
     assert not ops.attention_supported(torch.float32, 128, 512)
     with pytest.raises(Exception):
         ops.attention_fwd(qkv, out, lse, n, hl, dh, 500, 0.125)
+
+
+@pytest.mark.parametrize("dh,hl,hg,hoff,s", [(128, 2, 4, 2, 384), (64, 3, 3, 0, 256)])
+def test_keep_bit_cache_modes_bit_identical(cuda, dh, hl, hg, hoff, s):
+    """The keep-bit cache stores exactly the Philox decisions: forward with
+    generate / generate+store / read, and backward with generate / read, give the
+    same bits."""
+    torch.manual_seed(5)
+    n, p, seed, off = 2, 0.1, 11, 7
+    hd = hl * dh
+    qkv = torch.randn(n * s, 3 * hd, device=cuda).bfloat16()
+    scale = 1 / math.sqrt(dh)
+    bits = torch.zeros(ops.attention_mask_bytes(n, hl, s) // 4, dtype=torch.int32, device=cuda)
+    outs, lses = [], []
+    for mode in (0, 1, 2):
+        out = torch.empty(n * s, hd, device=cuda, dtype=torch.bfloat16)
+        lse = torch.empty(n * hl * s, device=cuda)
+        ops.attention_fwd(qkv, out, lse, n, hl, dh, s, scale, p, seed, off, heads_total=hg, head_offset=hoff,
+                          mask_bits=bits, mask_mode=mode)
+        outs.append(out)
+        lses.append(lse)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert torch.equal(lses[0], lses[2])
+    assert bits.abs().sum().item() > 0
+    dout = torch.randn(n * s, hd, device=cuda).bfloat16()
+    grads = []
+    for mode in (0, 2):
+        dqkv = torch.empty_like(qkv)
+        ops.attention_bwd(qkv, outs[0], lses[0], dout, dqkv, n, hl, dh, s, scale, p, seed, off, heads_total=hg,
+                          head_offset=hoff, mask_bits=bits, mask_mode=mode)
+        grads.append(dqkv)
+    torch.cuda.synchronize()
+    assert torch.equal(grads[0], grads[1])
