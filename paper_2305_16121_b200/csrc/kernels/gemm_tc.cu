@@ -80,11 +80,24 @@ struct TileInfo {
 
 template <int BN>
 __device__ __forceinline__ bool decode_tile(const TcParams& p, int t, TileInfo& ti) {
-  const int per_z = p.tiles_m * p.tiles_n;
-  ti.z = t / per_z;
-  const int r = t - ti.z * per_z;
-  const int mt = r / p.tiles_n;
-  const int nt = r - mt * p.tiles_n;
+  int mt, nt;
+  if (p.causal == OASES_CAUSAL_K_UPTO_M || p.causal == OASES_CAUSAL_K_FROM_M) {
+    // Causal K ranges make tile cost grow (UPTO) or shrink (FROM) with the
+    // m-tile: order tiles heaviest-first across the whole batch (m-tile is the
+    // slowest index) so the static persistent stride balances like LPT.
+    const int per_m = p.batch * p.tiles_n;
+    const int mi = t / per_m;
+    const int r = t - mi * per_m;
+    mt = p.causal == OASES_CAUSAL_K_UPTO_M ? p.tiles_m - 1 - mi : mi;
+    ti.z = r / p.tiles_n;
+    nt = r - ti.z * p.tiles_n;
+  } else {
+    const int per_z = p.tiles_m * p.tiles_n;
+    ti.z = t / per_z;
+    const int r = t - ti.z * per_z;
+    mt = r / p.tiles_n;
+    nt = r - mt * p.tiles_n;
+  }
   ti.m0 = mt * BM;
   ti.n0 = nt * BN;
   if (p.causal == OASES_CAUSAL_SKIP_UPPER && ti.n0 > ti.m0 + BM - 1) return false;
