@@ -73,7 +73,11 @@ typedef enum {
   OASES_EPI_DGELU = 3,     /* C = alpha*acc * gelu'(AUX[m,n])  (hadamard+gelu_grad, numerics.cpp:204) */
   OASES_EPI_BIAS_GELU_GRAD = 4, /* v = alpha*acc + bias[n]; C = gelu'(v), C2 = gelu(v)  (the recompute FC1:
                                    stores the factor the dgrad needs instead of the pre-activation) */
-  OASES_EPI_MUL = 5        /* C = alpha*acc * AUX[m,n]  (dgrad with a stored gelu'(pre)) */
+  OASES_EPI_MUL = 5,       /* C = alpha*acc * AUX[m,n]  (dgrad with a stored gelu'(pre)) */
+  OASES_EPI_ROWDOT = 6     /* C = alpha*acc (bf16); ROWDOT[(m / seq * heads + g) * seq + m % seq] =
+                              sum over the columns of group g (rowdot_group wide) of C[m,n]*AUX[m,n]:
+                              the attention backward's D = rowsum(dO o O) per head, fused into the
+                              GEMM producing dO */
 } oases_epilogue;
 
 typedef enum {
@@ -102,6 +106,10 @@ typedef struct {
   void* c2;             /* BIAS_GELU activation output, same layout/offsets/dtype as C */
   int32_t max_ctas;     /* persistent grid cap (0 = all SMs); leaves SMs to NCCL */
   int32_t pad_;
+  float* rowdot;                    /* ROWDOT output (f32) */
+  int32_t rowdot_group;             /* columns per group (head dim: 64 | 128) */
+  int32_t rowdot_seq, rowdot_heads; /* rows per sample, groups per row */
+  int32_t pad2_;
 } oases_gemm_desc;
 
 oases_status oases_gemm(const oases_gemm_desc* desc, void* stream);
@@ -147,7 +155,7 @@ typedef struct {
   uint64_t seed, offset;
   uint32_t* mask_bits;
   int32_t mask_mode;
-  int32_t pad_;
+  int32_t dsum_ready; /* bwd: workspace already holds D = rowsum(dO o O) (e.g. an EPI_ROWDOT GEMM) */
 } oases_attn_desc;
 
 int32_t oases_attention_supported(int dtype, int32_t head_dim, int32_t seq);

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("OASES_LIB") or os.path.join(_HERE, "liboases.so")
 
 OK, ERR_CONFIG, ERR_INFEASIBLE, ERR_IO, ERR_CUDA, ERR_NCCL = 0, 2, 3, 4, 5, 6
 F32, BF16 = 0, 1
-EPI_NONE, EPI_BIAS, EPI_BIAS_GELU, EPI_DGELU, EPI_BIAS_GELU_GRAD, EPI_MUL = 0, 1, 2, 3, 4, 5
+EPI_NONE, EPI_BIAS, EPI_BIAS_GELU, EPI_DGELU, EPI_BIAS_GELU_GRAD, EPI_MUL, EPI_ROWDOT = 0, 1, 2, 3, 4, 5, 6
 CAUSAL_NONE, CAUSAL_SKIP_UPPER, CAUSAL_K_UPTO_M, CAUSAL_K_FROM_M = 0, 1, 2, 3
 
 
@@ -61,6 +61,11 @@ class GemmDesc(C.Structure):
         ("c2", C.c_void_p),
         ("max_ctas", C.c_int32),
         ("pad_", C.c_int32),
+        ("rowdot", C.c_void_p),
+        ("rowdot_group", C.c_int32),
+        ("rowdot_seq", C.c_int32),
+        ("rowdot_heads", C.c_int32),
+        ("pad2_", C.c_int32),
     ]
 
 
@@ -91,7 +96,7 @@ class AttnDesc(C.Structure):
         ("offset", C.c_uint64),
         ("mask_bits", C.c_void_p),
         ("mask_mode", C.c_int32),
-        ("pad_", C.c_int32),
+        ("dsum_ready", C.c_int32),
     ]
 
 

@@ -1102,11 +1102,12 @@ GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream) {
   const unsigned dgrid = static_cast<unsigned>((drows * (d.head_dim / 8) + 255) / 256);
   const auto* dO = static_cast<const __nv_bfloat16*>(d.dout);
   const auto* O = static_cast<const __nv_bfloat16*>(d.out);
-  cudaError_t e = d.head_dim == 128
-                      ? launch_pdl(attn_dsum_kernel<128>, dim3(dgrid), dim3(256), 0, stream, dO, O, d.ld_dout, dsum,
-                                   d.seq, d.heads_local, 0, drows)
-                      : launch_pdl(attn_dsum_kernel<64>, dim3(dgrid), dim3(256), 0, stream, dO, O, d.ld_dout, dsum,
-                                   d.seq, d.heads_local, 0, drows);
+  cudaError_t e = cudaSuccess;
+  if (!d.dsum_ready)  // else the GEMM that produced dO wrote D (EPI_ROWDOT)
+    e = d.head_dim == 128 ? launch_pdl(attn_dsum_kernel<128>, dim3(dgrid), dim3(256), 0, stream, dO, O, d.ld_dout,
+                                       dsum, d.seq, d.heads_local, 0, drows)
+                          : launch_pdl(attn_dsum_kernel<64>, dim3(dgrid), dim3(256), 0, stream, dO, O, d.ld_dout,
+                                       dsum, d.seq, d.heads_local, 0, drows);
   if (e == cudaSuccess) {
     p.out = d.dqkv;
     p.ld_out = d.ld_dqkv;

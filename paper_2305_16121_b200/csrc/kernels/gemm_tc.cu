@@ -72,6 +72,8 @@ struct TcParams {
   int causal;
   int accumulate;
   float alpha;
+  float* rowdot;  // EPI_ROWDOT output
+  int rd_group, rd_seq, rd_heads;
 };
 
 struct TileInfo {
@@ -215,7 +217,7 @@ __device__ __forceinline__ void epi_prefetch(const TcParams& p, int c, int nbeg,
   for (int it = 0; it < G::IT; ++it) {
     const bool ok = full && it * G::RPI + lr < rows_left;
     const long long off = lane_base + nbeg + c * 32 + it * step;
-    if constexpr (EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL) {
+    if constexpr (EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL || EPI == OASES_EPI_ROWDOT) {
       pa[it] = make_uint4(0u, 0u, 0u, 0u);
       if (ok) pa[it] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const OutT*>(p.aux) + off));
     }
@@ -230,11 +232,12 @@ __device__ __forceinline__ void epi_prefetch(const TcParams& p, int c, int nbeg,
 template <typename OutT, int EPI, bool ACC>
 __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, long long row0, long long col0, int lr,
                                           int lc, int rows_left, long long step, long long lane_base, uint32_t taddr,
-                                          float4* stg, int lane) {
+                                          float4* stg, int lane, float (&racc)[StripeGeo<OutT>::IT]) {
   using G = StripeGeo<OutT>;
   constexpr int E = G::E, RPI = G::RPI, IT = G::IT;
   constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU || EPI == OASES_EPI_BIAS_GELU_GRAD;
-  constexpr bool DG = EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL;  // epilogues reading AUX
+  constexpr bool RD = EPI == OASES_EPI_ROWDOT;
+  constexpr bool DG = EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL || RD;  // epilogues reading AUX
   const int nc = nbeg + c * 32;
   // All of the chunk's global operand loads are in flight at once (one DRAM
   // latency per chunk instead of one per row pair). bf16 operands (4 vectors)
@@ -288,7 +291,15 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
         for (int i = 0; i < E; ++i) v[i] += b[i];
       const long long rel = cp - reinterpret_cast<OutT*>(p.c);
       if (valid >= E) {
-        if constexpr (DG) {
+        if constexpr (RD) {
+          // C stored as is; its bf16 values dotted with AUX over this lane's columns
+          float x[E];
+          unpack_vec<OutT, E>(pa[it], x);
+          float dsum = 0.f;
+#pragma unroll
+          for (int i = 0; i < E; ++i) dsum = fmaf(to_f(from_f<OutT>(v[i])), x[i], dsum);
+          racc[it] += dsum;
+        } else if constexpr (DG) {
           float x[E];
           unpack_vec<OutT, E>(pa[it], x);
 #pragma unroll
@@ -366,9 +377,33 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
   const int rows_left = p.M - m_base;  // rows of this stripe inside the problem
   const long long step = static_cast<long long>(G::RPI) * p.ldc;
   const long long lane_base = (row0 + lr) * p.ldc + col0 + lc * G::E;  // element offset of (row lr, column 0)
+  float racc[G::IT];
+#pragma unroll
+  for (int it = 0; it < G::IT; ++it) racc[it] = 0.f;
 #pragma unroll 1
-  for (int c = 0; c < NCH; ++c)
-    epi_chunk<OutT, EPI, ACC>(p, c, nbeg, row0, col0, lr, lc, rows_left, step, lane_base, taddr, stg, lane);
+  for (int c = 0; c < NCH; ++c) {
+    epi_chunk<OutT, EPI, ACC>(p, c, nbeg, row0, col0, lr, lc, rows_left, step, lane_base, taddr, stg, lane, racc);
+    if constexpr (EPI == OASES_EPI_ROWDOT) {
+      const int cend = static_cast<int>(col0) + nbeg + (c + 1) * 32;  // column after this chunk
+      if (cend % p.rd_group == 0 && cend <= p.N) {
+        // the group (head) ends here: reduce over the LPR lanes of each row, one lane writes
+        const int g = (cend - 1) / p.rd_group;
+#pragma unroll
+        for (int it = 0; it < G::IT; ++it) {
+          float t = racc[it];
+#pragma unroll
+          for (int o = 1; o < G::LPR; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+          const int row = it * G::RPI + lr;
+          if (lc == 0 && row < rows_left) {
+            const long long m = row0 + row;
+            const long long smp = m / p.rd_seq, i = m - smp * p.rd_seq;
+            p.rowdot[(smp * p.rd_heads + g) * p.rd_seq + i] = t;
+          }
+          racc[it] = 0.f;
+        }
+      }
+    }
+  }
 }
 
 // Calls BODY(OutT, EPI, ACC) for the runtime mode of p (compile-time specialised).
@@ -382,6 +417,7 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
       case 6: BODY(__nv_bfloat16, 3, false); break;                                       \
       case 8: BODY(__nv_bfloat16, 4, false); break;                                       \
       case 10: BODY(__nv_bfloat16, 5, false); break;                                      \
+      case 12: BODY(__nv_bfloat16, 6, false); break;                                      \
       case 16: BODY(float, 0, false); break;                                              \
       case 17: BODY(float, 0, true); break;                                               \
       case 18: BODY(float, 1, false); break;                                              \
@@ -919,7 +955,14 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
     *err = "gemm_tc: empty problem";
     return false;
   }
-  if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_MUL) {
+  if (d.epilogue == OASES_EPI_ROWDOT &&
+      (!d.rowdot || !d.aux || d.c_dtype == OASES_F32 || d.rowdot_group <= 0 || d.rowdot_group % 32 ||
+       d.N % d.rowdot_group || d.rowdot_seq <= 0 || d.M % d.rowdot_seq || d.batch != 1 ||
+       d.N != static_cast<int64_t>(d.rowdot_group) * d.rowdot_heads)) {
+    *err = "gemm_tc: ROWDOT needs bf16 C, AUX, rowdot, unbatched, N = heads*group (group % 32 == 0), M % seq == 0";
+    return false;
+  }
+  if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_ROWDOT) {
     *err = "gemm_tc: unknown epilogue";
     return false;
   }
@@ -950,6 +993,12 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
     return false;
   }
   const bool pair = use_pairs() && d.causal == OASES_CAUSAL_NONE && d.M > BM && d.N > 128;
+  if (d.epilogue == OASES_EPI_ROWDOT && ((pair ? PAIR_BN / 2 : BN / 2) % d.rowdot_group)) {
+    // each epilogue warp reduces its own column stripe: a group must not straddle two
+    *err = "gemm_tc: ROWDOT groups must tile the epilogue stripe (" + std::to_string(pair ? PAIR_BN / 2 : BN / 2) +
+           " columns)";
+    return false;
+  }
   if (!make_map(&out.ma, d.a, 64, d.a.mn_major ? 64 : BM, err)) return false;
   if (!make_map(&out.mb, d.b, 64, d.b.mn_major ? 64 : (pair ? 128 : BN), err)) return false;
   TcParams& p = out.p;
@@ -974,6 +1023,10 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
   p.c = d.c;
   p.c2 = d.c2;
   p.aux = d.aux;
+  p.rowdot = d.rowdot;
+  p.rd_group = d.rowdot_group;
+  p.rd_seq = d.rowdot_seq;
+  p.rd_heads = d.rowdot_heads;
   p.bias = d.bias;
   p.ldc = d.ldc;
   p.c_f32 = d.c_dtype == OASES_F32;

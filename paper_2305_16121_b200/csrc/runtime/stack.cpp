@@ -678,7 +678,8 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   char* dqkv = static_cast<char*>(w.dcol);
   if (fused_attn_) {
     oases_attn_desc a = attn_desc(w, block, sb, ws);
-    a.mask_mode = 2;  // the forward pass stored the keep bits
+    a.mask_mode = 2;                // the forward pass stored the keep bits
+    a.dsum_ready = rowdot_ ? 1 : 0;  // the proj dgrad's ROWDOT epilogue wrote D
     const GemmStatus st = oases::attention_bwd(a, ctx_.compute);
     if (!st.ok) {
       if (st.cuda) throw CudaError(st.err);
@@ -928,6 +929,17 @@ void Stack::backward(int wi, int block, int sb) {
   d.alpha = 1.f;
   if (att) {
     d.c = w.du; d.ldc = nrow;
+    // ROWDOT: each 128-column epilogue stripe of the CTA-pair kernel holds whole heads
+    rowdot_ = fused_attn_ && nrow_attn_ > 128 && Ts > 128 && 128 % dh_ == 0;
+    if (rowdot_) {
+      // D = rowsum(dO o O) per head for the attention backward, from the dgrad epilogue
+      d.epilogue = OASES_EPI_ROWDOT;
+      d.aux = ws.act;
+      d.rowdot = static_cast<float*>(w.attn_ws);
+      d.rowdot_group = dh_;
+      d.rowdot_seq = static_cast<int>(cfg_.s);
+      d.rowdot_heads = hl_;
+    }
     gemm2(dw, d);
     attention_bwd(w, block, sb, ws);
   } else {

@@ -176,7 +176,8 @@ class Stack {
   std::vector<Worker> workers_;
   int nblocks_ = 0;
   bool fused_attn_ = false;
-  bool fuse_bdr_ln_ = true;  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
+  bool fuse_bdr_ln_ = true;
+  bool rowdot_ = false;  // attention D = rowsum(dO o O) comes from the proj dgrad epilogue  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;

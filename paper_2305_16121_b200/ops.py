@@ -47,7 +47,8 @@ def operand(t: torch.Tensor, mn_major: bool = False, row_off=(0, 0), col_off=(0,
 
 def gemm_desc(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_off=(0, 0), c_col_off=(0, 0),
               c_col_base=0, epilogue=capi.EPI_NONE, causal=capi.CAUSAL_NONE, alpha=1.0, accumulate=False,
-              bias=None, aux=None, c2=None, max_ctas=0, dtype=capi.BF16):
+              bias=None, aux=None, c2=None, max_ctas=0, dtype=capi.BF16, rowdot=None, rowdot_group=0,
+              rowdot_seq=0, rowdot_heads=0):
     d = capi.GemmDesc()
     d.dtype = dtype
     d.c_dtype = _dtype(c)
@@ -67,6 +68,8 @@ def gemm_desc(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_o
     d.aux = None if aux is None else aux.data_ptr() + c_col_base * esz
     d.c2 = None if c2 is None else c2.data_ptr() + c_col_base * esz
     d.max_ctas = max_ctas
+    d.rowdot = None if rowdot is None else rowdot.data_ptr()
+    d.rowdot_group, d.rowdot_seq, d.rowdot_heads = rowdot_group, rowdot_seq, rowdot_heads
     return d
 
 

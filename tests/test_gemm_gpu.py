@@ -223,3 +223,25 @@ def test_gemm_gelu_grad_and_mul_epilogues(cuda, dt):
     ops.gemm(M, N, K, ops.operand(G), ops.operand(W), out, epilogue=capi.EPI_MUL, aux=dgl, dtype=kdt)
     torch.cuda.synchronize()
     assert relerr(out, (G.double() @ W.double().t()) * dgl.double()) < tol
+
+
+@pytest.mark.parametrize("dh,hl,seq,n", [(128, 4, 256, 3), (64, 6, 128, 2), (128, 16, 1024, 4)])
+def test_gemm_rowdot_epilogue(cuda, dh, hl, seq, n):
+    """EPI_ROWDOT: C = A B^T stored as usual, and per (sample, head, row)
+    D = sum over the head's columns of bf16(C) * AUX -- the attention backward's
+    rowsum(dO o O) produced by the proj dgrad GEMM."""
+    torch.manual_seed(12)
+    M, N, K = n * seq, hl * dh, 512
+    A = torch.randn(M, K, device=cuda).bfloat16()
+    B = (torch.randn(N, K, device=cuda) / math.sqrt(K)).bfloat16()
+    O = torch.randn(M, N, device=cuda).bfloat16()
+    C = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    D = torch.full((n * hl * seq,), float("nan"), device=cuda)
+    ops.gemm(M, N, K, ops.operand(A), ops.operand(B), C, epilogue=capi.EPI_ROWDOT, aux=O, rowdot=D,
+             rowdot_group=dh, rowdot_seq=seq, rowdot_heads=hl)
+    torch.cuda.synchronize()
+    ref_c = A.double() @ B.double().t()
+    assert relerr(C, ref_c) < 1e-2
+    ref_d = (C.double() * O.double()).view(n, seq, hl, dh).sum(-1).permute(0, 2, 1).reshape(-1)
+    assert torch.isfinite(D).all()
+    assert relerr(D, ref_d) < 1e-4
