@@ -98,6 +98,26 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Packed f32x2 arithmetic (FFMA2 / FADD2: two lanes of work per instruction).
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r, x, y, z;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(z) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(y), "l"(z));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r, x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
 // 16-byte chunk `ch` (8 bf16 columns, ch in 0..15 over 128 columns) of row r of a
 // [128 x 128] bf16 tile stored as two SW128 K-major [128 x 64] halves 16 KB apart.
 __device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int r, int ch) {
@@ -491,21 +511,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const float mx = cand > m + 8.f ? cand : m;
         const float alpha = ex2(m - mx);
         const float nmx = -mx;
-        float sp[4] = {0.f, 0.f, 0.f, 0.f};
+        float2 sp[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         uint32_t pk[16];
+        const float2 sl2x2 = make_float2(p.sl2, p.sl2), nmx2 = make_float2(nmx, nmx);
 #pragma unroll
         for (int kk = 0; kk < 32; kk += 2) {
-#ifdef OASES_EXP_NOEXP
-          const float a = fmaf(__uint_as_float(u[kk]), p.sl2, nmx);
-          const float b = fmaf(__uint_as_float(u[kk + 1]), p.sl2, nmx);
-#else
-          const float a = ex2(fmaf(__uint_as_float(u[kk]), p.sl2, nmx));
-          const float b = ex2(fmaf(__uint_as_float(u[kk + 1]), p.sl2, nmx));
-#endif
-          sp[(kk >> 1) & 3] += a + b;
-          pk[kk >> 1] = pack_bf16(a, b);
+          // pairs on the packed pipe: one FFMA2 for the exponents, one FADD2 for the sums
+          const float2 e = fma2(make_float2(__uint_as_float(u[kk]), __uint_as_float(u[kk + 1])), sl2x2, nmx2);
+          const float2 ab = make_float2(ex2(e.x), ex2(e.y));
+          sp[(kk >> 1) & 1] = add2(sp[(kk >> 1) & 1], ab);
+          pk[kk >> 1] = pack_bf16(ab.x, ab.y);
         }
-        const float sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+        const float sum = (sp[0].x + sp[1].x) + (sp[0].y + sp[1].y);
         l = l * alpha + sum;
         m = mx;
         if (p.thr) {
