@@ -848,10 +848,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(s_free);
       uint32_t pp[32];  // P, bf16x2
+      const float2 sl2x2 = make_float2(p.sl2, p.sl2), nlse2 = make_float2(nlse, nlse);
 #pragma unroll
       for (int k = 0; k < 64; k += 2) {
-        float a = ex2(fmaf(__uint_as_float(u[k >> 5][k & 31]), p.sl2, nlse));
-        float b = ex2(fmaf(__uint_as_float(u[k >> 5][(k & 31) + 1]), p.sl2, nlse));
+        const float2 e = fma2(make_float2(__uint_as_float(u[k >> 5][k & 31]), __uint_as_float(u[k >> 5][(k & 31) + 1])),
+                              sl2x2, nlse2);
+        float a = ex2(e.x), b = ex2(e.y);
         if (k > lim) a = 0.f;
         if (k + 1 > lim) b = 0.f;
         pp[k >> 1] = pack_bf16(a, b);
@@ -903,13 +905,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dp_free);
       const float c1 = p.scale * p.ks, c2 = -p.scale * dsum;
+      const float2 c1x2 = make_float2(c1, c1), c2x2 = make_float2(c2, c2), z2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const float2 pr = unpack_bf16(pp[k]);
         const float2 kp = unpack_bf16(pk[k]);
-        const float d0 = fmaf(kp.x * c1, __uint_as_float(v[k >> 4][(2 * k) & 31]), pr.x * c2);
-        const float d1 = fmaf(kp.y * c1, __uint_as_float(v[k >> 4][(2 * k + 1) & 31]), pr.y * c2);
-        pk[k] = pack_bf16(d0, d1);
+        // dS = (kp c1) dP + pr c2, two columns per packed instruction
+        const float2 dp = make_float2(__uint_as_float(v[k >> 4][(2 * k) & 31]), __uint_as_float(v[k >> 4][(2 * k + 1) & 31]));
+        const float2 d = fma2(fma2(kp, c1x2, z2), dp, fma2(pr, c2x2, z2));
+        pk[k] = pack_bf16(d.x, d.y);
       }
       mbar_wait(buf_free1, it & 1);
       if (warp == 2 && lane == 0) ATRACE(6, it);
