@@ -171,6 +171,7 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
   for (int w = 0; w < W; ++w) workers_[static_cast<size_t>(w)].rank = W > 1 ? w : ctx.rank;
   alloc_all();
   touched_.assign(static_cast<size_t>(W), std::vector<std::array<bool, OASES_P_COUNT>>(static_cast<size_t>(nblocks_)));
+  bwd_seen_.assign(static_cast<size_t>(W), std::vector<bool>(static_cast<size_t>(nblocks_), false));
   loss_touched_.assign(static_cast<size_t>(W), false);
 }
 
@@ -249,11 +250,18 @@ void Stack::alloc_all() {
       }
     }
     w.ws.resize(static_cast<size_t>(nslots));
-    for (auto& per_sb : w.ws) {
-      for (Workspace& ws : per_sb) {
-        ws.ln = cfg_.ln ? arena_.alloc(static_cast<size_t>(Ts * h) * es) : nullptr;
+    for (int slot = 0; slot < nslots; ++slot) {
+      // the weight-gradient GEMMs read the two sub-batches' LN output and
+      // activation as one [2 T_sub, .] operand: both halves of a slot are one
+      // allocation (slot parity == block parity, so its row width is fixed)
+      const int64_t slot_nrow = is_attention(slot) ? nrow_attn_ : nrow_ffn_;
+      void* ln_full = cfg_.ln ? arena_.alloc(static_cast<size_t>(2 * Ts * h) * es) : nullptr;
+      void* act_full = arena_.alloc(static_cast<size_t>(2 * Ts * std::max<int64_t>(slot_nrow, 1)) * es);
+      for (int sb = 0; sb < 2; ++sb) {
+        Workspace& ws = w.ws[static_cast<size_t>(slot)][static_cast<size_t>(sb)];
+        ws.ln = ln_full ? half(ln_full, sb, h) : nullptr;
         ws.col = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
-        ws.act = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
+        ws.act = half(act_full, sb, slot_nrow);
         if (prob && fused_attn_) {
           ws.lse = static_cast<float*>(arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float)));
         } else if (prob) {
@@ -262,9 +270,9 @@ void Stack::alloc_all() {
         }
       }
     }
-    w.gar = arena_.alloc(static_cast<size_t>(Ts * h) * es);
+    w.gar = arena_.alloc(static_cast<size_t>(2 * Ts * h) * es);  // [sb][T_sub, h]
     w.du = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
-    w.dcol = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
+    w.dcol = arena_.alloc(static_cast<size_t>(2 * Ts * ncol_max) * es);  // [sb][T_sub, ncol] of the block
     if (prob) w.dp = arena_.alloc(static_cast<size_t>(prob) * es);
     if (prob && fused_attn_) w.attn_ws = arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float));
     if (prob && fused_attn_ && cfg_.p_attn > 0.f) {
@@ -335,6 +343,7 @@ bool Stack::touch(const Worker& w, int block, int p) {
 void Stack::begin_step() {
   for (auto& per_worker : touched_)
     for (auto& a : per_worker) a.fill(false);
+  for (auto& per_worker : bwd_seen_) std::fill(per_worker.begin(), per_worker.end(), false);
   std::fill(loss_touched_.begin(), loss_touched_.end(), false);
 }
 
@@ -608,7 +617,7 @@ oases_attn_desc Stack::attn_desc(Worker& w, int block, int sb, const Workspace& 
   a.lse = ws.lse;
   a.dout = w.du;
   a.ld_dout = nrow_attn_;
-  a.dqkv = w.dcol;
+  a.dqkv = half(w.dcol, sb, ncol_attn_);
   a.ld_dqkv = ncol_attn_;
   a.ds = w.dp;
   a.workspace = w.attn_ws;
@@ -675,7 +684,7 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   const int64_t hd = static_cast<int64_t>(hl_) * dh_;
   const size_t es = esize();
   const char* qkv = static_cast<const char*>(ws.col);
-  char* dqkv = static_cast<char*>(w.dcol);
+  char* dqkv = static_cast<char*>(half(w.dcol, sb, ncol_attn_));
   if (fused_attn_) {
     oases_attn_desc a = attn_desc(w, block, sb, ws);
     a.mask_mode = 2;                // the forward pass stored the keep bits
@@ -849,6 +858,12 @@ void Stack::backward(int wi, int block, int sb) {
   const int hi = static_cast<int>(h);
   void* g = half(w.grad, sb, h);
   const size_t usb = static_cast<size_t>(sb);
+  void* gar_sb = half(w.gar, sb, h);
+  // The weight gradients of a block are computed once per step, by its second
+  // backward call (the other sub-batch's), over both sub-batches at once:
+  // K = 2 T_sub, no f32 read-modify-write of dW between the sub-batches.
+  const bool wgrad_now = bwd_seen_[static_cast<size_t>(wi)][static_cast<size_t>(block)];
+  bwd_seen_[static_cast<size_t>(wi)][static_cast<size_t>(block)] = true;
   // 1. gradient arriving at x_{b+1}; with LayerNorm the same pass also writes
   //    g_ar = dropout'(g) (step 2) when the row-group kernel covers the width
   bool gar_done = false;
@@ -870,7 +885,7 @@ void Stack::backward(int wi, int block, int sb) {
       const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
       const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && ln_bwd_dropout_supported(dtype(), Ts, hi);
       check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
-                                    nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute, fuse ? w.gar : nullptr,
+                                    nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute, fuse ? gar_sb : nullptr,
                                     cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0)),
                  "layernorm_bwd");
       gar_done = fuse;
@@ -892,12 +907,12 @@ void Stack::backward(int wi, int block, int sb) {
   const void* gar = g;
   if (cfg_.p_hidden > 0.f) {
     if (!gar_done) {
-      check_cuda(col_pass(dtype(), g, w.gar, nullptr, 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed,
+      check_cuda(col_pass(dtype(), g, gar_sb, nullptr, 0, w.col_ws, Ts, hi, cfg_.p_hidden, cfg_.seed,
                           drop_offset(block, sb, 0), ctx_.compute),
                  "dropout bwd");
       ++launches_;
     }
-    gar = w.gar;
+    gar = gar_sb;
   }
   if (cfg_.bias) {
     // row-bias gradient = column sums of g_ar: side stream, under the row GEMMs
@@ -911,15 +926,20 @@ void Stack::backward(int wi, int block, int sb) {
   Workspace& ws = ws_for(w, block, sb);
   const bool att = is_attention(block);
   const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
-  // 3. row-parallel GEMM: dW_row += g_ar^T act ; d(act) = g_ar W_row
+  // 3. row-parallel GEMM: dW_row (+)= g_ar^T act over both sub-batches ; d(act) = g_ar W_row
+  // (g_ar is the sub-batch half of w.gar unless the dropout is off and g_ar == g,
+  // a half of w.grad: both hold the two sub-batches contiguously)
+  const void* gar_base = gar == gar_sb ? w.gar : w.grad;
   oases_gemm_desc dw{};
-  dw.c_dtype = OASES_F32;
-  dw.M = h; dw.N = nrow; dw.K = Ts;
-  dw.batch = 1; dw.batch_inner = 1;
-  dw.a = operand(gar, Ts, h, h, true);
-  dw.b = operand(ws.act, Ts, nrow, nrow, true);
-  dw.c = bp.g[OASES_P_W_ROW]; dw.ldc = nrow;
-  dw.alpha = 1.f; dw.accumulate = touch(w, block, OASES_P_W_ROW) ? 1 : 0;
+  if (wgrad_now) {
+    dw.c_dtype = OASES_F32;
+    dw.M = h; dw.N = nrow; dw.K = 2 * Ts;
+    dw.batch = 1; dw.batch_inner = 1;
+    dw.a = operand(gar_base, 2 * Ts, h, h, true);
+    dw.b = operand(ws_for(w, block, 0).act, 2 * Ts, nrow, nrow, true);
+    dw.c = bp.g[OASES_P_W_ROW]; dw.ldc = nrow;
+    dw.alpha = 1.f; dw.accumulate = touch(w, block, OASES_P_W_ROW) ? 1 : 0;
+  }
   oases_gemm_desc d{};
   d.c_dtype = dtype();
   d.M = Ts; d.N = nrow; d.K = h;
@@ -940,45 +960,51 @@ void Stack::backward(int wi, int block, int sb) {
       d.rowdot_seq = static_cast<int>(cfg_.s);
       d.rowdot_heads = hl_;
     }
-    gemm2(dw, d);
+    if (wgrad_now) gemm2(dw, d);
+    else gemm(d);
     attention_bwd(w, block, sb, ws);
   } else {
     // dpre = (g_ar W_row) o gelu'(pre)   (hadamard + gelu_grad, numerics.cpp:203-204; gelu'(pre)
     // was stored by the FC1 epilogue that produced the activation)
-    d.c = w.dcol; d.ldc = ncol;
+    d.c = half(w.dcol, sb, ncol); d.ldc = ncol;
     d.epilogue = OASES_EPI_MUL;
     d.aux = ws.col;
-    gemm2(dw, d);
+    if (wgrad_now) gemm2(dw, d);
+    else gemm(d);
   }
   // 4. column bias
   if (cfg_.bias) {
     // the column-bias gradient only feeds the step's result: side stream, under the column GEMMs
     const bool acc = touch(w, block, OASES_P_B_COL);
     fork_side();
-    check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, Ts,
+    check_cuda(col_pass(dtype(), half(w.dcol, sb, ncol), nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, Ts,
                         static_cast<int>(ncol), 0.f, 0, 0, ctx_.side),
                "colsum");
     launches_ += 2;
   }
-  // 5. column-parallel GEMM: dW_col += dcol^T ln ; d_ln partial = dcol W_col -> AR_b (backward f)
-  const void* ln = cfg_.ln ? ws.ln : w.xs[static_cast<size_t>(block)][usb];
+  // 5. column-parallel GEMM: dW_col (+)= dcol^T ln over both sub-batches ; d_ln partial = dcol W_col
+  //    -> AR_b (backward f)
+  const void* ln_base = cfg_.ln ? ws_for(w, block, 0).ln : w.xs[static_cast<size_t>(block)][0];
   dw = oases_gemm_desc{};
-  dw.c_dtype = OASES_F32;
-  dw.M = ncol; dw.N = h; dw.K = Ts;
-  dw.batch = 1; dw.batch_inner = 1;
-  dw.a = operand(w.dcol, Ts, ncol, ncol, true);
-  dw.b = operand(ln, Ts, h, h, true);
-  dw.c = bp.g[OASES_P_W_COL]; dw.ldc = h;
-  dw.alpha = 1.f; dw.accumulate = touch(w, block, OASES_P_W_COL) ? 1 : 0;
+  if (wgrad_now) {
+    dw.c_dtype = OASES_F32;
+    dw.M = ncol; dw.N = h; dw.K = 2 * Ts;
+    dw.batch = 1; dw.batch_inner = 1;
+    dw.a = operand(w.dcol, 2 * Ts, ncol, ncol, true);
+    dw.b = operand(ln_base, 2 * Ts, h, h, true);
+    dw.c = bp.g[OASES_P_W_COL]; dw.ldc = h;
+    dw.alpha = 1.f; dw.accumulate = touch(w, block, OASES_P_W_COL) ? 1 : 0;
+  }
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = Ts; d.N = h; d.K = ncol;
   d.batch = 1; d.batch_inner = 1;
-  d.a = operand(w.dcol, Ts, ncol, ncol, false);
+  d.a = operand(half(w.dcol, sb, ncol), Ts, ncol, ncol, false);
   d.b = operand(bp.p[OASES_P_W_COL], ncol, h, h, true);
   d.c = w.bwd_ar[block % 2][usb]; d.ldc = h;
   d.alpha = 1.f;
-  gemm2(dw, d);
+  if (wgrad_now) gemm2(dw, d);
+  else gemm(d);
   join_side();
 }
 

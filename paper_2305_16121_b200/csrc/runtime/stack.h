@@ -181,6 +181,7 @@ class Stack {
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;
+  std::vector<std::vector<bool>> bwd_seen_;  // [worker][block] first backward call of the step done
   std::vector<bool> x_stored_;  // [block] x_b readable after a step (bind_storage)
   int64_t launches_ = 0;
   bool timing_ = false;
