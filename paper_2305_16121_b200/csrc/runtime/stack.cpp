@@ -287,11 +287,12 @@ void Stack::alloc_all() {
           w.mask_bits[static_cast<size_t>(b / 2)][static_cast<size_t>(sb)] = static_cast<uint32_t*>(arena_.alloc(mbytes));
     }
     w.y = arena_.alloc(static_cast<size_t>(Ts * h) * es);
-    w.ln_ws = arena_.alloc(layernorm_bwd_workspace(Ts, static_cast<int>(h)));
-    w.col_ws = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
-                                     colsum_workspace(Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
-    w.col_ws2 = arena_.alloc(std::max(colsum_workspace(Ts, static_cast<int>(h)),
-                                     colsum_workspace(Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
+    // row statistics of both sub-batches (the parameter pass runs once over 2 T_sub rows)
+    w.ln_ws = arena_.alloc(layernorm_bwd_workspace(2 * Ts, static_cast<int>(h)));
+    w.col_ws = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
+                                     colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
+    w.col_ws2 = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
+                                      colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
     w.loss = static_cast<double*>(arena_.alloc(sizeof(double)));
     w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
   }
@@ -881,20 +882,26 @@ void Stack::backward(int wi, int block, int sb) {
     const BlockParams& nxt = w.params[static_cast<size_t>(block + 1)];
     const void* dln = w.bwd_ar[(block + 1) % 2][usb];
     if (cfg_.ln) {
-      const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
       const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
       const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && ln_bwd_dropout_supported(dtype(), Ts, hi);
+      // this sub-batch's row statistics land in rows [sb T_sub, (sb+1) T_sub) of the workspace
+      void* stats_sb = static_cast<char*>(w.ln_ws) + static_cast<size_t>(sb) * Ts * 2 * sizeof(float);
       check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
-                                    nullptr, 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.compute, fuse ? gar_sb : nullptr,
+                                    nullptr, 0, stats_sb, Ts, hi, cfg_.eps, ctx_.compute, fuse ? gar_sb : nullptr,
                                     cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0)),
                  "layernorm_bwd");
       gar_done = fuse;
-      // dgamma/dbeta: side stream, under this op's GEMMs (joined at the op's end)
-      fork_side();
-      check_cuda(layernorm_bwd_part(2, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, nullptr, 0, nxt.g[OASES_P_LN_GAMMA],
-                                    nxt.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, Ts, hi, cfg_.eps, ctx_.side),
-                 "layernorm_bwd params");
-      launches_ += 3;
+      ++launches_;
+      if (wgrad_now) {
+        // dgamma/dbeta over both sub-batches: side stream, under this op's GEMMs (joined at the op's end)
+        const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
+        fork_side();
+        check_cuda(layernorm_bwd_part(2, dtype(), w.xs[static_cast<size_t>(block + 1)][0], nxt.p[OASES_P_LN_GAMMA],
+                                      w.bwd_ar[(block + 1) % 2][0], nullptr, 0, nxt.g[OASES_P_LN_GAMMA],
+                                      nxt.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, 2 * Ts, hi, cfg_.eps, ctx_.side),
+                   "layernorm_bwd params");
+        launches_ += 2;
+      }
     } else {
       check_cuda(bias_dropout_residual_fwd(dtype(), dln, nullptr, cfg_.residual ? g : nullptr, g, Ts, hi, 0.f, 0, 0,
                                            ctx_.compute),
@@ -914,12 +921,12 @@ void Stack::backward(int wi, int block, int sb) {
     }
     gar = gar_sb;
   }
-  if (cfg_.bias) {
-    // row-bias gradient = column sums of g_ar: side stream, under the row GEMMs
+  if (cfg_.bias && wgrad_now) {
+    // row-bias gradient = column sums of g_ar over both sub-batches: side stream, under the row GEMMs
     const bool acc = touch(w, block, OASES_P_B_ROW);
     fork_side();
-    check_cuda(col_pass(dtype(), gar, nullptr, bp.g[OASES_P_B_ROW], acc ? 1 : 0, w.col_ws, Ts, hi, 0.f, 0, 0,
-                        ctx_.side),
+    check_cuda(col_pass(dtype(), gar == gar_sb ? w.gar : w.grad, nullptr, bp.g[OASES_P_B_ROW], acc ? 1 : 0, w.col_ws,
+                        2 * Ts, hi, 0.f, 0, 0, ctx_.side),
                "row bias grad");
     launches_ += 2;
   }
@@ -973,11 +980,12 @@ void Stack::backward(int wi, int block, int sb) {
     else gemm(d);
   }
   // 4. column bias
-  if (cfg_.bias) {
-    // the column-bias gradient only feeds the step's result: side stream, under the column GEMMs
+  if (cfg_.bias && wgrad_now) {
+    // the column-bias gradient (both sub-batches) only feeds the step's result: side stream, under
+    // the column GEMMs
     const bool acc = touch(w, block, OASES_P_B_COL);
     fork_side();
-    check_cuda(col_pass(dtype(), half(w.dcol, sb, ncol), nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, Ts,
+    check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, 2 * Ts,
                         static_cast<int>(ncol), 0.f, 0, 0, ctx_.side),
                "colsum");
     launches_ += 2;
