@@ -5,28 +5,36 @@
 // probabilities) is computed here without materialising the [seq, seq]
 // probability matrix in HBM:
 //
-//   attn_fwd_kernel   one CTA per (sample x local head, 128-query tile).
-//                     S_j = Q K_j^T into TMEM (double-buffered), online
-//                     softmax in registers (one query row per thread), the
-//                     dropout keep-mask of DESIGN.md "Dropout keys" applied to
-//                     the unnormalised probabilities, P_j -> swizzled smem,
-//                     O += P_j V_j accumulated in TMEM (rescaled in place when
-//                     the running max grows). Writes ctx (bf16) and the row
-//                     log-sum-exp (log2 domain, f32) for the backward.
-//   attn_dsum_kernel  D_i = sum_d dO_i,d * O_i,d  (= sum_j P_ij dP_ij).
+//   attn_fwd_kernel   persistent (one CTA per SM, zigzag order over (sample x
+//                     local head, 128-query tile) items). S_j = Q K_j^T into
+//                     three TMEM buffers, issued two KV tiles ahead; online
+//                     softmax in registers (one query row per thread, 16 warps:
+//                     4 per TMEM lane quarter x 32 key columns, row max / sum
+//                     exchanged through smem), the dropout keep-mask of
+//                     DESIGN.md "Dropout keys" applied to the unnormalised
+//                     probabilities; P_j (bf16) written back over S_j in TMEM
+//                     and consumed from there by the TS-form MMA O += P_j V_j
+//                     (O rescaled in place only when the running max grows by
+//                     more than 8). Writes ctx (bf16), the row log-sum-exp
+//                     (log2 domain, f32) and optionally the keep bits.
+//                     Warps: 0 Q/K TMA, 1 MMA issuer + TMEM owner, 2 V TMA,
+//                     3..18 softmax.
+//   attn_dsum_kernel  D_i = sum_d dO_i,d * O_i,d  (= sum_j P_ij dP_ij), when the
+//                     dO-producing GEMM did not emit it (EPI_ROWDOT).
 //   attn_dkdv_kernel  one CTA per (sample x head, 128-key tile), streaming the
 //                     query tiles at or below the diagonal: S = Q K^T and
 //                     dP_drop = dO V^T into TMEM, P = exp2(S - lse), the
 //                     dropped P -> smem -> dV += P_drop^T dO; dS = P o (dP - D)
 //                     -> smem -> dK += dS^T Q. dS is also TMA-stored to HBM so
 //                     dQ = dS K runs as one batched causal tcgen05 GEMM
-//                     (deterministic: no atomics anywhere).
+//                     (deterministic: no atomics anywhere). Warps: 0 TMA,
+//                     1 MMA issuer + TMEM owner, 2..9 row math (warp w owns
+//                     TMEM lanes 32*(w%4) .. +31 and half (w-2)/4 of the 128
+//                     key columns).
 //
-// Warp roles (320 threads, 1 CTA per SM): warp 0 TMA producer, warp 1 MMA
-// issuer + TMEM owner, warps 2..9 the row-wise math: warp w owns TMEM lanes
-// 32*(w%4) .. +31 (query/key rows of the 128-row tile) and half (w-2)/4 of the
-// 128 key columns; the two warps of a row exchange their partial row maxima
-// through smem (forward only -- the backward needs no row reductions).
+// Dropout keep bits: Philox4x32-10 with the seed's round keys in the kernel
+// parameters; the forward pass can store one bit per causal-band element
+// (mask_mode 1) which the recompute forward and the backward read (mode 2).
 #include <cmath>
 #include <string>
 
@@ -315,16 +323,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int off = kq ? C::K_OFF : C::V_OFF, col = kq ? p.k_col : p.v_col;
           mbar_wait(empty, ph);
           ATRACE(kq ? 6 : 7, g);
-#ifdef OASES_EXP_NOLOAD
-          mbar_arrive(full);
-          (void)off; (void)col;
-#else
           mbar_arrive_expect_tx(full, C::TILE_BYTES);
 #pragma unroll
           for (int gg = 0; gg < DH / 64; ++gg)
             tma_load_2d(smem + off + st * C::TILE_BYTES + gg * 16384, &tqkv, full, col + jl * DH + gg * 64,
                         row0 + j * kTile);
-#endif
         }
       }
     }
@@ -348,14 +351,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-#ifndef OASES_EXP_NOMMA
           umma_bf16(tmem + st * kTile, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
                     id_s, kk > 0 ? 1u : 0u);
-#ifdef OASES_EXP_DOUBLEMMA
-          umma_bf16(tmem + st * kTile, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
-                    id_s, 1u);
-#endif
-#endif
         }
         umma_commit(&s_full[st]);
         umma_commit(&k_empty[kv]);
@@ -374,9 +371,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < kTile / 16; ++kk) {
           const uint64_t bd = umma_desc_sw128(vb + kk * 2048, 16384, 1024);
-#ifndef OASES_EXP_NOMMA
           umma_bf16_ts(tmem + C::O_COL + ob * DH, tmem + st * kTile + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
-#endif
         }
         umma_commit(&v_empty[kv]);
         umma_commit(&pv_done[st]);
@@ -458,22 +453,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int st = g % C::NS;
         const uint32_t bits_j = mword;
         if (cached && j < qt) mword = p.mask_bits[mask_word(p, z, qt, j + 1, rr, part)];
-#ifdef OASES_EXP_ONESPIN
-        if (part == 0) mbar_wait(&s_full[st], (g / C::NS) & 1);
-        named_bar_sync(1 + q, 128);
-#else
         mbar_wait(&s_full[st], (g / C::NS) & 1);
-#endif
         if (warp == 3 && lane == 0) ATRACE(4, g);
         tc_fence_after();
-#ifdef OASES_EXP_NOSOFT
-        {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[st]);
-          continue;
-        }
-#endif
         uint32_t u[32];
         tmem_ld32(tl + st * kTile + c0, u);
         tmem_wait_ld();
@@ -493,16 +475,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int kk = 4; kk < 32; ++kk) mp[kk & 3] = fmaxf(mp[kk & 3], __uint_as_float(u[kk]));
           mpart = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
         }
-#ifdef OASES_EXP_NOBAR
-        const float mloc = mpart;
-#else
         tc_fence_before();           // this warp's S loads precede the barrier (P overwrites S below)
         named_bar_sync(1 + q, 128);  // the quarter's previous partials are consumed
         red[part * kTile + rr] = mpart;
         named_bar_sync(1 + q, 128);
         tc_fence_after();
         const float mloc = fmaxf(fmaxf(red[rr], red[kTile + rr]), fmaxf(red[2 * kTile + rr], red[3 * kTile + rr]));
-#endif
         // Conditional rescaling: keep the running max unless the row max grew by
         // more than 8 (log2 units). P = exp2(s - m) then stays <= 256 (exact in
         // bf16's range) and O, l are rescaled only when it pays; the result is
