@@ -12,10 +12,12 @@ namespace oases {
 // (as bias_dropout_residual_fwd), y = LN(xout) (bit-identical to layernorm_fwd
 // of xout). cudaErrorNotSupported when bdr_layernorm_supported() is false.
 bool bdr_layernorm_supported(long long rows, int cols);
+// keep_bits (optional): stores the dropout keep decisions, 1 bit per element
+// (bit e % 16 of word e / 16), for the backward's dropout gradient.
 cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
                                                 void* xout, const void* gamma, const void* beta, void* y,
                                                 long long rows, int cols, float eps, float p, uint64_t seed,
-                                                uint64_t offset, cudaStream_t st);
+                                                uint64_t offset, cudaStream_t st, uint16_t* keep_bits = nullptr);
 cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, long long rows,
                           int cols, float eps, cudaStream_t st);
 size_t layernorm_bwd_workspace(long long rows, int cols);
@@ -30,7 +32,8 @@ bool ln_bwd_dropout_supported(int dtype, long long rows, int cols);
 cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,
                                int acc_dx, float* dgamma, float* dbeta, int acc_params, void* workspace,
                                long long rows, int cols, float eps, cudaStream_t st, void* gout = nullptr,
-                               float drop_p = 0.f, uint64_t seed = 0, uint64_t offset = 0);
+                               float drop_p = 0.f, uint64_t seed = 0, uint64_t offset = 0,
+                               const uint16_t* keep_bits = nullptr);
 // batch = n_samples * heads_local; rows are (sample, local head, query).
 cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,
                         float dropout_p, uint64_t seed, uint64_t offset, int heads_local, int heads_total,

@@ -316,7 +316,8 @@ __global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__
                                                            float2* __restrict__ stats, long long rows, int cols,
                                                            float eps, T* __restrict__ gout = nullptr,
                                                            uint32_t thr = 0, float ks = 1.f, uint64_t seed = 0,
-                                                           uint64_t offset = 0) {
+                                                           uint64_t offset = 0,
+                                                           const uint16_t* __restrict__ keep_bits = nullptr) {
   if constexpr (DROP) {
     pdl_trigger();
     pdl_wait();
@@ -401,7 +402,13 @@ __global__ void __launch_bounds__(256) ln_bwd_block_kernel(const T* __restrict__
 #pragma unroll
           for (int e = 0; e < V; ++e) o[k][t][e] = __bfloat162float(__float2bfloat16_rn(o[k][t][e]));
         }
-        apply_dropout<V>(o[k][t], static_cast<unsigned long long>(off), seed, offset, thr, ks);
+        if (keep_bits) {  // decisions cached by the forward pass
+          const uint32_t bits = keep_bits[off >> 4] >> (off & 15);
+#pragma unroll
+          for (int e = 0; e < V; ++e) o[k][t][e] = (bits >> e) & 1u ? o[k][t][e] * ks : 0.f;
+        } else {
+          apply_dropout<V>(o[k][t], static_cast<unsigned long long>(off), seed, offset, thr, ks);
+        }
         vstore(gout + off, o[k][t]);
       }
     }
@@ -797,7 +804,7 @@ template <typename T>
 cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx, int acc_dx, float* dgamma,
                      float* dbeta, int acc_params, void* workspace, long long rows, int cols, float eps,
                      cudaStream_t st, int which = 3, void* gout = nullptr, float drop_p = 0.f, uint64_t seed = 0,
-                     uint64_t offset = 0) {
+                     uint64_t offset = 0, const uint16_t* keep_bits = nullptr) {
   float2* stats = static_cast<float2*>(workspace);
   float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) +
                                          ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)));
@@ -819,13 +826,13 @@ cudaError_t ln_bwd_t(const void* x, const void* gamma, const void* dy, void* dx,
     const dim3 gr(static_cast<unsigned>(rows));
     if (nvec == 1)
       launch_pdl(ln_bwd_block_kernel<T, 1, 1, true>, gr, dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, rows, cols,
-                 eps, GO, thr, ks, seed, offset);
+                 eps, GO, thr, ks, seed, offset, keep_bits);
     else if (nvec == 2)
       launch_pdl(ln_bwd_block_kernel<T, 2, 1, true>, gr, dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, rows, cols,
-                 eps, GO, thr, ks, seed, offset);
+                 eps, GO, thr, ks, seed, offset, keep_bits);
     else
       launch_pdl(ln_bwd_block_kernel<T, 4, 1, true>, gr, dim3(256), 0, st, X, G, DY, DX, acc_dx, stats, rows, cols,
-                 eps, GO, thr, ks, seed, offset);
+                 eps, GO, thr, ks, seed, offset, keep_bits);
   } else if (nvec && rows < (1LL << 31)) {
     // one row per block (measured faster than 2 for the backward)
     if (nvec == 1)
@@ -875,7 +882,7 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const T* __restrict__ in, 
                                                       const T* __restrict__ gamma, const T* __restrict__ beta,
                                                       T* __restrict__ y, long long rows, int cols, float eps,
                                                       uint32_t thr, float ks, int drop, uint64_t seed,
-                                                      uint64_t offset) {
+                                                      uint64_t offset, uint16_t* __restrict__ keep_bits) {
   pdl_trigger();
   pdl_wait();
   __shared__ float sm[2][8][8];  // [statistic][row of the block][warp of the row]
@@ -901,7 +908,20 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const T* __restrict__ in, 
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[k][e] += b[e];
       }
-      if (drop) apply_dropout16(v[k], static_cast<unsigned long long>(base + c), seed, offset, thr, ks);
+      if (drop) {
+        // one Philox call for the 16 elements; the keep decisions optionally
+        // cached (1 bit each) for the backward's dropout gradient
+        uint32_t u[4];
+        Philox::gen(seed, offset, static_cast<unsigned long long>(base + c) >> 4, u);
+        uint32_t bits = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const bool kp = keep_byte(u, q, thr);
+          v[k][q] = kp ? v[k][q] * ks : 0.f;
+          bits |= static_cast<uint32_t>(kp) << q;
+        }
+        if (keep_bits) keep_bits[(base + c) >> 4] = static_cast<uint16_t>(bits);
+      }
       if (res) {
         float r[16];
         load16(res + base + c, r);
@@ -953,7 +973,7 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const T* __restrict__ in, 
 template <typename T, bool BDR>
 cudaError_t ln_rows_launch(const void* in, const void* bias, const void* res, void* xout, const void* gamma,
                            const void* beta, void* y, long long rows, int cols, float eps, float p, uint64_t seed,
-                           uint64_t offset, cudaStream_t st) {
+                           uint64_t offset, cudaStream_t st, uint16_t* keep_bits = nullptr) {
   const int nv = ln_rows_nv(cols);
   if (!nv || rows >= (1LL << 31) * 4) return cudaErrorNotSupported;
   const int rb = 256 / (cols / (16 * nv));
@@ -969,9 +989,9 @@ cudaError_t ln_rows_launch(const void* in, const void* bias, const void* res, vo
   auto Be = static_cast<const T*>(beta);
   auto Y = static_cast<T*>(y);
   switch (nv) {
-    case 1: launch_pdl(ln_rows_kernel<T, 1, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
-    case 2: launch_pdl(ln_rows_kernel<T, 2, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
-    default: launch_pdl(ln_rows_kernel<T, 4, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset); break;
+    case 1: launch_pdl(ln_rows_kernel<T, 1, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset, keep_bits); break;
+    case 2: launch_pdl(ln_rows_kernel<T, 2, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset, keep_bits); break;
+    default: launch_pdl(ln_rows_kernel<T, 4, BDR>, dim3(grid), dim3(256), 0, st, I, Bi, R, X, G, Be, Y, rows, cols, eps, thr, ks, drop, seed, offset, keep_bits); break;
   }
   return cudaGetLastError();
 }
@@ -1026,23 +1046,24 @@ bool ln_bwd_dropout_supported(int dtype, long long rows, int cols) {
 cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
                                                 void* xout, const void* gamma, const void* beta, void* y,
                                                 long long rows, int cols, float eps, float p, uint64_t seed,
-                                                uint64_t offset, cudaStream_t st) {
+                                                uint64_t offset, cudaStream_t st, uint16_t* keep_bits) {
   if (!bdr_layernorm_supported(rows, cols)) return cudaErrorNotSupported;
   if (dtype == OASES_BF16)
     return ln_rows_launch<__nv_bfloat16, true>(in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset,
-                                               st);
-  return ln_rows_launch<float, true>(in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset, st);
+                                               st, keep_bits);
+  return ln_rows_launch<float, true>(in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset, st,
+                                     keep_bits);
 }
 
 cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* gamma, const void* dy, void* dx,
                                int acc_dx, float* dgamma, float* dbeta, int acc_params, void* workspace,
                                long long rows, int cols, float eps, cudaStream_t st, void* gout, float drop_p,
-                               uint64_t seed, uint64_t offset) {
+                               uint64_t seed, uint64_t offset, const uint16_t* keep_bits) {
   if (dtype == OASES_BF16)
     return ln_bwd_t<__nv_bfloat16>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st,
-                                   which, gout, drop_p, seed, offset);
+                                   which, gout, drop_p, seed, offset, keep_bits);
   return ln_bwd_t<float>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st, which,
-                         gout, drop_p, seed, offset);
+                         gout, drop_p, seed, offset, keep_bits);
 }
 
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,

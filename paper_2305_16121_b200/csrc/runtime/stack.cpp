@@ -161,6 +161,11 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
     const char* e = std::getenv("OASES_FUSED_BDR_LN");
     fuse_bdr_ln_ = !(e && e[0] == '0');
   }
+  // the fused forward kernel caches the hidden-dropout decisions for the backward
+  hbits_ = cfg.ln && fuse_bdr_ln_ && cfg.p_hidden > 0.f && cfg.h % 16 == 0 &&
+           bdr_layernorm_supported(static_cast<int64_t>(cfg.b / 2) * cfg.s, static_cast<int>(cfg.h)) &&
+           ln_bwd_dropout_supported(cfg.bytes == 2 ? OASES_BF16 : OASES_F32, static_cast<int64_t>(cfg.b / 2) * cfg.s,
+                                    static_cast<int>(cfg.h));
   // Fused tcgen05 attention unless OASES_FUSED_ATTN=0 (A/B runs of the unfused chain).
   {
     const char* e = std::getenv("OASES_FUSED_ATTN");
@@ -275,6 +280,13 @@ void Stack::alloc_all() {
     w.dcol = arena_.alloc(static_cast<size_t>(2 * Ts * ncol_max) * es);  // [sb][T_sub, ncol] of the block
     if (prob) w.dp = arena_.alloc(static_cast<size_t>(prob) * es);
     if (prob && fused_attn_) w.attn_ws = arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float));
+    if (hbits_) {
+      w.hbits.assign(static_cast<size_t>(nblocks_), {nullptr, nullptr});
+      for (int b = 0; b + 1 < nblocks_; ++b)
+        for (int sb = 0; sb < 2; ++sb)
+          w.hbits[static_cast<size_t>(b)][static_cast<size_t>(sb)] =
+              static_cast<uint16_t*>(arena_.alloc(static_cast<size_t>(Ts * h / 16) * sizeof(uint16_t)));
+    }
     if (prob && fused_attn_ && cfg_.p_attn > 0.f) {
       oases_attn_desc md{};
       md.samples = static_cast<int>(bh);
@@ -429,17 +441,18 @@ void Stack::join_side() {
 // x_b = x_{b-1} + dropout(ar + bias_row_{b-1}), then LN_b(x_b) -> ln: one
 // fused HBM pass where the row-group kernel covers the shape (its LN is
 // bit-identical to ln_fwd of the stored x_b), else the two kernels.
-void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln) {
+void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln, bool store_bits) {
   const int64_t Ts = tokens_sub(), h = cfg_.h;
   const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
   const BlockParams& bp = w.params[static_cast<size_t>(block)];
   const void* bias = cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr;
   const void* res = cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr;
   if (cfg_.ln && fuse_bdr_ln_ && bdr_layernorm_supported(Ts, static_cast<int>(h))) {
+    uint16_t* bits = store_bits && hbits_ ? w.hbits[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr;
     check_cuda(bias_dropout_residual_layernorm_fwd(dtype(), ar, bias, res, x, bp.p[OASES_P_LN_GAMMA],
                                                    bp.p[OASES_P_LN_BETA], ln, Ts, static_cast<int>(h), cfg_.eps,
                                                    cfg_.p_hidden, cfg_.seed, drop_offset(block - 1, sb, 0),
-                                                   ctx_.compute),
+                                                   ctx_.compute, bits),
                "bdr + layernorm");
     ++launches_;
     return;
@@ -757,7 +770,7 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
   const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
   const void* ln = x;
   if (block > 0 && with_bdr) {
-    bdr_then_ln(w, block, sb, w.fwd_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln);
+    bdr_then_ln(w, block, sb, w.fwd_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln, true);
   } else if (cfg_.ln) {
     ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
   }
@@ -815,7 +828,7 @@ void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) 
   const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
   const void* ln = x;
   if (rebuild_x && block > 0) {
-    bdr_then_ln(w, block, sb, w.rec_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln);
+    bdr_then_ln(w, block, sb, w.rec_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln, false);
   } else if (cfg_.ln) {
     ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
   }
@@ -888,7 +901,8 @@ void Stack::backward(int wi, int block, int sb) {
       void* stats_sb = static_cast<char*>(w.ln_ws) + static_cast<size_t>(sb) * Ts * 2 * sizeof(float);
       check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
                                     nullptr, 0, stats_sb, Ts, hi, cfg_.eps, ctx_.compute, fuse ? gar_sb : nullptr,
-                                    cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0)),
+                                    cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0),
+                                    fuse && hbits_ ? w.hbits[static_cast<size_t>(block)][usb] : nullptr),
                  "layernorm_bwd");
       gar_done = fuse;
       ++launches_;

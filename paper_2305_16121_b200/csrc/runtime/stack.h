@@ -100,6 +100,10 @@ struct Worker {
   // attention-dropout keep bits per [attention block][sb], written by the
   // forward pass, read by the recompute forward and the backward
   std::vector<std::array<uint32_t*, 2>> mask_bits;
+  // hidden-dropout keep bits per [block b][sb] of the dropout on AR_b's output,
+  // written by the forward's fused bias-dropout-residual + LN of block b+1,
+  // read by the backward's fused LN-backward + dropout'
+  std::vector<std::array<uint16_t*, 2>> hbits;
   void* y = nullptr;     // [T_sub, h] final output for the loss head
   void* ln_ws = nullptr;
   void* col_ws = nullptr;
@@ -162,7 +166,7 @@ class Stack {
   void join_side();  // compute stream waits for the side stream's current tail
   bool side_forked_ = false;
   void ln_fwd(const void* x, const void* g, const void* b, void* y);
-  void bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln);
+  void bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln, bool store_bits);
   oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int mask_mode);
   void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
@@ -177,7 +181,8 @@ class Stack {
   int nblocks_ = 0;
   bool fused_attn_ = false;
   bool fuse_bdr_ln_ = true;
-  bool rowdot_ = false;  // attention D = rowsum(dO o O) comes from the proj dgrad epilogue  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
+  bool rowdot_ = false;
+  bool hbits_ = false;  // hidden-dropout keep bits cached (fused forward kernel covers the shape)  // attention D = rowsum(dO o O) comes from the proj dgrad epilogue  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;
