@@ -222,8 +222,11 @@ struct FwdCfg {
   static constexpr int Q_OFF = 0;                        // [2] double-buffered across items
   static constexpr int K_OFF = 2 * TILE_BYTES;           // [2]
   static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;   // [2]
-  static constexpr int RED_OFF = V_OFF + 2 * TILE_BYTES;  // row max / row sum exchange [4 parts][128 rows]
-  static constexpr int BAR_OFF = RED_OFF + 4 * kTile * 4;
+  // row-max exchange [2 parities][4 parts][128 rows] (one barrier per KV tile),
+  // then the row-sum exchange of the item epilogue [4 parts][128 rows]
+  static constexpr int RED_OFF = V_OFF + 2 * TILE_BYTES;
+  static constexpr int REDL_OFF = RED_OFF + 2 * 4 * kTile * 4;
+  static constexpr int BAR_OFF = REDL_OFF + 4 * kTile * 4;
   static constexpr int SMEM = BAR_OFF + 256;
   // TMEM: NS S/P buffers of 128 columns + NO O accumulators of DH columns.
   // Three S buffers give the S MMA of iteration g+3 the slack of a whole
@@ -428,7 +431,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int c0 = part * 32;
     constexpr int OC = DH / 4;  // O columns per warp
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    float* red = reinterpret_cast<float*>(smem + C::RED_OFF);  // [part][row]
+    float* redm = reinterpret_cast<float*>(smem + C::RED_OFF);   // [parity][part][row]
+    float* redl = reinterpret_cast<float*>(smem + C::REDL_OFF);  // [part][row]
     PhiloxLite ph;
     philox_init(p, ph);
     int g = 0;
@@ -475,12 +479,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int kk = 4; kk < 32; ++kk) mp[kk & 3] = fmaxf(mp[kk & 3], __uint_as_float(u[kk]));
           mpart = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
         }
-        tc_fence_before();           // this warp's S loads precede the barrier (P overwrites S below)
-        named_bar_sync(1 + q, 128);  // the quarter's previous partials are consumed
-        red[part * kTile + rr] = mpart;
+        // Partials alternate between two buffers: a warp can only write a buffer
+        // again after the next tile's barrier, which every warp of the quarter
+        // reaches after reading it. The barrier also orders every warp's S loads
+        // before any P store over S below.
+        float* rm = redm + (g & 1) * 4 * kTile;
+        rm[part * kTile + rr] = mpart;
+        tc_fence_before();
         named_bar_sync(1 + q, 128);
         tc_fence_after();
-        const float mloc = fmaxf(fmaxf(red[rr], red[kTile + rr]), fmaxf(red[2 * kTile + rr], red[3 * kTile + rr]));
+        const float mloc = fmaxf(fmaxf(rm[rr], rm[kTile + rr]), fmaxf(rm[2 * kTile + rr], rm[3 * kTile + rr]));
         // Conditional rescaling: keep the running max unless the row max grew by
         // more than 8 (log2 units). P = exp2(s - m) then stays <= 256 (exact in
         // bf16's range) and O, l are rescaled only when it pays; the result is
@@ -558,10 +566,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[st]);
       }
       // ---- item epilogue: O / l -> ctx, lse
+      redl[part * kTile + rr] = l;  // previous item's sums were read before this item's tile barriers
       named_bar_sync(1 + q, 128);
-      red[part * kTile + rr] = l;
-      named_bar_sync(1 + q, 128);
-      const float lt = (red[rr] + red[kTile + rr]) + (red[2 * kTile + rr] + red[3 * kTile + rr]);
+      const float lt = (redl[rr] + redl[kTile + rr]) + (redl[2 * kTile + rr] + redl[3 * kTile + rr]);
       mbar_wait(&pv_done[(g - 1) % C::NS], ((g - 1) / C::NS) & 1);
       tc_fence_after();
       const float inv = p.ks / lt;
