@@ -215,7 +215,13 @@ def main():
         uid = obj[0]
     tp = world
     mc = ModelConfig(dtype="bf16", hidden_dropout=args.dropout, attention_dropout=args.dropout, **cfg)
-    ctx = Context(tp=tp, rank=rank, device=local, unique_id=uid)
+    # TMP > 1: the persistent GEMM / attention grids leave SMs to NCCL so the
+    # AllReduce of one sub-batch can run under the other sub-batch's compute
+    # (a full-width persistent grid would block the collective until it ends)
+    reserve = int(os.environ.get("OASES_NCCL_SMS", "16")) if tp > 1 else 0
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    ctx = Context(tp=tp, rank=rank, device=local, unique_id=uid, nccl_max_ctas=reserve,
+                  gemm_max_ctas=(sms - reserve) // 2 * 2 if reserve else 0)
     stack = LayerStack(ctx, mc)
     stack.init_random(1234)
     plan = plan_for(mc, args.variant)
@@ -298,6 +304,7 @@ def main():
                    "global_batch": cfg["batch"], "seq_len": cfg["seq"], "hidden": cfg["hidden"],
                    "heads": cfg["heads"], "layers": cfg["layers"], "parallelism": f"tp{tp}",
                    "schedule": args.variant, "dropout": args.dropout, "cuda_graph": not args.no_graph,
+                   "sms_reserved_for_nccl": reserve,
                    "l2": "working set (>4 GB) exceeds the 126 MB L2; no flush"},
         "exposed_comm_pct": 100.0 * traced.comm_exposed / traced.makespan if traced.makespan else 0.0,
         "measured_sim": {"makespan_s": traced.makespan, "comm_exposed_s": traced.comm_exposed,

@@ -1052,6 +1052,8 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (grid > static_cast<unsigned>(sms)) grid = static_cast<unsigned>(sms);  // persistent: one CTA per SM
+    // leave SMs to the overlapped collectives when the caller caps the persistent grids
+    if (d.max_ctas > 0 && grid > static_cast<unsigned>(d.max_ctas)) grid = static_cast<unsigned>(d.max_ctas);
   }
   cudaError_t e;
   if (d.head_dim == 128) {
