@@ -110,6 +110,9 @@ typedef struct {
   int32_t rowdot_group;             /* columns per group (head dim: 64 | 128) */
   int32_t rowdot_seq, rowdot_heads; /* rows per sample, groups per row */
   int32_t pad2_;
+  float* colsum; /* MUL epilogue, optional: COLSUM[m / 32][n] = sum over rows m..m+31 of the stored C
+                    (bf16-rounded), f32, N % 32 == 0; oases_colsum_finalize sums the [ceil(M/32), N]
+                    partials into the bias gradient (replaces a column-sum pass over C) */
 } oases_gemm_desc;
 
 oases_status oases_gemm(const oases_gemm_desc* desc, void* stream);
@@ -221,6 +224,10 @@ size_t oases_colsum_workspace(int64_t rows, int64_t cols);
 /* dbias (+)= column sums of x. */
 oases_status oases_colsum(int dtype, const void* x, float* out, int accumulate, float* workspace,
                           int64_t rows, int64_t cols, void* stream);
+/* out[n] (+)= sum_k partials[k][n], k < chunks, fixed order (deterministic): the second half of
+ * oases_colsum for partials a GEMM's MUL epilogue wrote (oases_gemm_desc.colsum). */
+oases_status oases_colsum_finalize(const float* partials, int64_t chunks, int64_t cols, float* out,
+                                   int accumulate, void* stream);
 
 /* Exact-erf GeLU and its derivative (numerics.cpp:50-55,66-76). */
 oases_status oases_gelu_fwd(int dtype, const void* x, void* y, int64_t n, void* stream);

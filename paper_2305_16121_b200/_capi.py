@@ -66,6 +66,7 @@ class GemmDesc(C.Structure):
         ("rowdot_seq", C.c_int32),
         ("rowdot_heads", C.c_int32),
         ("pad2_", C.c_int32),
+        ("colsum", C.c_void_p),
     ]
 
 
@@ -217,6 +218,7 @@ _SIGNATURES = [
     ("oases_colsum_workspace", C.c_size_t, [C.c_int64, C.c_int64]),
     ("oases_colsum", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_void_p]),
+    ("oases_colsum_finalize", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int, C.c_void_p]),
     ("oases_gelu_fwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("oases_gelu_bwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("oases_gelu_sq_loss", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int64,

@@ -512,6 +512,12 @@ cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, v
   return cudaGetLastError();
 }
 
+cudaError_t col_finalize(const float* part, long long chunks, int cols, float* out, int acc, cudaStream_t st) {
+  launch_pdl(col_finalize_fast_kernel, dim3((cols + 31) / 32), dim3(kThreads), 0, st, part, static_cast<int>(chunks),
+             cols, out, acc);
+  return cudaGetLastError();
+}
+
 cudaError_t gelu_fwd(int dtype, const void* x, void* y, long long n, cudaStream_t st) {
   const unsigned g = grid_for(n, kThreads);
   if (dtype == OASES_BF16)

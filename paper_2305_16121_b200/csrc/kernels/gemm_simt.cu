@@ -120,6 +120,10 @@ GemmStatus gemm_simt(const oases_gemm_desc& d, cudaStream_t stream) {
     st.err = "gemm_simt: f32 operands require f32 output";
     return st;
   }
+  if (d.colsum) {
+    st.err = "gemm_simt: COLSUM partials are implemented on the bf16 tensor-core path only";
+    return st;
+  }
   if (d.epilogue == OASES_EPI_ROWDOT) {
     st.err = "gemm_simt: the ROWDOT epilogue is implemented on the bf16 tensor-core path only";
     return st;

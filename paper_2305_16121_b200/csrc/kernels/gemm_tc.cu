@@ -74,6 +74,7 @@ struct TcParams {
   float alpha;
   float* rowdot;  // EPI_ROWDOT output
   int rd_group, rd_seq, rd_heads;
+  float* colsum;  // EPI_MUL column-sum partials [ceil(M/32)][N] (or null)
 };
 
 struct TileInfo {
@@ -238,6 +239,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
   constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU || EPI == OASES_EPI_BIAS_GELU_GRAD;
   constexpr bool RD = EPI == OASES_EPI_ROWDOT;
   constexpr bool DG = EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL || RD;  // epilogues reading AUX
+  constexpr bool CS = EPI == OASES_EPI_MUL;  // optional column-sum partials of the stored C
   const int nc = nbeg + c * 32;
   // All of the chunk's global operand loads are in flight at once (one DRAM
   // latency per chunk instead of one per row pair). bf16 operands (4 vectors)
@@ -262,6 +264,9 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
   __syncwarp();
   const int n = nc + lc * E;
   const int valid = p.N - n;  // elements of this lane's group inside the problem
+  float cs[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) cs[i] = 0.f;
   if (valid > 0) {
     float b[E];
     if constexpr (BIAS) {
@@ -311,6 +316,9 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
 #pragma unroll
           for (int i = 0; i < E; ++i) v[i] += o[i];
         }
+        if constexpr (CS)
+#pragma unroll
+          for (int i = 0; i < E; ++i) cs[i] += to_f(from_f<OutT>(v[i]));  // the value stored
         if constexpr (EPI == OASES_EPI_BIAS_GELU) {
           // C2 == null: only the activation is wanted (pre-activation dead), into C
           if (p.c2) st_vec<OutT, E>(cp, v);
@@ -354,6 +362,21 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
             cp[i] = from_f<OutT>(x);
           }
         }
+      }
+    }
+  }
+  if constexpr (CS) {
+    if (p.colsum) {  // N % 32 == 0 (host-checked): every lane's group is whole
+      // reduce over the rows of the stripe (lanes of equal lc), fixed order
+#pragma unroll
+      for (int o = G::LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < E; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
+      if (lr == 0) {
+        float* dst = p.colsum + (row0 >> 5) * static_cast<long long>(p.N) + n;
+#pragma unroll
+        for (int i = 0; i < E; i += 4)
+          *reinterpret_cast<float4*>(dst + i) = make_float4(cs[i], cs[i + 1], cs[i + 2], cs[i + 3]);
       }
     }
   }
@@ -962,6 +985,11 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
     *err = "gemm_tc: ROWDOT needs bf16 C, AUX, rowdot, unbatched, N = heads*group (group % 32 == 0), M % seq == 0";
     return false;
   }
+  if (d.colsum && (d.epilogue != OASES_EPI_MUL || d.batch != 1 || d.N % 32 || d.c_row_off[0] || d.c_row_off[1] ||
+                   (reinterpret_cast<uintptr_t>(d.colsum) % 16))) {
+    *err = "gemm_tc: COLSUM partials need the MUL epilogue, unbatched, N % 32 == 0, no row offsets, 16 B aligned";
+    return false;
+  }
   if (d.epilogue < OASES_EPI_NONE || d.epilogue > OASES_EPI_ROWDOT) {
     *err = "gemm_tc: unknown epilogue";
     return false;
@@ -1027,6 +1055,7 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
   p.rd_group = d.rowdot_group;
   p.rd_seq = d.rowdot_seq;
   p.rd_heads = d.rowdot_heads;
+  p.colsum = d.colsum;
   p.bias = d.bias;
   p.ldc = d.ldc;
   p.c_f32 = d.c_dtype == OASES_F32;

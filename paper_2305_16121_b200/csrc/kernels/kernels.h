@@ -53,6 +53,8 @@ size_t colsum_workspace(long long rows, int cols);
 // dx = dropout'(in) (if dx), out (+)= column sums of dx (if out).
 cudaError_t col_pass(int dtype, const void* in, void* dx, float* out, int acc, void* ws, long long rows, int cols,
                      float p, uint64_t seed, uint64_t offset, cudaStream_t st);
+// out (+)= sum over `chunks` rows of part[chunks][cols] (fixed order).
+cudaError_t col_finalize(const float* part, long long chunks, int cols, float* out, int acc, cudaStream_t st);
 cudaError_t gelu_fwd(int dtype, const void* x, void* y, long long n, cudaStream_t st);
 cudaError_t gelu_bwd(int dtype, const void* x, const void* dy, void* dx, long long n, cudaStream_t st);
 size_t loss_workspace();

@@ -227,6 +227,16 @@ oases_status oases_colsum(int dtype, const void* x, float* out, int accumulate, 
   });
 }
 
+oases_status oases_colsum_finalize(const float* partials, int64_t chunks, int64_t cols, float* out, int accumulate,
+                                   void* stream) {
+  return guarded([&] {
+    if (!partials || !out || chunks <= 0 || cols <= 0) throw tmpsim::ConfigError("oases_colsum_finalize: empty");
+    need_device();
+    check_cuda(oases::col_finalize(partials, chunks, static_cast<int>(cols), out, accumulate, S(stream)),
+               "colsum_finalize");
+  });
+}
+
 oases_status oases_gelu_fwd(int dtype, const void* x, void* y, int64_t n, void* stream) {
   return guarded([&] {
     check_dtype(dtype);

@@ -166,6 +166,12 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
            bdr_layernorm_supported(static_cast<int64_t>(cfg.b / 2) * cfg.s, static_cast<int>(cfg.h)) &&
            ln_bwd_dropout_supported(cfg.bytes == 2 ? OASES_BF16 : OASES_F32, static_cast<int64_t>(cfg.b / 2) * cfg.s,
                                     static_cast<int>(cfg.h));
+  // FFN column-bias gradient from the FC2 dgrad epilogue's partials unless OASES_FUSED_COLSUM=0
+  {
+    const char* e = std::getenv("OASES_FUSED_COLSUM");
+    colsum_ = cfg.bias && cfg.bytes == 2 && (static_cast<int64_t>(cfg.b / 2) * cfg.s) % 32 == 0 &&
+              ncol_ffn_ % 32 == 0 && !(e && e[0] == '0');
+  }
   // Fused tcgen05 attention unless OASES_FUSED_ATTN=0 (A/B runs of the unfused chain).
   {
     const char* e = std::getenv("OASES_FUSED_ATTN");
@@ -305,6 +311,10 @@ void Stack::alloc_all() {
                                      colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
     w.col_ws2 = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
                                       colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
+    // [2 T_sub / 32, ncol_ffn] partials of the fused FFN column-bias gradient (own buffer: the
+    // attention blocks' side-stream column sums may run between the two sub-batches' FC2 dgrads)
+    w.col_part = colsum_ ? static_cast<float*>(arena_.alloc(static_cast<size_t>(2 * Ts / 32 * ncol_ffn_) * sizeof(float)))
+                         : nullptr;
     w.loss = static_cast<double*>(arena_.alloc(sizeof(double)));
     w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
   }
@@ -990,6 +1000,9 @@ void Stack::backward(int wi, int block, int sb) {
     d.c = half(w.dcol, sb, ncol); d.ldc = ncol;
     d.epilogue = OASES_EPI_MUL;
     d.aux = ws.col;
+    // column-bias gradient partials (32-row sums of dpre) from the same epilogue: this
+    // sub-batch's rows [sb T_sub / 32, (sb + 1) T_sub / 32) of the partials
+    if (colsum_) d.colsum = w.col_part + static_cast<int64_t>(sb) * (Ts / 32) * ncol;
     if (wgrad_now) gemm2(dw, d);
     else gemm(d);
   }
@@ -999,10 +1012,17 @@ void Stack::backward(int wi, int block, int sb) {
     // the column GEMMs
     const bool acc = touch(w, block, OASES_P_B_COL);
     fork_side();
-    check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, 2 * Ts,
-                        static_cast<int>(ncol), 0.f, 0, 0, ctx_.side),
-               "colsum");
-    launches_ += 2;
+    if (colsum_ && !att) {  // partials of both sub-batches' FC2 dgrad epilogues
+      check_cuda(col_finalize(w.col_part, 2 * Ts / 32, static_cast<int>(ncol),
+                              bp.g[OASES_P_B_COL], acc ? 1 : 0, ctx_.side),
+                 "colsum finalize");
+      launches_ += 1;
+    } else {
+      check_cuda(col_pass(dtype(), w.dcol, nullptr, bp.g[OASES_P_B_COL], acc ? 1 : 0, w.col_ws2, 2 * Ts,
+                          static_cast<int>(ncol), 0.f, 0, 0, ctx_.side),
+                 "colsum");
+      launches_ += 2;
+    }
   }
   // 5. column-parallel GEMM: dW_col (+)= dcol^T ln over both sub-batches ; d_ln partial = dcol W_col
   //    -> AR_b (backward f)

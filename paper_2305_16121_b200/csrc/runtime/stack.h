@@ -108,6 +108,7 @@ struct Worker {
   void* ln_ws = nullptr;
   void* col_ws = nullptr;
   void* col_ws2 = nullptr;  // side-stream column sums (bias gradients)
+  float* col_part = nullptr;  // FC2 dgrad epilogue's 32-row column-sum partials (FFN column bias)
   double* loss = nullptr;     // device scalar (f64)
   double* loss_ws = nullptr;  // partials
 };
@@ -179,10 +180,11 @@ class Stack {
   DeviceArena arena_;
   std::vector<Worker> workers_;
   int nblocks_ = 0;
-  bool fused_attn_ = false;
+  bool fused_attn_ = false;  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
   bool fuse_bdr_ln_ = true;
-  bool rowdot_ = false;
-  bool hbits_ = false;  // hidden-dropout keep bits cached (fused forward kernel covers the shape)  // attention D = rowsum(dO o O) comes from the proj dgrad epilogue  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
+  bool rowdot_ = false;  // attention D = rowsum(dO o O) comes from the proj dgrad epilogue
+  bool hbits_ = false;   // hidden-dropout keep bits cached (fused forward kernel covers the shape)
+  bool colsum_ = false;  // FFN column-bias gradient partials come from the FC2 dgrad (MUL) epilogue
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   std::vector<bool> loss_touched_;

@@ -48,7 +48,7 @@ def operand(t: torch.Tensor, mn_major: bool = False, row_off=(0, 0), col_off=(0,
 def gemm_desc(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_off=(0, 0), c_col_off=(0, 0),
               c_col_base=0, epilogue=capi.EPI_NONE, causal=capi.CAUSAL_NONE, alpha=1.0, accumulate=False,
               bias=None, aux=None, c2=None, max_ctas=0, dtype=capi.BF16, rowdot=None, rowdot_group=0,
-              rowdot_seq=0, rowdot_heads=0):
+              rowdot_seq=0, rowdot_heads=0, colsum=None):
     d = capi.GemmDesc()
     d.dtype = dtype
     d.c_dtype = _dtype(c)
@@ -70,6 +70,7 @@ def gemm_desc(M, N, K, a, b, c: torch.Tensor, *, batch=1, batch_inner=1, c_row_o
     d.max_ctas = max_ctas
     d.rowdot = None if rowdot is None else rowdot.data_ptr()
     d.rowdot_group, d.rowdot_seq, d.rowdot_heads = rowdot_group, rowdot_seq, rowdot_heads
+    d.colsum = None if colsum is None else colsum.data_ptr()
     return d
 
 
@@ -189,6 +190,13 @@ def colsum(x, out, accumulate=False, stream=None):
     ws = torch.empty(capi.lib().oases_colsum_workspace(rows, cols) // 4 + 64, dtype=torch.float32, device=x.device)
     check(capi.lib().oases_colsum(_dtype(x), _ptr(x), _ptr(out), int(accumulate), _ptr(ws), rows, cols,
                                   _stream(stream)))
+
+
+def colsum_finalize(partials, out, accumulate=False, stream=None):
+    """out (+)= partials.sum(0) in a fixed order (partials: [chunks, cols] f32, e.g. from gemm(colsum=))."""
+    chunks, cols = partials.shape
+    check(capi.lib().oases_colsum_finalize(_ptr(partials), chunks, cols, _ptr(out), int(accumulate),
+                                           _stream(stream)))
 
 
 def gelu_fwd(x, y, stream=None):

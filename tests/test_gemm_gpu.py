@@ -225,6 +225,52 @@ def test_gemm_gelu_grad_and_mul_epilogues(cuda, dt):
     assert relerr(out, (G.double() @ W.double().t()) * dgl.double()) < tol
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (1000, 384, 192), (4096, 8192, 2048), (96, 2080, 64)])
+def test_gemm_mul_colsum_partials(cuda, M, N, K):
+    """MUL epilogue with colsum partials: COLSUM[m / 32][n] = sum of the stored bf16 C over
+    rows m..m+31 (CTA-pair and single-CTA kernels, ragged M), then oases_colsum_finalize
+    gives the column-bias gradient -- equal to oases_colsum over C, the unfused pass."""
+    torch.manual_seed(13)
+    G = torch.randn(M, K, device=cuda).bfloat16()
+    W = (torch.randn(N, K, device=cuda) / math.sqrt(K)).bfloat16()
+    X = torch.rand(M, N, device=cuda).bfloat16()
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    chunks = (M + 31) // 32
+    part = torch.full((chunks, N), float("nan"), device=cuda)
+    ops.gemm(M, N, K, ops.operand(G), ops.operand(W), out, epilogue=capi.EPI_MUL, aux=X, colsum=part)
+    ref = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(M, N, K, ops.operand(G), ops.operand(W), ref, epilogue=capi.EPI_MUL, aux=X)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)  # the stored C does not change
+    assert torch.isfinite(part).all()
+    pad = torch.zeros(chunks * 32, N, device=cuda, dtype=torch.float64)
+    pad[:M] = out.double()
+    assert relerr(part, pad.view(chunks, 32, N).sum(1)) < 1e-6
+    db = torch.full((N,), 2.0, device=cuda)
+    ops.colsum_finalize(part, db, accumulate=True)
+    db2 = torch.full((N,), 2.0, device=cuda)
+    ops.colsum(out, db2, accumulate=True)
+    torch.cuda.synchronize()
+    assert relerr(db - 2.0, out.double().sum(0)) < 1e-5
+    assert relerr(db, db2) < 1e-5
+    # fixed reduction order: a second run gives the same bits
+    part2 = torch.empty_like(part)
+    ops.gemm(M, N, K, ops.operand(G), ops.operand(W), out, epilogue=capi.EPI_MUL, aux=X, colsum=part2)
+    torch.cuda.synchronize()
+    assert torch.equal(part, part2)
+
+
+def test_gemm_colsum_rejected_outside_mul(cuda):
+    A = torch.randn(128, 64, device=cuda).bfloat16()
+    C = torch.empty(128, 128, device=cuda, dtype=torch.bfloat16)
+    part = torch.empty(4, 128, device=cuda)
+    with pytest.raises(Exception, match="COLSUM"):
+        ops.gemm(128, 128, 64, ops.operand(A), ops.operand(A[:128]), C, colsum=part)
+    with pytest.raises(Exception, match="COLSUM"):
+        ops.gemm(128, 120, 64, ops.operand(A), ops.operand(A[:120]), C[:, :120], epilogue=capi.EPI_MUL, aux=C,
+                 colsum=part)
+
+
 @pytest.mark.parametrize("dh,hl,seq,n", [(128, 4, 256, 3), (64, 6, 128, 2), (128, 16, 1024, 4)])
 def test_gemm_rowdot_epilogue(cuda, dh, hl, seq, n):
     """EPI_ROWDOT: C = A B^T stored as usual, and per (sample, head, row)
