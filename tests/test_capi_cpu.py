@@ -87,3 +87,63 @@ def test_host_only_entry_points():
     assert L.oases_gemm(None, None) == capi.ERR_CONFIG
     assert b"null descriptor" in L.oases_last_error()
     assert L.oases_colsum_finalize(None, 0, 0, None, 0, None) == capi.ERR_CONFIG
+
+
+CPP_CONSUMER = r"""
+#include <cstdio>
+#include "oases/tmpsim.hpp"
+#include "oases/runtime.hpp"
+using namespace tmpsim;
+int main() {
+  ModelSpec spec;
+  spec.hidden_size = 4096; spec.num_layers = 3; spec.seq_len = 2048;
+  spec.attention_heads = 32; spec.global_batch = 8; spec.bytes_per_element = 2;
+  spec.recompute_enabled = true;
+  const ModelGraph g = build_block_graph(build_operator_sequence(spec), spec);
+  const CostVectors costs = build_cost_vectors(g, spec, b200_profile(8));
+  const Strategy s{std::vector<int>(g.block_count(), 8)};
+  for (ScheduleVariant v : {ScheduleVariant::Oases, ScheduleVariant::CrossPass}) {
+    const SchedulePlan plan = make_schedule(g, v);
+    const SimResult r = simulate(plan, costs, s);
+    std::printf("%zu %d %.17g %.17g %.17g\n", validate_plan(plan).size(), comm_op_count(plan), r.makespan,
+                r.comm_exposed, r.peak_memory);
+  }
+  try {
+    make_schedule(g, static_cast<ScheduleVariant>(99));
+  } catch (const ConfigError&) {
+    std::printf("ConfigError\n");
+  }
+  return 0;
+}
+"""
+
+
+def test_cpp_consumer_links_the_tmpsim_api(tmp_path):
+    """A C++ caller of the reference's tmpsim API (its headers swapped for include/oases/*.hpp,
+    INTEGRATION.md) compiles, links liboases.so and gets the same plans and simulations as the
+    Python binding -- host-only, no device needed."""
+    if not os.path.exists(capi.LIB_PATH):
+        pytest.skip("liboases.so not built")
+    import paper_2305_16121_b200.tmpsim as t
+
+    src = tmp_path / "consumer.cpp"
+    src.write_text(CPP_CONSUMER)
+    exe = tmp_path / "consumer"
+    libdir = os.path.dirname(capi.LIB_PATH)
+    subprocess.check_call(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                           "-L", libdir, "-loases", f"-Wl,-rpath,{libdir}"])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    assert out[2] == "ConfigError"
+    spec = t.ModelSpec()
+    spec.hidden_size, spec.num_layers, spec.seq_len = 4096, 3, 2048
+    spec.attention_heads, spec.global_batch, spec.bytes_per_element = 32, 8, 2
+    spec.recompute_enabled = True
+    g = t.build_block_graph(t.build_operator_sequence(spec), spec)
+    costs = t.build_cost_vectors(g, spec, t.b200_profile(8))
+    s = t.Strategy([8] * g.block_count())
+    for line, v in zip(out[:2], (t.ScheduleVariant.Oases, t.ScheduleVariant.CrossPass)):
+        plan = t.make_schedule(g, v)
+        r = t.simulate(plan, costs, s)
+        nviol, ncomm, mk, ce, pm = line.split()
+        assert int(nviol) == 0 and int(ncomm) == t.comm_op_count(plan)
+        assert float(mk) == r.makespan and float(ce) == r.comm_exposed and float(pm) == r.peak_memory
