@@ -38,7 +38,7 @@ typedef enum {
   OASES_ERR_NCCL = 6
 } oases_status;
 
-typedef enum { OASES_F32 = 0, OASES_BF16 = 1 } oases_dtype;
+typedef enum { OASES_F32 = 0, OASES_BF16 = 1, OASES_F64 = 2 } oases_dtype;
 
 const char* oases_last_error(void);
 const char* oases_version(void);

@@ -34,6 +34,13 @@ class IoError : public std::runtime_error {
  public:
   explicit IoError(const std::string& w) : std::runtime_error(w) {}
 };
+// B200 extension: a CUDA or NCCL failure (no device, launch error, collective
+// error). The runtime has no CPU fallback, so value-level and execution entry
+// points raise this instead of silently computing on the host.
+class DeviceError : public std::runtime_error {
+ public:
+  explicit DeviceError(const std::string& w) : std::runtime_error(w) {}
+};
 
 // ------------------------------------------------------------- model.hpp:13-84
 enum class OpKind { ForwardCompute, RecomputeCompute, BackwardCompute, AllReduce, AllGather };
@@ -259,6 +266,57 @@ double rank_correlation(const CostVectors& costs, const std::vector<EdgeCostMatr
                         const std::vector<Strategy>& strategies, const std::vector<double>& measured_times);
 double spearman(const std::vector<double>& a, const std::vector<double>& b);
 std::string run_length_notation(const std::vector<int>& degrees);
+
+// ------------------------------------------------------------- numerics.hpp:10-60
+// The reference's value-level checker API. Same types, fields and semantics;
+// every function computes ON THE GPU (f64): the Matrix primitives in device
+// kernels with the reference's scalar arithmetic (no FMA contraction, same
+// summation order), and the ToyShardedModel checks by running the toy as an
+// f64 FFN block stack through this build's runtime -- the literal in-process
+// AllReduce is the runtime's worker-order sum kernel, and
+// recompute_elision_equivalence executes the CrossPass (replayed AllReduce)
+// and Oases (elided) plans with the plan executor. Throws DeviceError without
+// a CUDA device.
+struct Matrix {
+  int rows = 0;
+  int cols = 0;
+  std::vector<double> data;
+
+  Matrix() = default;
+  Matrix(int r, int c) : rows(r), cols(c), data(static_cast<std::size_t>(r) * c, 0.0) {}
+  double& at(int r, int c) { return data[static_cast<std::size_t>(r) * cols + c]; }
+  double at(int r, int c) const { return data[static_cast<std::size_t>(r) * cols + c]; }
+};
+
+Matrix matmul(const Matrix& a, const Matrix& b);
+Matrix transpose(const Matrix& a);
+Matrix add(const Matrix& a, const Matrix& b);
+Matrix hadamard(const Matrix& a, const Matrix& b);
+Matrix gelu(const Matrix& a);
+Matrix gelu_grad(const Matrix& a);  // elementwise derivative at a
+double max_abs_diff(const Matrix& a, const Matrix& b);
+
+struct GradIdentityCheck {
+  double autodiff_deviation = 0.0;
+  double finite_difference_deviation = 0.0;
+};
+GradIdentityCheck allreduce_grad_identity(int workers, int rows, int cols, unsigned seed);
+
+struct ToyShardedModel {
+  int workers = 1;
+  Matrix input;              // batch x model_dim
+  std::vector<Matrix> w_in;  // model_dim x (hidden/workers) column shards
+  std::vector<Matrix> w_out; // (hidden/workers) x model_dim row shards
+};
+
+ToyShardedModel make_toy_sharded_model(int workers, int batch, int model_dim, int hidden_dim, unsigned seed);
+double sharded_output_deviation(const ToyShardedModel& model);
+
+struct ElisionCheck {
+  double grad_deviation = 0.0;
+  bool loss_bit_identical = false;
+};
+ElisionCheck recompute_elision_equivalence(const ToyShardedModel& model);
 
 // ------------------------------------------------------------- trace_export.hpp:15-22
 void write_chrome_trace(const SimResult& result, const SchedulePlan& plan, const std::filesystem::path& path);

@@ -35,6 +35,7 @@
 //   1 attention); element index local to the sub-batch tensor; attention uses
 //   the GLOBAL head index so the mask is TMP-degree invariant.
 // =============================================================================
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -55,25 +56,121 @@ struct Mat {
   double at(int r, int c) const { return d[static_cast<size_t>(r) * cols + c]; }
 };
 
-// numerics.cpp:13-24: i-k-j with zero skip. Rows are independent, so the
-// OpenMP split over i leaves every element's summation order unchanged.
-Mat matmul(const Mat& a, const Mat& b) {
-  Mat c(a.rows, b.cols);
-#pragma omp parallel for schedule(static) if (static_cast<long long>(a.rows) * a.cols * b.cols > 200000)
-  for (int i = 0; i < a.rows; ++i) {
-    double* ci = &c.d[static_cast<size_t>(i) * c.cols];
-    for (int k = 0; k < a.cols; ++k) {
-      const double av = a.d[static_cast<size_t>(i) * a.cols + k];
-      if (av == 0.0) continue;
-      const double* bk = &b.d[static_cast<size_t>(k) * b.cols];
-      for (int j = 0; j < b.cols; ++j) ci[j] += av * bk[j];
+// numerics.cpp:13-24: c[i][j] = sum_k a[i][k] b[k][j], accumulated in
+// ascending k with the terms of a[i][k] == 0 skipped. The blocking below
+// (B packed into 8-column panels, row/column tiles in parallel, k-blocks in
+// ascending order, a 4x8 register tile) changes WHICH element is updated when,
+// but never the sequence of additions into any one element, so the result is
+// bit-identical to the reference loop (pinned by tests/test_oracle.py against
+// the reference's own tensors); -ffp-contract=off keeps mul and add separate.
+// A row quad whose k-block holds a zero takes the select form of the skip.
+typedef double v4d __attribute__((vector_size(32)));
+typedef long long v4l __attribute__((vector_size(32)));
+
+template <bool kSkip>
+__attribute__((always_inline)) inline void mm_quad(const double* __restrict ar, int lda, const double* __restrict bp, double* __restrict c, int ldc,
+                    int ncols, int k0, int k1) {
+  alignas(32) double tmp[4][8] = {};
+  for (int r = 0; r < 4; ++r)
+    for (int t = 0; t < ncols; ++t) tmp[r][t] = c[static_cast<size_t>(r) * ldc + t];
+  v4d a00, a01, a10, a11, a20, a21, a30, a31;
+  std::memcpy(&a00, tmp[0], 32); std::memcpy(&a01, tmp[0] + 4, 32);
+  std::memcpy(&a10, tmp[1], 32); std::memcpy(&a11, tmp[1] + 4, 32);
+  std::memcpy(&a20, tmp[2], 32); std::memcpy(&a21, tmp[2] + 4, 32);
+  std::memcpy(&a30, tmp[3], 32); std::memcpy(&a31, tmp[3] + 4, 32);
+  for (int k = k0; k < k1; ++k) {
+    v4d b0, b1;
+    std::memcpy(&b0, bp + static_cast<size_t>(k) * 8, 32);
+    std::memcpy(&b1, bp + static_cast<size_t>(k) * 8 + 4, 32);
+#define OASES_ORACLE_ROW(R, A0, A1)                         \
+  {                                                         \
+    const double av = ar[static_cast<size_t>(R) * lda + k]; \
+    const v4d avv = {av, av, av, av};                       \
+    const v4d s0 = A0 + avv * b0, s1 = A1 + avv * b1;       \
+    if (kSkip) {                                            \
+      const long long kk = av != 0.0 ? -1LL : 0LL;          \
+      const v4l m = {kk, kk, kk, kk};                       \
+      A0 = m ? s0 : A0;                                     \
+      A1 = m ? s1 : A1;                                     \
+    } else {                                                \
+      A0 = s0;                                              \
+      A1 = s1;                                              \
+    }                                                       \
+  }
+    OASES_ORACLE_ROW(0, a00, a01)
+    OASES_ORACLE_ROW(1, a10, a11)
+    OASES_ORACLE_ROW(2, a20, a21)
+    OASES_ORACLE_ROW(3, a30, a31)
+#undef OASES_ORACLE_ROW
+  }
+  std::memcpy(tmp[0], &a00, 32); std::memcpy(tmp[0] + 4, &a01, 32);
+  std::memcpy(tmp[1], &a10, 32); std::memcpy(tmp[1] + 4, &a11, 32);
+  std::memcpy(tmp[2], &a20, 32); std::memcpy(tmp[2] + 4, &a21, 32);
+  std::memcpy(tmp[3], &a30, 32); std::memcpy(tmp[3] + 4, &a31, 32);
+  for (int r = 0; r < 4; ++r)
+    for (int t = 0; t < ncols; ++t) c[static_cast<size_t>(r) * ldc + t] = tmp[r][t];
+}
+
+// rows [i0, i1) x panels [p0, p1) x k in [k0, k1); bpk = packed B ([panel][K][8])
+__attribute__((target_clones("avx2", "default")))
+void mm_block(const double* __restrict a, int lda, const double* __restrict bpk, int K, double* __restrict c, int ldc,
+              int ncol, int i0, int i1, int p0, int p1, int k0, int k1) {
+  int i = i0;
+  for (; i + 4 <= i1; i += 4) {
+    const double* ar = a + static_cast<size_t>(i) * lda;
+    bool zero = false;
+    for (int r = 0; r < 4 && !zero; ++r)
+      for (int k = k0; k < k1; ++k)
+        if (ar[static_cast<size_t>(r) * lda + k] == 0.0) {
+          zero = true;
+          break;
+        }
+    for (int pnl = p0; pnl < p1; ++pnl) {
+      const double* bp = bpk + static_cast<size_t>(pnl) * K * 8;
+      double* cc = c + static_cast<size_t>(i) * ldc + pnl * 8;
+      const int nc = std::min(8, ncol - pnl * 8);
+      if (zero) mm_quad<true>(ar, lda, bp, cc, ldc, nc, k0, k1);
+      else mm_quad<false>(ar, lda, bp, cc, ldc, nc, k0, k1);
     }
   }
+  for (; i < i1; ++i)
+    for (int k = k0; k < k1; ++k) {
+      const double av = a[static_cast<size_t>(i) * lda + k];
+      if (av == 0.0) continue;
+      for (int pnl = p0; pnl < p1; ++pnl) {
+        const double* bk = bpk + (static_cast<size_t>(pnl) * K + k) * 8;
+        double* ci = c + static_cast<size_t>(i) * ldc + pnl * 8;
+        const int nc = std::min(8, ncol - pnl * 8);
+        for (int t = 0; t < nc; ++t) ci[t] += av * bk[t];
+      }
+    }
+}
+
+Mat matmul(const Mat& a, const Mat& b) {
+  Mat c(a.rows, b.cols);
+  const int K = a.cols, N = b.cols, np = (N + 7) / 8;
+  const bool par = static_cast<long long>(a.rows) * K * N > 200000;
+  std::vector<double> bpk(static_cast<size_t>(np) * K * 8, 0.0);
+#pragma omp parallel for schedule(static) if (par)
+  for (int pnl = 0; pnl < np; ++pnl)
+    for (int k = 0; k < K; ++k)
+      for (int t = 0; t < 8 && pnl * 8 + t < N; ++t)
+        bpk[(static_cast<size_t>(pnl) * K + k) * 8 + t] = b.d[static_cast<size_t>(k) * N + pnl * 8 + t];
+  constexpr int IB = 64, PB = 32, KB = 256;  // 64 rows x 256 columns x 256 k per task step
+  const int nib = (a.rows + IB - 1) / IB, npb = (np + PB - 1) / PB;
+#pragma omp parallel for collapse(2) schedule(dynamic) if (par)
+  for (int ib = 0; ib < nib; ++ib)
+    for (int pb = 0; pb < npb; ++pb) {
+      const int i0 = ib * IB, i1 = std::min(a.rows, i0 + IB), p0 = pb * PB, p1 = std::min(np, p0 + PB);
+      for (int k0 = 0; k0 < K; k0 += KB)
+        mm_block(a.d.data(), K, bpk.data(), K, c.d.data(), N, N, i0, i1, p0, p1, k0, std::min(K, k0 + KB));
+    }
   return c;
 }
 
 Mat transpose(const Mat& a) {
   Mat t(a.cols, a.rows);
+#pragma omp parallel for schedule(static) if (static_cast<long long>(a.rows) * a.cols > 1000000)
   for (int i = 0; i < a.rows; ++i)
     for (int j = 0; j < a.cols; ++j) t.at(j, i) = a.at(i, j);
   return t;
@@ -174,6 +271,7 @@ struct Oracle {
   void ln_fwd(const Mat& xin, const Mat& g, const Mat& be, Mat& y) const {
     const int h = cfg.hidden;
     y = Mat(T, h);
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < T; ++r) {
       double mean = 0.0;
       for (int c = 0; c < h; ++c) mean += xin.at(r, c);
@@ -188,6 +286,10 @@ struct Oracle {
   void ln_bwd(const Mat& xin, const Mat& g, const Mat& dy, Mat& dx, Mat& dg, Mat& db) const {
     const int h = cfg.hidden;
     dx = Mat(T, h);
+    Mat xhat(T, h);
+    // rows in parallel; the parameter gradients are summed over rows in row
+    // order afterwards (same per-element order as a serial row loop)
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < T; ++r) {
       double mean = 0.0;
       for (int c = 0; c < h; ++c) mean += xin.at(r, c);
@@ -199,11 +301,10 @@ struct Oracle {
       double s1 = 0.0, s2 = 0.0;
       for (int c = 0; c < h; ++c) {
         const double xh = (xin.at(r, c) - mean) * rstd;
+        xhat.at(r, c) = xh;
         const double gg = dy.at(r, c) * g.d[c];
         s1 += gg;
         s2 += gg * xh;
-        dg.d[c] += dy.at(r, c) * xh;
-        db.d[c] += dy.at(r, c);
       }
       s1 /= h;
       s2 /= h;
@@ -212,6 +313,12 @@ struct Oracle {
         dx.at(r, c) = rstd * (dy.at(r, c) * g.d[c] - s1 - xh * s2);
       }
     }
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < h; ++c)
+      for (int r = 0; r < T; ++r) {
+        dg.d[c] += dy.at(r, c) * xhat.at(r, c);
+        db.d[c] += dy.at(r, c);
+      }
   }
 
   // ---------------------------------------------------------------- attention
@@ -255,11 +362,14 @@ struct Oracle {
             }
             Pd.at(row, j) = pdv;
           }
-          for (int e = 0; e < d; ++e) {
-            double acc = 0.0;
-            for (int j = 0; j <= i; ++j) acc += Pd.at(row, j) * qkv.at(n * s + j, 2 * Ht * d + jl * d + e);
-            ctx.at(n * s + i, jl * d + e) = acc;
+          // ctx[i][e] = sum_{j<=i} Pd[i][j] V[j][e], ascending j per element (j outer for locality)
+          std::vector<double> acc(d, 0.0);
+          for (int j = 0; j <= i; ++j) {
+            const double pj = Pd.at(row, j);
+            const double* vj = &qkv.d[static_cast<size_t>(n * s + j) * qkv.cols + 2 * Ht * d + jl * d];
+            for (int e = 0; e < d; ++e) acc[e] += pj * vj[e];
           }
+          for (int e = 0; e < d; ++e) ctx.at(n * s + i, jl * d + e) = acc[e];
         }
       }
   }
@@ -295,22 +405,36 @@ struct Oracle {
           }
           for (int j = 0; j <= i; ++j) dS[static_cast<size_t>(i) * s + j] = scale * P.at(row, j) * (dP[j] - dot);
         }
-        for (int i = 0; i < s; ++i)
-          for (int e = 0; e < d; ++e) {
-            double dq = 0.0;
-            for (int j = 0; j <= i; ++j) dq += dS[static_cast<size_t>(i) * s + j] * qkv.at(n * s + j, Ht * d + jl * d + e);
-            dqkv.at(n * s + i, jl * d + e) = dq;
+        // loop orders below keep every element's summation order (ascending j for dQ,
+        // ascending i for dK/dV) with the reduction index outside the e loop
+        std::vector<double> dq(d), dk(d), dv(d);
+        for (int i = 0; i < s; ++i) {
+          std::fill(dq.begin(), dq.end(), 0.0);
+          for (int j = 0; j <= i; ++j) {
+            const double sij = dS[static_cast<size_t>(i) * s + j];
+            const double* kj = &qkv.d[static_cast<size_t>(n * s + j) * qkv.cols + Ht * d + jl * d];
+            for (int e = 0; e < d; ++e) dq[e] += sij * kj[e];
           }
-        for (int j = 0; j < s; ++j)
-          for (int e = 0; e < d; ++e) {
-            double dk = 0.0, dv = 0.0;
-            for (int i = j; i < s; ++i) {
-              dk += dS[static_cast<size_t>(i) * s + j] * qkv.at(n * s + i, jl * d + e);
-              dv += Pd.at((n * Ht + jl) * s + i, j) * dctx.at(n * s + i, jl * d + e);
+          for (int e = 0; e < d; ++e) dqkv.at(n * s + i, jl * d + e) = dq[e];
+        }
+        for (int j = 0; j < s; ++j) {
+          std::fill(dk.begin(), dk.end(), 0.0);
+          std::fill(dv.begin(), dv.end(), 0.0);
+          for (int i = j; i < s; ++i) {
+            const double sij = dS[static_cast<size_t>(i) * s + j];
+            const double pij = Pd.at((n * Ht + jl) * s + i, j);
+            const double* qi = &qkv.d[static_cast<size_t>(n * s + i) * qkv.cols + jl * d];
+            const double* oi = &dctx.d[static_cast<size_t>(n * s + i) * dctx.cols + jl * d];
+            for (int e = 0; e < d; ++e) {
+              dk[e] += sij * qi[e];
+              dv[e] += pij * oi[e];
             }
-            dqkv.at(n * s + j, Ht * d + jl * d + e) = dk;
-            dqkv.at(n * s + j, 2 * Ht * d + jl * d + e) = dv;
           }
+          for (int e = 0; e < d; ++e) {
+            dqkv.at(n * s + j, Ht * d + jl * d + e) = dk[e];
+            dqkv.at(n * s + j, 2 * Ht * d + jl * d + e) = dv[e];
+          }
+        }
       }
   }
   int worker_of_current = 0;
@@ -323,6 +447,7 @@ struct Oracle {
     const uint32_t thr = oracle::keep_threshold(p);
     const double ks = oracle::keep_scale(p);
     out = Mat(T, h);
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < T; ++r) {
       const int n = r / s, sb = n / half();
       const uint64_t rl = static_cast<uint64_t>(r - sb * half() * s);
@@ -341,6 +466,7 @@ struct Oracle {
     if (!(p > 0.f)) return;
     const uint32_t thr = oracle::keep_threshold(p);
     const double ks = oracle::keep_scale(p);
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < T; ++r) {
       const int n = r / s, sb = n / half();
       const uint64_t rl = static_cast<uint64_t>(r - sb * half() * s);
@@ -367,7 +493,8 @@ struct Oracle {
           attn_fwd(b, r, wb.col_out, wb.act, wb.P, wb.Pd);
         } else {
           wb.act = wb.col_out;
-          for (double& v : wb.act.d) v = gelu_s(v);
+#pragma omp parallel for schedule(static)
+          for (size_t i = 0; i < wb.act.d.size(); ++i) wb.act.d[i] = gelu_s(wb.act.d[i]);
         }
         ar = add(ar, matmul(wb.act, wb.p[W_ROW]));  // the literal in-process AllReduce
       }
@@ -411,6 +538,7 @@ struct Oracle {
           attn_bwd(b, wb.col_out, wb.P, wb.Pd, du, dcol);
         } else {
           dcol = du;
+#pragma omp parallel for schedule(static)
           for (size_t i = 0; i < dcol.d.size(); ++i) dcol.d[i] *= gelu_grad_s(wb.col_out.d[i]);
         }
         if (cfg.use_bias)

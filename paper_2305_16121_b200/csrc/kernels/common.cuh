@@ -43,6 +43,12 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   const float phi = 0.39894228040143268f * __expf(-0.5f * x * x);
   return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * phi;
 }
+// f64 GeLU and its derivative in the reference's own expressions (numerics.cpp:50-55)
+__device__ __forceinline__ double gelu_d(double x) { return 0.5 * x * (1.0 + erf(x / 1.4142135623730951)); }
+__device__ __forceinline__ double gelu_grad_d(double x) {
+  const double phi = exp(-0.5 * x * x) / 2.5066282746310002;
+  return 0.5 * (1.0 + erf(x / 1.4142135623730951)) + x * phi;
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

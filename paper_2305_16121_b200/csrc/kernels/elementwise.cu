@@ -333,6 +333,35 @@ __global__ void __launch_bounds__(kThreads) local_allreduce_kernel(BufList b, in
   }
 }
 
+// literal sum in worker order, 0 + x_0 + x_1 + ... (numerics.cpp:160-163)
+__global__ void __launch_bounds__(kThreads) local_allreduce_f64_kernel(BufList b, int w, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double s = static_cast<const double*>(b.p[0])[i];
+    for (int k = 1; k < w; ++k) s = __dadd_rn(s, static_cast<const double*>(b.p[k])[i]);
+    for (int k = 0; k < w; ++k) static_cast<double*>(b.p[k])[i] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) fill_f64_kernel(double* p, long long n, double v) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void __launch_bounds__(kThreads) fill_uniform_f64_kernel(double* p, long long n, double scale,
+                                                                    uint64_t seed, uint64_t offset) {
+  for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x * 4) {
+    uint32_t u[4];
+    Philox::gen(seed, offset, static_cast<unsigned long long>(i) >> 2, u);
+    for (int q = 0; q < 4 && i + q < n; ++q) {
+      const double r = (static_cast<double>(u[q]) + 0.5) * (1.0 / 4294967296.0);  // (0,1)
+      p[i + q] = (2.0 * r - 1.0) * scale;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- fills
 template <typename T>
 __global__ void __launch_bounds__(kThreads) fill_uniform_kernel(T* p, long long n, float scale, uint64_t seed,
@@ -362,6 +391,42 @@ __global__ void __launch_bounds__(kThreads) convert_kernel(const S* src, D* dst,
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     dst[i] = from_f<D>(to_f(src[i]));
+}
+
+// ---------------------------------------------------------------- f64 (value-level toy checks)
+// The f64 mode runs the reference's toy checker (numerics.hpp:35-60) through the
+// runtime: no dropout, no LayerNorm; plain scalar kernels in the reference's
+// operation order (numerics.cpp:34-39 add, 175-188 loss head).
+__global__ void __launch_bounds__(kThreads) bdr_f64_kernel(const double* __restrict__ x, const double* __restrict__ bias,
+                                                           const double* __restrict__ res, double* __restrict__ out,
+                                                           long long n, int cols) {
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double v = x[e];
+    if (bias) v = __dadd_rn(v, bias[e % cols]);
+    out[e] = res ? __dadd_rn(res[e], v) : v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) gelu_sq_loss_f64_kernel(const double* __restrict__ z, double* __restrict__ dz,
+                                                                    double* __restrict__ part, long long n) {
+  double acc = 0.0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double v = z[i];
+    const double g = gelu_d(v);
+    acc += 0.5 * g * g;
+    if (dz) dz[i] = __dmul_rn(g, gelu_grad_d(v));
+  }
+  acc = warp_sum(acc);
+  __shared__ double sm[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += sm[w];
+    part[blockIdx.x] = s;
+  }
 }
 
 struct ColSplit {
@@ -429,6 +494,14 @@ cudaError_t bias_dropout_residual_fwd(int dtype, const void* x, const void* bias
   const int drop = p > 0.f;
   const uint32_t thr = dropout_threshold(p);
   const float ks = dropout_keep_scale(p);
+  if (dtype == OASES_F64) {
+    if (drop) return cudaErrorNotSupported;  // the f64 toy mode has no dropout
+    bdr_f64_kernel<<<grid_for(n, kThreads), kThreads, 0, st>>>(static_cast<const double*>(x),
+                                                              static_cast<const double*>(bias),
+                                                              static_cast<const double*>(res),
+                                                              static_cast<double*>(out), n, cols);
+    return cudaGetLastError();
+  }
   if (dtype == OASES_BF16) {
     using T = __nv_bfloat16;
     auto X = static_cast<const T*>(x);
@@ -544,7 +617,9 @@ cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int a
                          cudaStream_t st) {
   unsigned g = grid_for(n, kThreads * 4);
   if (g > 1024) g = 1024;
-  if (dtype == OASES_BF16)
+  if (dtype == OASES_F64)
+    gelu_sq_loss_f64_kernel<<<g, kThreads, 0, st>>>(static_cast<const double*>(z), static_cast<double*>(dz), ws, n);
+  else if (dtype == OASES_BF16)
     launch_pdl(gelu_sq_loss_kernel<__nv_bfloat16>, dim3(g), dim3(kThreads), 0, st, static_cast<const __nv_bfloat16*>(z),
                static_cast<__nv_bfloat16*>(dz), ws, n);
   else
@@ -559,7 +634,8 @@ cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cu
   BufList b{};
   for (int i = 0; i < w; ++i) b.p[i] = bufs[i];
   const unsigned g = grid_for(n, kThreads);
-  if (dtype == OASES_BF16) local_allreduce_kernel<__nv_bfloat16><<<g, kThreads, 0, st>>>(b, w, n);
+  if (dtype == OASES_F64) local_allreduce_f64_kernel<<<g, kThreads, 0, st>>>(b, w, n);
+  else if (dtype == OASES_BF16) local_allreduce_kernel<__nv_bfloat16><<<g, kThreads, 0, st>>>(b, w, n);
   else local_allreduce_kernel<float><<<g, kThreads, 0, st>>>(b, w, n);
   return cudaGetLastError();
 }
@@ -567,7 +643,9 @@ cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cu
 cudaError_t fill_uniform(int dtype, void* p, long long n, float scale, uint64_t seed, uint64_t offset,
                          cudaStream_t st) {
   const unsigned g = grid_for(n, kThreads * 4);
-  if (dtype == OASES_BF16)
+  if (dtype == OASES_F64)
+    fill_uniform_f64_kernel<<<g, kThreads, 0, st>>>(static_cast<double*>(p), n, scale, seed, offset);
+  else if (dtype == OASES_BF16)
     fill_uniform_kernel<<<g, kThreads, 0, st>>>(static_cast<__nv_bfloat16*>(p), n, scale, seed, offset);
   else
     fill_uniform_kernel<<<g, kThreads, 0, st>>>(static_cast<float*>(p), n, scale, seed, offset);
@@ -576,13 +654,18 @@ cudaError_t fill_uniform(int dtype, void* p, long long n, float scale, uint64_t 
 
 cudaError_t fill_const(int dtype, void* p, long long n, float v, cudaStream_t st) {
   const unsigned g = grid_for(n, kThreads);
-  if (dtype == OASES_BF16) fill_const_kernel<<<g, kThreads, 0, st>>>(static_cast<__nv_bfloat16*>(p), n, v);
+  if (dtype == OASES_F64) fill_f64_kernel<<<g, kThreads, 0, st>>>(static_cast<double*>(p), n, v);
+  else if (dtype == OASES_BF16) fill_const_kernel<<<g, kThreads, 0, st>>>(static_cast<__nv_bfloat16*>(p), n, v);
   else fill_const_kernel<<<g, kThreads, 0, st>>>(static_cast<float*>(p), n, v);
   return cudaGetLastError();
 }
 
 cudaError_t convert(int sd, const void* src, int dd, void* dst, long long n, cudaStream_t st) {
   const unsigned g = grid_for(n, kThreads);
+  if (sd == OASES_F64 || dd == OASES_F64) {
+    if (sd != dd) return cudaErrorNotSupported;
+    return cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
   if (sd == OASES_F32 && dd == OASES_BF16)
     convert_kernel<<<g, kThreads, 0, st>>>(static_cast<const float*>(src), static_cast<__nv_bfloat16*>(dst), n);
   else if (sd == OASES_BF16 && dd == OASES_F32)

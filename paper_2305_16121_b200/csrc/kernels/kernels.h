@@ -63,3 +63,13 @@ cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int a
 cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cudaStream_t st);
 
 }  // namespace oases
+
+namespace oases {
+// f64 value-level numerics (numerics_f64.cu; the reference's numerics.hpp:10-60 on the device)
+enum { F64_ADD = 0, F64_HADAMARD = 1, F64_GELU = 2, F64_GELU_GRAD = 3 };
+cudaError_t map_f64(int op, const double* a, const double* b, double* out, long long n, cudaStream_t st);
+cudaError_t transpose_f64(const double* a, double* t, int rows, int cols, cudaStream_t st);
+cudaError_t max_abs_diff_f64(const double* a, const double* b, long long n, double* out, cudaStream_t st);
+cudaError_t grad_identity_fd_f64(const double* x, const double* weights, int workers, int n, double h, double* fd,
+                                 cudaStream_t st);
+}  // namespace oases

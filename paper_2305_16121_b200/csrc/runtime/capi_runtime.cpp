@@ -58,14 +58,24 @@ oases::ModelCfg to_cfg(const oases_model_desc& m) {
 }
 
 tmpsim::SchedulePlan unflatten(const oases_flat_plan& f) {
-  if (f.n_ops < 0 || f.n_forward < 0 || f.n_forward > f.n_ops || (f.n_ops && !f.ops))
+  if (f.n_ops < 0 || f.n_forward < 0 || f.n_forward > f.n_ops || (f.n_ops && !f.ops) || f.n_deps < 0 ||
+      (f.n_deps > 0 && !f.deps))
     throw ConfigError("plan_bind: malformed flat plan");
+  if (f.variant < 0 || f.variant > static_cast<int>(tmpsim::ScheduleVariant::Oases))
+    throw ConfigError("plan_bind: unknown schedule variant " + std::to_string(f.variant));
   tmpsim::SchedulePlan p;
   p.variant = static_cast<tmpsim::ScheduleVariant>(f.variant);
   p.split_batch = f.split_batch != 0;
   p.has_recompute = f.has_recompute != 0;
   for (int i = 0; i < f.n_ops; ++i) {
     const oases_plan_op& o = f.ops[i];
+    // enum and index ranges (the executor indexes per-sub-batch and per-block arrays with them)
+    if (o.kind < 0 || o.kind > static_cast<int>(tmpsim::OpKind::AllGather) || o.pass < 0 ||
+        o.pass > static_cast<int>(tmpsim::Pass::Backward) || o.stream < 0 ||
+        o.stream > static_cast<int>(tmpsim::Stream::Comm))
+      throw ConfigError("plan_bind: op " + std::to_string(i) + " has an out-of-range kind/pass/stream");
+    if (o.sub_batch < 0 || o.sub_batch > 1 || o.block < 0)
+      throw ConfigError("plan_bind: op " + std::to_string(i) + " has sub_batch outside {0,1} or a negative block");
     tmpsim::ScheduledOp op;
     op.id = o.id;
     op.base_id = o.base_id;

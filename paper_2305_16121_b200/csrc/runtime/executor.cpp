@@ -22,6 +22,96 @@ using tmpsim::ConfigError;
 using tmpsim::OpKind;
 using tmpsim::Pass;
 
+namespace {
+
+// validate_plan (schedule.cpp:470-521) accepts graphs with several compute ops
+// per block (custom operator sequences); this executor maps ONE plan op to a
+// block's whole kernel list and shares activation workspaces between blocks, so
+// it also needs:
+//  * exactly one forward, (recompute,) backward compute op per (block, sub-batch)
+//    and at most one comm op per (pass, block, sub-batch);
+//  * the second backward op of a block (which computes the weight gradients over
+//    both sub-batches) directly follows the first among backward computes (the
+//    per-sub-batch gradient scratch is shared by all blocks), and
+//  * every backward op finds its block's forward/recompute activations still in
+//    the workspace slot they were written to (slot = block % 2 with recompute).
+// A plan that breaks these would run and produce wrong gradients, so it is
+// rejected with ConfigError instead.
+void check_buffer_discipline(const tmpsim::SchedulePlan& plan, int nblocks, bool recompute) {
+  const int n = plan.total_ops();
+  const int halves = plan.split_batch ? 2 : 1;
+  std::map<std::tuple<int, int, int>, int> ncomp, ncomm;
+  for (int id = 0; id < n; ++id) {
+    const auto& op = plan.op(id);
+    if (op.block < 0 || op.block >= nblocks) throw ConfigError("plan_bind: op " + std::to_string(id) + " block out of range");
+    if (!plan.split_batch && op.sub_batch != 0)
+      throw ConfigError("plan_bind: unsplit plan with sub_batch != 0 at op " + std::to_string(id));
+    auto key = std::make_tuple(static_cast<int>(op.pass), op.block, op.sub_batch);
+    if (tmpsim::is_comm(op.kind)) {
+      if (++ncomm[key] > 1)
+        throw ConfigError("plan_bind: more than one comm op for (pass, block " + std::to_string(op.block) +
+                          ", sub-batch " + std::to_string(op.sub_batch) + ")");
+    } else if (++ncomp[key] > 1) {
+      throw ConfigError("plan_bind: more than one compute op for (pass, block " + std::to_string(op.block) +
+                        ", sub-batch " + std::to_string(op.sub_batch) + "); the executor runs one kernel list per block");
+    }
+  }
+  std::vector<Pass> passes = {Pass::Forward, Pass::Backward};
+  if (plan.has_recompute) passes.push_back(Pass::Recompute);
+  for (int b = 0; b < nblocks; ++b)
+    for (Pass p : passes)
+      for (int sb = 0; sb < halves; ++sb)
+        if (!ncomp.count(std::make_tuple(static_cast<int>(p), b, sb)))
+          throw ConfigError("plan_bind: block " + std::to_string(b) + " lacks a " + tmpsim::to_string(p) +
+                            " compute op for sub-batch " + std::to_string(sb));
+  // workspace ownership walk in compute-stream issue order
+  std::map<std::pair<int, int>, int> owner;  // (slot, sb) -> block whose activations it holds
+  auto slot = [&](int b) { return recompute ? b % 2 : b; };
+  int prev_b = -1, prev_block = -1;
+  std::vector<int> seen(static_cast<size_t>(nblocks), 0);
+  for (int id = 0; id < n; ++id) {
+    const auto& op = plan.op(id);
+    if (tmpsim::is_comm(op.kind)) continue;
+    if (op.kind == OpKind::ForwardCompute || op.kind == OpKind::RecomputeCompute) {
+      // forward ops of a recompute plan only feed their own row GEMM (the saved x_b is
+      // separate); the recompute op (or, without recompute, the forward) fills the slot
+      if (op.kind == OpKind::RecomputeCompute || !plan.has_recompute)
+        for (int sb = 0; sb < 2; ++sb)
+          if (halves == 2 ? sb == op.sub_batch : true) owner[{slot(op.block), sb}] = op.block;
+      if (op.kind == OpKind::ForwardCompute && plan.has_recompute)
+        for (int sb = 0; sb < 2; ++sb)
+          if (halves == 2 ? sb == op.sub_batch : true) owner[{slot(op.block), sb}] = -1 - op.block;
+      continue;
+    }
+    // backward compute
+    const int b = op.block;
+    const int k = ++seen[static_cast<size_t>(b)];
+    auto holds = [&](int sb) {
+      auto it = owner.find({slot(b), sb});
+      return it != owner.end() && it->second == b;
+    };
+    const bool ok = halves == 1 ? holds(0) && holds(1)
+                                : (k == 1 ? holds(op.sub_batch) : holds(0) && holds(1) && prev_b == id && prev_block == b);
+    if (!ok)
+      throw ConfigError("plan_bind: backward op " + std::to_string(id) + " of block " + std::to_string(b) +
+                        " would read activations or gradient scratch overwritten by another block (the two "
+                        "backward ops of a block must follow each other and their recompute)");
+    // the next backward op must be this block's second one when the plan is split
+    prev_b = -1;
+    prev_block = -1;
+    if (halves == 2 && k == 1) {
+      for (int j = id + 1; j < n; ++j)
+        if (plan.op(j).kind == OpKind::BackwardCompute) {
+          prev_b = j;
+          prev_block = b;
+          break;
+        }
+    }
+  }
+}
+
+}  // namespace
+
 Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stack), plan_(plan) {
   const auto bad = tmpsim::validate_plan(plan);
   if (!bad.empty()) throw ConfigError("plan_bind: invalid plan: " + bad.front().code + ": " + bad.front().detail);
@@ -37,9 +127,10 @@ Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stac
       throw ConfigError("plan_bind: resharding AllGathers (mixed per-block degrees) are not executable yet");
     if (tmpsim::is_comm(op.kind) && op.pass == Pass::Recompute) rec_comm.emplace(op.block, op.sub_batch);
   }
-  if (n > 0 && max_block + 1 != stack.num_blocks())
+  if (max_block + 1 != stack.num_blocks())
     throw ConfigError("plan_bind: plan has " + std::to_string(max_block + 1) + " blocks, stack has " +
                       std::to_string(stack.num_blocks()));
+  check_buffer_discipline(plan, stack.num_blocks(), stack.cfg().recompute);
   // WAR protection: a compute op that writes an AllReduce buffer waits for the
   // last comm op that used the same buffer (the plan's data edges cover RAW).
   std::map<std::tuple<int, int, int>, int> last_comm_on;
@@ -148,7 +239,8 @@ void Executor::issue(bool trace) {
     if (wait >= 0 && ops_[static_cast<size_t>(wait)].stream == 1)
       check_cuda(cudaStreamWaitEvent(c.compute, t1_[static_cast<size_t>(wait)], 0), "wait tail");
     if (trace) check_cuda(cudaEventRecord(t0_[static_cast<size_t>(n + k)], c.compute), "record");
-    for (int w = 0; w < W; ++w) stack_.tail(w, k);
+    if (stack_.num_blocks() > 0)  // an empty stack has no LN_0 to run backward through
+      for (int w = 0; w < W; ++w) stack_.tail(w, k);
     check_cuda(cudaEventRecord(t1_[static_cast<size_t>(n + k)], c.compute), "record");
   }
   check_cuda(cudaEventRecord(fork_, c.comm), "record");

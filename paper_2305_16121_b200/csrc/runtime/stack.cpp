@@ -93,7 +93,19 @@ std::unique_ptr<Context> make_context(const oases_ctx_desc& d) {
 
 // ================================================================== arena
 DeviceArena::~DeviceArena() {
-  for (void* p : blocks_) cudaFree(p);
+  for (auto& b : blocks_) cudaFree(b.first);
+}
+
+void DeviceArena::release(void* p) {
+  if (!p) return;
+  for (size_t i = 0; i < blocks_.size(); ++i)
+    if (blocks_[i].first == p) {
+      check_cuda(cudaFree(p), "cudaFree");
+      total_ -= blocks_[i].second;
+      blocks_.erase(blocks_.begin() + static_cast<std::ptrdiff_t>(i));
+      return;
+    }
+  throw ConfigError("arena: release of a pointer it does not own");
 }
 
 void* DeviceArena::alloc(size_t bytes) {
@@ -102,7 +114,7 @@ void* DeviceArena::alloc(size_t bytes) {
   void* p = nullptr;
   check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
   check_cuda(cudaMemset(p, 0, bytes), "cudaMemset");
-  blocks_.push_back(p);
+  blocks_.emplace_back(p, bytes);
   total_ += bytes;
   return p;
 }
@@ -131,7 +143,11 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
   const int t = ctx.tp;
   if (cfg.h <= 0 || cfg.s <= 0 || cfg.b <= 0 || cfg.layers < 0) throw ConfigError("stack: sizes must be positive");
   if (cfg.b % 2) throw ConfigError("stack: global_batch must be even (two sub-batches)");
-  if (cfg.bytes != 2 && cfg.bytes != 4) throw ConfigError("stack: bytes_per_element must be 2 (bf16) or 4 (f32)");
+  if (cfg.bytes != 2 && cfg.bytes != 4 && cfg.bytes != 8)
+    throw ConfigError("stack: bytes_per_element must be 2 (bf16), 4 (f32) or 8 (f64 value-level toy mode)");
+  if (cfg.bytes == 8 && (cfg.attention || cfg.ln || cfg.p_hidden > 0.f || cfg.p_attn > 0.f))
+    throw ConfigError("stack: f64 mode runs the reference's toy FFN blocks (numerics.hpp:35-60): no attention, "
+                      "LayerNorm or dropout");
   if (cfg.f % t) throw ConfigError("stack: ffn hidden must be divisible by tp");
   if (cfg.attention) {
     if (cfg.heads < 1 || cfg.h % cfg.heads || cfg.heads % t)
@@ -237,7 +253,7 @@ void Stack::alloc_all() {
       for (int p = 0; p < OASES_P_COUNT; ++p) {
         if (!bp.numel[p]) continue;
         bp.p[p] = arena_.alloc(static_cast<size_t>(bp.numel[p]) * es);
-        bp.g[p] = static_cast<float*>(arena_.alloc(static_cast<size_t>(bp.numel[p]) * sizeof(float)));
+        bp.g[p] = static_cast<float*>(arena_.alloc(static_cast<size_t>(bp.numel[p]) * gsize()));
       }
       if (cfg_.ln) {
         check_cuda(fill_const(dtype(), bp.p[OASES_P_LN_GAMMA], h, 1.f, nullptr), "fill gamma");
@@ -304,7 +320,7 @@ void Stack::alloc_all() {
         for (int sb = 0; sb < 2; ++sb)
           w.mask_bits[static_cast<size_t>(b / 2)][static_cast<size_t>(sb)] = static_cast<uint32_t*>(arena_.alloc(mbytes));
     }
-    w.y = arena_.alloc(static_cast<size_t>(Ts * h) * es);
+    w.y = arena_.alloc(static_cast<size_t>(2 * Ts * h) * es);
     // row statistics of both sub-batches (the parameter pass runs once over 2 T_sub rows)
     w.ln_ws = arena_.alloc(layernorm_bwd_workspace(2 * Ts, static_cast<int>(h)));
     w.col_ws = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
@@ -328,6 +344,12 @@ void Stack::bind_storage(const std::vector<bool>& stored) {
   if (static_cast<int>(stored.size()) != nblocks_) throw ConfigError("bind_storage: one flag per block");
   const int64_t T = 2 * tokens_sub(), h = cfg_.h;
   const size_t bytes = static_cast<size_t>(T * h) * esize();
+  // buffers the previous plan needed and this one does not are freed, so the
+  // reported device bytes are those of the bound plan (a rebound stack measures
+  // the same peak_memory as a fresh one)
+  check_cuda(cudaDeviceSynchronize(), "bind_storage sync");
+  bool any_scratch = false;
+  for (int b = 1; b < nblocks_; ++b) any_scratch = any_scratch || !stored[static_cast<size_t>(b)];
   for (Worker& w : workers_) {
     for (int b = 1; b < nblocks_; ++b) {
       auto& own = w.x_own[static_cast<size_t>(b)];
@@ -338,12 +360,20 @@ void Stack::bind_storage(const std::vector<bool>& stored) {
         }
         w.xs[static_cast<size_t>(b)] = own;
       } else {
+        if (own[0]) {
+          arena_.release(own[0]);
+          own = {nullptr, nullptr};
+        }
         if (!w.x_scratch[0]) {
           void* base = arena_.alloc(bytes);
           w.x_scratch = {half(base, 0, h), half(base, 1, h)};
         }
         w.xs[static_cast<size_t>(b)] = w.x_scratch;
       }
+    }
+    if (!any_scratch && w.x_scratch[0]) {
+      arena_.release(w.x_scratch[0]);
+      w.x_scratch = {nullptr, nullptr};
     }
   }
   x_stored_ = stored;
@@ -488,6 +518,18 @@ void Stack::set_param(int worker, int block, int p, const double* host) {
   BlockParams& bp = workers_[static_cast<size_t>(worker)].params[static_cast<size_t>(block)];
   const int64_t n = bp.numel[p];
   if (!n) throw ConfigError("set_param: block has no such parameter");
+  if (dtype() == OASES_F64) {  // value-level toy mode: the host values as they are
+    std::vector<double> d(static_cast<size_t>(n));
+    if (p == OASES_P_W_COL || p == OASES_P_W_ROW) {
+      const int64_t out = bp.rows[p], in = n / out;
+      for (int64_t o = 0; o < out; ++o)
+        for (int64_t i = 0; i < in; ++i) d[static_cast<size_t>(o * in + i)] = host[i * out + o];
+    } else {
+      for (int64_t i = 0; i < n; ++i) d[static_cast<size_t>(i)] = host[i];
+    }
+    check_cuda(cudaMemcpy(bp.p[p], d.data(), static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice), "H2D");
+    return;
+  }
   std::vector<float> f(static_cast<size_t>(n));
   if (p == OASES_P_W_COL || p == OASES_P_W_ROW) {
     const int64_t out = bp.rows[p], in = n / out;  // device [out, in]; host [in, out]
@@ -510,9 +552,15 @@ void Stack::get_grad(int worker, int block, int p, double* host) {
   BlockParams& bp = workers_[static_cast<size_t>(worker)].params[static_cast<size_t>(block)];
   const int64_t n = bp.numel[p];
   if (!n) throw ConfigError("get_grad: block has no such parameter");
-  std::vector<float> f(static_cast<size_t>(n));
+  std::vector<double> f(static_cast<size_t>(n));
   check_cuda(cudaDeviceSynchronize(), "get_grad sync");
-  check_cuda(cudaMemcpy(f.data(), bp.g[p], static_cast<size_t>(n) * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+  if (gdtype() == OASES_F64) {
+    check_cuda(cudaMemcpy(f.data(), bp.g[p], static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost), "D2H");
+  } else {
+    std::vector<float> f32(static_cast<size_t>(n));
+    check_cuda(cudaMemcpy(f32.data(), bp.g[p], static_cast<size_t>(n) * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < n; ++i) f[static_cast<size_t>(i)] = f32[static_cast<size_t>(i)];
+  }
   if (p == OASES_P_W_COL || p == OASES_P_W_ROW) {
     const int64_t out = bp.rows[p], in = n / out;
     for (int64_t o = 0; o < out; ++o)
@@ -556,7 +604,7 @@ void Stack::set_input(const void* host, int host_dtype, cudaStream_t st) {
   std::vector<float> f32;
   std::vector<uint16_t> b16;
   int src_dtype = host_dtype;
-  if (host_dtype == 2) {  // f64 -> activation dtype on the host
+  if (host_dtype == 2 && my != OASES_F64) {  // f64 -> activation dtype on the host
     const double* d = static_cast<const double*>(host);
     if (my == OASES_F32) {
       f32.resize(static_cast<size_t>(n));
@@ -584,7 +632,9 @@ void Stack::set_input(const void* host, int host_dtype, cudaStream_t st) {
 namespace {
 void download(const void* dev, int dtype, int64_t n, double* host) {
   check_cuda(cudaDeviceSynchronize(), "download sync");
-  if (dtype == OASES_F32) {
+  if (dtype == OASES_F64) {
+    check_cuda(cudaMemcpy(host, dev, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost), "D2H");
+  } else if (dtype == OASES_F32) {
     std::vector<float> f(static_cast<size_t>(n));
     check_cuda(cudaMemcpy(f.data(), dev, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost), "D2H");
     for (int64_t i = 0; i < n; ++i) host[i] = f[static_cast<size_t>(i)];
@@ -611,7 +661,7 @@ void Stack::get_activation(int worker, int block, int sb, double* host) {
     throw ConfigError("get_activation: index out of range");
   Worker& w = workers_[static_cast<size_t>(worker)];
   if (block == nblocks_) {
-    download(w.y, dtype(), tokens_sub() * cfg_.h, host);  // final output of the last traced sub-batch
+    download(half(w.y, sb, cfg_.h), dtype(), tokens_sub() * cfg_.h, host);  // x_B, the stack's output
     return;
   }
   download(w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)], dtype(), tokens_sub() * cfg_.h, host);
@@ -893,13 +943,14 @@ void Stack::backward(int wi, int block, int sb) {
   bool gar_done = false;
   if (block == nblocks_ - 1) {
     const BlockParams& bp = w.params[static_cast<size_t>(block)];
+    void* y = half(w.y, sb, h);
     check_cuda(bias_dropout_residual_fwd(dtype(), w.fwd_ar[block % 2][usb], cfg_.bias ? bp.p[OASES_P_B_ROW] : nullptr,
-                                         cfg_.residual ? w.xs[static_cast<size_t>(block)][usb] : nullptr, w.y, Ts, hi,
+                                         cfg_.residual ? w.xs[static_cast<size_t>(block)][usb] : nullptr, y, Ts, hi,
                                          cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0), ctx_.compute),
                "bdr_fwd (loss head)");
     const bool acc = loss_touched_[static_cast<size_t>(wi)];
     loss_touched_[static_cast<size_t>(wi)] = true;
-    check_cuda(gelu_sq_loss(dtype(), w.y, g, w.loss, acc ? 1 : 0, w.loss_ws, Ts * h, ctx_.compute), "loss head");
+    check_cuda(gelu_sq_loss(dtype(), y, g, w.loss, acc ? 1 : 0, w.loss_ws, Ts * h, ctx_.compute), "loss head");
     launches_ += 3;
   } else {
     const BlockParams& nxt = w.params[static_cast<size_t>(block + 1)];
@@ -963,7 +1014,7 @@ void Stack::backward(int wi, int block, int sb) {
   const void* gar_base = gar == gar_sb ? w.gar : w.grad;
   oases_gemm_desc dw{};
   if (wgrad_now) {
-    dw.c_dtype = OASES_F32;
+    dw.c_dtype = gdtype();
     dw.M = h; dw.N = nrow; dw.K = 2 * Ts;
     dw.batch = 1; dw.batch_inner = 1;
     dw.a = operand(gar_base, 2 * Ts, h, h, true);
@@ -1029,7 +1080,7 @@ void Stack::backward(int wi, int block, int sb) {
   const void* ln_base = cfg_.ln ? ws_for(w, block, 0).ln : w.xs[static_cast<size_t>(block)][0];
   dw = oases_gemm_desc{};
   if (wgrad_now) {
-    dw.c_dtype = OASES_F32;
+    dw.c_dtype = gdtype();
     dw.M = ncol; dw.N = h; dw.K = 2 * Ts;
     dw.batch = 1; dw.batch_inner = 1;
     dw.a = operand(w.dcol, 2 * Ts, ncol, ncol, true);

@@ -43,10 +43,11 @@ class DeviceArena {
  public:
   ~DeviceArena();
   void* alloc(size_t bytes);  // 256-byte aligned, zero-initialised
+  void release(void* p);      // frees a block returned by alloc (no-op for nullptr)
   size_t bytes() const { return total_; }
 
  private:
-  std::vector<void*> blocks_;
+  std::vector<std::pair<void*, size_t>> blocks_;
   size_t total_ = 0;
 };
 
@@ -104,7 +105,7 @@ struct Worker {
   // written by the forward's fused bias-dropout-residual + LN of block b+1,
   // read by the backward's fused LN-backward + dropout'
   std::vector<std::array<uint16_t*, 2>> hbits;
-  void* y = nullptr;     // [T_sub, h] final output for the loss head
+  void* y = nullptr;     // [2][T_sub, h] final output x_B (per sub-batch half) for the loss head
   void* ln_ws = nullptr;
   void* col_ws = nullptr;
   void* col_ws2 = nullptr;  // side-stream column sums (bias gradients)
@@ -123,7 +124,10 @@ class Stack {
   int num_blocks() const { return nblocks_; }
   int num_workers() const { return static_cast<int>(workers_.size()); }
   bool is_attention(int b) const { return cfg_.attention && (b % 2 == 0); }
-  int dtype() const { return cfg_.bytes == 2 ? OASES_BF16 : OASES_F32; }
+  int dtype() const { return cfg_.bytes == 2 ? OASES_BF16 : (cfg_.bytes == 8 ? OASES_F64 : OASES_F32); }
+  // gradient dtype: f32 (f64 in the value-level toy mode)
+  int gdtype() const { return cfg_.bytes == 8 ? OASES_F64 : OASES_F32; }
+  size_t gsize() const { return cfg_.bytes == 8 ? 8 : 4; }
   size_t esize() const { return static_cast<size_t>(cfg_.bytes); }
   int64_t tokens_sub() const { return static_cast<int64_t>(cfg_.b / 2) * cfg_.s; }
   int64_t param_numel(int block, int p) const;

@@ -12,11 +12,11 @@
 
 namespace oases {
 
-struct CudaError : std::runtime_error {
-  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+struct CudaError : tmpsim::DeviceError {
+  explicit CudaError(const std::string& w) : tmpsim::DeviceError(w) {}
 };
-struct NcclError : std::runtime_error {
-  explicit NcclError(const std::string& w) : std::runtime_error(w) {}
+struct NcclError : tmpsim::DeviceError {
+  explicit NcclError(const std::string& w) : tmpsim::DeviceError(w) {}
 };
 
 void set_last_error(const std::string& msg);
@@ -46,6 +46,9 @@ oases_status guarded(F&& f) {
   } catch (const NcclError& e) {
     set_last_error(e.what());
     return OASES_ERR_NCCL;
+  } catch (const tmpsim::DeviceError& e) {
+    set_last_error(e.what());
+    return OASES_ERR_CUDA;
   } catch (const std::exception& e) {
     set_last_error(e.what());
     return OASES_ERR_CONFIG;

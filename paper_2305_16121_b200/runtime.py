@@ -222,9 +222,46 @@ class LayerStack:
         """x: host array [batch*seq, hidden]; float64 converted, or a contiguous buffer of the activation dtype."""
         if isinstance(x, np.ndarray) and x.dtype == np.float64:
             a = np.ascontiguousarray(x)
+            self._check_numel(a.size)
             check(capi.lib().oases_stack_set_input(self._h, a.ctypes.data_as(C.c_void_p), 2))
         else:
-            check(capi.lib().oases_stack_set_input(self._h, C.c_void_p(_host_ptr(x)), self._dt()))
+            check(capi.lib().oases_stack_set_input(self._h, C.c_void_p(self._host_ptr(x)), self._dt()))
+
+    def _check_numel(self, n):
+        want = self.cfg.batch * self.cfg.seq * self.cfg.hidden
+        if n != want:
+            raise ValueError(f"input must hold batch*seq*hidden = {want} elements, got {n}")
+
+    def _host_ptr(self, x) -> int:
+        """Pointer of a contiguous HOST buffer in the stack's activation dtype holding exactly
+        batch*seq*hidden elements (the C-ABI copies 2*T_sub*hidden elements from it)."""
+        want = "bf16" if self.cfg.dtype == "bf16" else "f32"
+        try:
+            import torch
+
+            if isinstance(x, torch.Tensor):
+                if x.is_cuda:
+                    raise ValueError("step input must be a host buffer")
+                if not x.is_contiguous():
+                    raise ValueError("input tensor must be contiguous")
+                got = {torch.bfloat16: "bf16", torch.float32: "f32"}.get(x.dtype)
+                if got != want:
+                    raise TypeError(f"input dtype {x.dtype} does not match the stack's {want} activations")
+                self._check_numel(x.numel())
+                return x.data_ptr()
+        except ImportError:
+            pass
+        if isinstance(x, np.ndarray):
+            if not x.flags["C_CONTIGUOUS"]:
+                raise ValueError("input array must be C-contiguous")
+            got = "f32" if x.dtype == np.float32 else ("bf16" if x.dtype == np.uint16 or x.dtype.name == "bfloat16"
+                                                        else x.dtype.name)
+            if got != want:
+                raise TypeError(f"input dtype {x.dtype} does not match the stack's {want} activations "
+                                "(pass float64 to convert, or bf16 bits as uint16)")
+            self._check_numel(x.size)
+            return x.ctypes.data
+        raise TypeError("unsupported input buffer")
 
     def _dt(self):
         return capi.BF16 if self.cfg.dtype == "bf16" else capi.F32
@@ -243,9 +280,10 @@ class LayerStack:
         if input is not None:
             if isinstance(input, np.ndarray) and input.dtype == np.float64:
                 self._in = np.ascontiguousarray(input)
+                self._check_numel(self._in.size)
                 ptr, dt = self._in.ctypes.data_as(C.c_void_p), 2
             else:
-                ptr, dt = C.c_void_p(_host_ptr(input)), self._dt()
+                ptr, dt = C.c_void_p(self._host_ptr(input)), self._dt()
         check(capi.lib().oases_step(self._h, ptr, dt, int(trace), C.byref(r)))
         ev = [(r.events[i].op_id, r.events[i].stream, r.events[i].start, r.events[i].end) for i in range(r.n_events)]
         return StepResult(r.makespan, r.compute_busy_fraction, r.comm_exposed, r.peak_memory, r.loss, ev)
@@ -270,21 +308,6 @@ class LayerStack:
         k = capi.KernelStats()
         check(capi.lib().oases_stack_kernel_stats(self._h, C.byref(k)))
         return {"gemm_ms": k.gemm_ms, "gemm_flops": k.gemm_flops, "gemm_launches": k.gemm_launches}
-
-
-def _host_ptr(x) -> int:
-    try:
-        import torch
-
-        if isinstance(x, torch.Tensor):
-            if x.is_cuda:
-                raise ValueError("step input must be a host buffer")
-            return x.data_ptr()
-    except ImportError:
-        pass
-    if isinstance(x, np.ndarray):
-        return x.ctypes.data
-    raise TypeError("unsupported input buffer")
 
 
 def shard_parameter(param: int, full: np.ndarray, *, tp: int, rank: int, attention: bool, heads: int = 1,
