@@ -10,10 +10,21 @@ PKG     := paper_2305_16121_b200
 SRC     := $(PKG)/csrc
 BUILD   := build
 JSON_INC ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
-NCCL_INC ?= /usr/include
+# NCCL: the build links the same libnccl.so.2 torch loads (the nvidia-nccl wheel,
+# 2.28.x) and records its directory as rpath, so the process has ONE NCCL no
+# matter whether torch or liboases is imported first (the system 2.27 lacks
+# symbols libtorch_cuda needs).
+NCCL_DIR ?= $(shell $(PYTHON) -c "import nvidia.nccl, os; print(list(nvidia.nccl.__path__)[0])" 2>/dev/null)
+ifeq ($(NCCL_DIR),)
+NCCL_INC := /usr/include
+NCCL_LINK := -lnccl
+else
+NCCL_INC := $(NCCL_DIR)/include
+NCCL_LINK := -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_DIR)/lib
+endif
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -ccbin /usr/bin/g++ -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr -Iinclude
-CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(CUDA)/include -I$(JSON_INC)
+NVFLAGS := -ccbin /usr/bin/g++ -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr -Iinclude -I$(NCCL_INC)
+CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(NCCL_INC) -I$(CUDA)/include -I$(JSON_INC)
 
 CU_SRCS  := $(wildcard $(SRC)/kernels/*.cu) $(wildcard $(SRC)/runtime/*.cu)
 CPP_SRCS := $(wildcard $(SRC)/host/*.cpp) $(wildcard $(SRC)/runtime/*.cpp)
@@ -35,7 +46,7 @@ $(BUILD)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/runtime/*.h $(SRC)/host/*.h include
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
-	$(NVCC) -ccbin /usr/bin/g++ -shared $(ARCH) -o $@ $^ -L$(CUDA)/lib64 -lcudart -Xlinker -rpath,$(CUDA)/lib64 -lnccl
+	$(NVCC) -ccbin /usr/bin/g++ -shared $(ARCH) -o $@ $^ -L$(CUDA)/lib64 -lcudart -Xlinker -rpath,$(CUDA)/lib64 $(NCCL_LINK)
 
 $(CORE): $(SRC)/python/bindings.cpp $(LIB) include/oases/tmpsim.hpp include/oases/runtime.hpp
 	$(CXX) -std=c++20 -O2 -shared -fPIC $(PYBIND_INC) -Iinclude -I$(CUDA)/include -I$(JSON_INC) $< -o $@ \

@@ -320,6 +320,13 @@ ElisionCheck recompute_elision_equivalence(const ToyShardedModel& model);
 
 // ------------------------------------------------------------- trace_export.hpp:15-22
 void write_chrome_trace(const SimResult& result, const SchedulePlan& plan, const std::filesystem::path& path);
+void write_svg_timeline(const SimResult& result, const SchedulePlan& plan, const std::filesystem::path& path);
+
+// ------------------------------------------------------------- json_io.hpp:40-43
+// The reference's named hardware presets ("3090", "nvlink-3090", same values)
+// plus "b200" (b200_profile(8), runtime.hpp). Unknown names: ConfigError.
+HardwareProfile preset_profile(const std::string& name);
+std::vector<std::string> preset_profile_names();
 std::string sim_result_to_json_text(const SimResult& result);
 
 }  // namespace tmpsim

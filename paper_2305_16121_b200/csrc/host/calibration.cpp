@@ -42,4 +42,26 @@ HardwareProfile b200_profile(int num_devices, double nvlink_bytes_per_s, double 
   return hp;
 }
 
+// Named presets of the reference (json_io.cpp:160-178: two synthetic 3090
+// clusters, kept value-for-value so configs naming them still load) and this
+// build's B200 node.
+HardwareProfile preset_profile(const std::string& name) {
+  if (name == "b200") return b200_profile(8);
+  HardwareProfile hw;
+  hw.num_devices = 8;
+  hw.memory_capacity = 24LL * 1024 * 1024 * 1024;
+  hw.compute_throughput = 1.4e13;
+  hw.candidate_degrees = {2, 4, 8};
+  hw.latency_by_group = {{2, 5e-6}, {4, 1e-5}, {8, 2e-5}};
+  if (name == "nvlink-3090")
+    hw.bandwidth_by_group = {{2, 2.0e10}, {4, 1.7e9}, {8, 1.2e9}};
+  else if (name == "3090")
+    hw.bandwidth_by_group = {{2, 5.0e9}, {4, 4.2e9}, {8, 3.0e9}};
+  else
+    throw ConfigError("unknown hardware preset '" + name + "' (have: 3090, nvlink-3090, b200)");
+  return hw;
+}
+
+std::vector<std::string> preset_profile_names() { return {"3090", "nvlink-3090", "b200"}; }
+
 }  // namespace tmpsim

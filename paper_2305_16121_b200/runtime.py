@@ -44,7 +44,7 @@ class ModelConfig:
     batch: int            # micro-batch, split into two sub-batches
     layers: int
     ffn: int = 0          # 0 -> 4*hidden
-    dtype: str = "bf16"   # "bf16" | "f32"
+    dtype: str = "bf16"   # "bf16" | "f32" | "f64" (the reference's toy FFN blocks only)
     recompute: bool = True
     attention: bool = True
     layernorm: bool = True
@@ -61,7 +61,7 @@ class ModelConfig:
 
     @property
     def bytes_per_element(self):
-        return 2 if self.dtype == "bf16" else 4
+        return {"bf16": 2, "f32": 4, "f64": 8}[self.dtype]
 
     @property
     def num_blocks(self):
@@ -235,7 +235,7 @@ class LayerStack:
     def _host_ptr(self, x) -> int:
         """Pointer of a contiguous HOST buffer in the stack's activation dtype holding exactly
         batch*seq*hidden elements (the C-ABI copies 2*T_sub*hidden elements from it)."""
-        want = "bf16" if self.cfg.dtype == "bf16" else "f32"
+        want = self.cfg.dtype
         try:
             import torch
 
@@ -244,7 +244,7 @@ class LayerStack:
                     raise ValueError("step input must be a host buffer")
                 if not x.is_contiguous():
                     raise ValueError("input tensor must be contiguous")
-                got = {torch.bfloat16: "bf16", torch.float32: "f32"}.get(x.dtype)
+                got = {torch.bfloat16: "bf16", torch.float32: "f32", torch.float64: "f64"}.get(x.dtype)
                 if got != want:
                     raise TypeError(f"input dtype {x.dtype} does not match the stack's {want} activations")
                 self._check_numel(x.numel())
@@ -254,8 +254,8 @@ class LayerStack:
         if isinstance(x, np.ndarray):
             if not x.flags["C_CONTIGUOUS"]:
                 raise ValueError("input array must be C-contiguous")
-            got = "f32" if x.dtype == np.float32 else ("bf16" if x.dtype == np.uint16 or x.dtype.name == "bfloat16"
-                                                        else x.dtype.name)
+            got = {"float32": "f32", "float64": "f64", "uint16": "bf16", "bfloat16": "bf16"}.get(x.dtype.name,
+                                                                                                x.dtype.name)
             if got != want:
                 raise TypeError(f"input dtype {x.dtype} does not match the stack's {want} activations "
                                 "(pass float64 to convert, or bf16 bits as uint16)")
@@ -264,7 +264,7 @@ class LayerStack:
         raise TypeError("unsupported input buffer")
 
     def _dt(self):
-        return capi.BF16 if self.cfg.dtype == "bf16" else capi.F32
+        return {"bf16": capi.BF16, "f32": capi.F32, "f64": 2}[self.cfg.dtype]
 
     def bind(self, plan):
         self._flat = _FlatPlan(plan)

@@ -10,6 +10,11 @@ Fixtures:
   sim_cases.json      simulate() on random measured-cost tables (load_measured_costs)
   planner_cases.json  node_cost / edge costs / objective / memory / solve / brute_force
   misc.json           volumes, comm_time, spearman, run_length_notation, cost vectors
+  reference_smoke_test.py.txt  the reference's own Python smoke test, byte for byte
+                      (proj/tests/python/smoke_test.py; its sha256 in
+                      reference_smoke_test.sha256) -- run against this build's
+                      module under the name `tmpsim` by tests/test_numerics_gpu.py,
+                      because /root/reference does not exist on the GPU box
 """
 import json
 import os
@@ -237,7 +242,21 @@ def make_misc():
         json.dump(misc, f, separators=(",", ":"))
 
 
+def make_smoke_fixture():
+    import hashlib
+    import shutil
+
+    src = "/root/reference/proj/tests/python/smoke_test.py"
+    dst = os.path.join(HERE, "reference_smoke_test.py.txt")  # .txt: never collected by pytest
+    shutil.copyfile(src, dst)
+    with open(src, "rb") as f:
+        digest = hashlib.sha256(f.read()).hexdigest()
+    with open(os.path.join(HERE, "reference_smoke_test.sha256"), "w") as f:
+        f.write(digest + "  proj/tests/python/smoke_test.py\n")
+
+
 if __name__ == "__main__":
+    make_smoke_fixture()
     make_toys()
     make_plans()
     make_sim_cases()

@@ -209,9 +209,10 @@ def test_misc_matches_reference():
             assert t.memory_usage(c, S) == mem
 
 
-def test_reference_python_smoke_runs_unchanged():
-    """proj/tests/python/smoke_test.py:30-107 against this module (minus the toy numerics,
-    which live in the fp64 oracle and the GPU stack)."""
+def test_reference_python_smoke_host_subset():
+    """The host (schedule / simulate / planner) half of proj/tests/python/smoke_test.py on CPU.
+    The whole file runs byte-for-byte, value-level GPU checks included, in
+    tests/test_numerics_gpu.py::test_reference_smoke_test_verbatim."""
     spec_ = t.ModelSpec()
     spec_.hidden_size, spec_.num_layers, spec_.seq_len, spec_.attention_heads = 256, 2, 64, 4
     spec_.global_batch, spec_.bytes_per_element, spec_.recompute_enabled = 4, 2, True
@@ -265,3 +266,32 @@ def test_measured_rows_roundtrip(tmp_path):
     bad.field = "nope"
     with pytest.raises(t.ConfigError):
         t.write_measured_costs([bad], str(path))
+
+
+def test_smoke_fixture_is_the_reference_file():
+    """tests/golden/reference_smoke_test.py.txt is the reference's smoke test byte for byte."""
+    import hashlib
+
+    g = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    data = open(os.path.join(g, "reference_smoke_test.py.txt"), "rb").read()
+    want = open(os.path.join(g, "reference_smoke_test.sha256")).read().split()[0]
+    assert hashlib.sha256(data).hexdigest() == want
+    ref = "/root/reference/proj/tests/python/smoke_test.py"
+    if os.path.exists(ref):
+        assert open(ref, "rb").read() == data
+
+
+def test_value_api_fails_loudly_without_a_device():
+    """No CPU fallback: the value-level numerics raise DeviceError when no GPU is present."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    for call in (lambda: t.matmul(t.Matrix(2, 2), t.Matrix(2, 2)),
+                 lambda: t.recompute_elision_equivalence(t.make_toy_sharded_model(2, 4, 6, 8, 7)),
+                 lambda: t.allreduce_grad_identity(2, 4, 4, 1)):
+        with pytest.raises(t.DeviceError):
+            call()
+    assert t.make_toy_sharded_model(2, 4, 6, 8, 7).workers == 2  # input generation is host-side
+    with pytest.raises(t.ConfigError):
+        t.preset_profile("nope")
+    assert set(t.preset_profile_names()) >= {"3090", "nvlink-3090"}
