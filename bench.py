@@ -15,10 +15,18 @@ each device-timed with cudaEvents on the compute stream inside the library
 (2.4 GB of weights, 1.6 GB of saved activations) exceeds the 126 MB L2, so no
 explicit flush is needed. `e2e` re-times the same step through the public
 API with the input batch copied from pinned host memory every step and the
-loss read back. `roofline` uses live cudaEvent timings of every linear-layer
-GEMM launch of one extra step. `cpu_baseline` times the reference's own CPU
-implementation of the path (oracle/_ref/ref_bench, built from /root/reference)
-on a bounded sample.
+loss read back. `roofline` uses cudaEvent timings of every linear-layer GEMM
+launch inside a replay of the captured step. `cpu_baseline` (and the
+`--impl reference` arm, one sample per step) runs the fp64 full-layer CPU
+restatement on a bounded sample of the configured workload with every host
+core, plus the reference's own toy checker (oracle/_ref, built from
+/root/reference) per call at its shipped sizes.
+
+`--gpus N` outside torchrun re-executes itself under torch.distributed.run with
+N ranks. Extras (skip with --no-extras): at N=1 one rank of the north-star
+config C3 at TMP=8 (`c3_tp8`, collectives disabled) and TMP=2 emulated
+in-process (`emulated_tp2_exposure`, real comm-stream AllReduce kernels); at
+N=8 the C3 config itself at TMP=8 over NCCL.
 """
 import argparse
 import json
@@ -106,37 +114,58 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(cfg, seconds=12.0):
-    """The reference's own CPU path (tmpsim::recompute_elision_equivalence) on the host cores."""
-    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
-    threads = os.cpu_count() or 1
-    rows = 16  # one reference call ~ 3.8 GMAC at C2 widths: a few seconds per sample
-    h, f = cfg["hidden"], 4 * cfg["hidden"]
-    macs_per_sample = step_flops(cfg) / 2.0 / cfg["batch"]
-    if os.path.exists(exe):
-        out = subprocess.check_output([exe, "1", str(rows), str(h), str(f), str(seconds), str(threads)], text=True)
-        r = json.loads(out)
-        return {"value": r["macs_per_s"] / macs_per_sample, "unit": "samples/s", "cores": threads,
-                "kind": "reference",
-                "sample": (f"reference toy FFN checker (recompute_elision_equivalence, numerics.cpp:234) "
-                           f"{rows} tokens x h{h} x ffn{f}, {threads} independent threads for {r['seconds']:.1f} s; "
-                           f"{r['macs_per_s'] / 1e9:.2f} GMAC/s scaled by the step's MAC count"),
-                "macs_per_s": r["macs_per_s"]}
-    # fallback: the fp64 oracle port (full layer) on a small sample
+def oracle_sample(cfg, sample_batch=2, threads=None):
+    """One bounded sample of the configured workload on the host cores: the fp64
+    full-layer restatement (oracle/gpt_oracle.cpp, OpenMP on every host core)
+    running `sample_batch` sequences of the config's shape through ONE of its
+    identical layers, forward + backward. The stack's step is `layers` such
+    layers, so the sample is 1/layers of the per-layer work of `sample_batch`
+    samples: samples/s = sample_batch / layers / seconds."""
     from oracle.oracle import LayerCfg, Oracle
 
-    c = LayerCfg(hidden=256, heads=2, seq=128, batch=2, layers=1)
+    threads = threads or os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    c = LayerCfg(hidden=cfg["hidden"], heads=cfg["heads"], seq=cfg["seq"], batch=sample_batch, layers=1,
+                 hidden_dropout=0.1, attention_dropout=0.1)
     o = Oracle(c)
-    o.init_params(1)
-    t0 = time.time()
-    n = 0
-    while time.time() - t0 < seconds:
-        o.run()
-        n += 1
-    dt = time.time() - t0
-    sample_macs = step_flops(dict(hidden=256, heads=2, seq=128, batch=2, layers=1), "CrossPass") / 2.0 * 0.75
-    return {"value": n * sample_macs / dt / macs_per_sample, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": "fp64 oracle full layer h256 s128 b2, scaled by MAC count"}
+    o.init_params(1, extras=True)
+    t0 = time.perf_counter()
+    o.run()
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "value": sample_batch / cfg["layers"] / dt, "unit": "samples/s", "cores": threads,
+            "kind": "port",
+            "sample": (f"fp64 full-layer restatement (oracle/gpt_oracle.cpp; LN, causal attention, GeLU FFN, "
+                       f"bias-dropout-residual, dropout 0.1): {sample_batch} sequences x s{cfg['seq']} x "
+                       f"h{cfg['hidden']} through 1 of the {cfg['layers']} identical layers, fwd+bwd, "
+                       f"{threads} OpenMP threads, {dt:.2f} s measured; value = {sample_batch}/{cfg['layers']} "
+                       f"samples / time")}
+
+
+def reference_toy_calls(threads=1, seconds=1.0):
+    """The reference's own CPU implementation of the path (tmpsim::recompute_elision_equivalence,
+    proj/src/numerics.cpp:234-256, built from /root/reference into oracle/_ref) timed per call
+    at its shipped sizes (main.cpp:236-240 verify-numerics (w,4,6,8w)) and at the FFN-only
+    scaled shape of BASELINE.md 5.2 (256x256x1024), single-threaded."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return {"error": "oracle/_ref/ref_bench not built"}
+    out = {}
+    for name, (w, rows, d, h) in {"toy_w2_4x6x16": (2, 4, 6, 16), "toy_w4_4x6x32": (4, 4, 6, 32),
+                                  "ffn_256x256x1024": (2, 256, 256, 1024)}.items():
+        r = json.loads(subprocess.check_output([exe, str(w), str(rows), str(d), str(h), str(seconds), str(threads)],
+                                               text=True))
+        out[name] = {"us_per_call": r["seconds"] / r["calls"] * 1e6, "gmac_per_s": r["macs_per_s"] / 1e9,
+                     "threads": threads}
+    return out
+
+
+def cpu_baseline(cfg):
+    cb = oracle_sample(cfg)
+    try:
+        cb["reference_toy"] = reference_toy_calls()
+    except Exception as e:  # noqa: BLE001
+        cb["reference_toy"] = {"error": str(e)}
+    return cb
 
 
 def load_traffic():
@@ -151,25 +180,100 @@ def load_traffic():
 
 
 def run_reference(args, cfg):
+    """Reference arm: the CPU implementation of the path on the host cores, one bounded
+    sample of the configured workload per step (rank 0 only under torchrun)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline(cfg, seconds=args.ref_seconds))
-    timed = vals[args.warmup:]
-    v = statistics.mean(x["value"] for x in timed)
+    samples = [oracle_sample(cfg, args.ref_batch) for _ in range(args.warmup + args.steps)]
+    timed = samples[args.warmup:]
+    secs = [x["seconds"] for x in timed]
+    v = args.ref_batch / cfg["layers"] / statistics.mean(secs)
     cb = dict(timed[-1])
     cb["value"] = v
+    try:
+        cb["reference_toy"] = reference_toy_calls()
+    except Exception as e:  # noqa: BLE001
+        cb["reference_toy"] = {"error": str(e)}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cfg["batch"] / v * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(secs) * 1e3,
+            "ms_per_step_sd": statistics.pstdev(secs) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (mt19937 U(-1,1) inputs, numerics.cpp:136-154 init)",
-            "config": dict(workload=f"{args.config} GPT layer stack, reference CPU numerics", **cfg,
-                           parallelism=f"tp{args.gpus}"),
+            "data": "synthetic (mt19937 U(-1,1) input, U(+-1/sqrt(fan_in)) weights, numerics.cpp:136-154 conventions)",
+            "config": dict(workload=(f"{args.config} GPT layer stack on the host CPU: each step = {args.ref_batch} "
+                                     f"sequences through 1 of {cfg['layers']} identical layers (fwd+bwd, fp64)"),
+                           **cfg, parallelism="host OpenMP"),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun re-executes itself as N ranks (one per GPU)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    if os.environ.get("OASES_BENCH_PRINT_LAUNCH"):
+        print(json.dumps({"launch": cmd}), flush=True)
+        return
+    os.execv(sys.executable, cmd)
+
+
+def c3_rank_slice(steps=10, warmup=3):
+    """One TMP rank of the north-star config C3 at TMP=8 (h4096, 32 heads, s2048, b8,
+    24 layers; per rank QKV N=1536, proj K=512, 4 heads), collectives disabled: the
+    compute side of that rank's step on this GPU."""
+    from paper_2305_16121_b200.runtime import Context, LayerStack, ModelConfig, plan_for
+
+    cfg = dict(CONFIGS["c3"])
+    mc = ModelConfig(dtype="bf16", hidden_dropout=0.1, attention_dropout=0.1, **cfg)
+    ctx = Context(tp=8, comm_disabled=True)
+    st = LayerStack(ctx, mc)
+    st.init_random(1234)
+    st.bind(plan_for(mc, "Oases"))
+    st.capture_graph()
+    for _ in range(warmup):
+        st.step(trace=False)
+    ms = [st.step(trace=False).makespan * 1e3 for _ in range(steps)]
+    mem = st.step(trace=True).peak_memory
+    st.close()
+    ctx.close()
+    t = statistics.mean(ms)
+    tf = step_flops(cfg) / 8 / (t * 1e-3) / 1e12
+    return {"config": "c3 (h4096 a32 s2048 b8 L24), one rank of TMP=8, collectives disabled", "ms_per_step": t,
+            "ms_per_step_sd": statistics.pstdev(ms), "tflops": tf,
+            "frac_of_sustained_peak": tf / PEAKS["bf16_tflops_sustained"], "peak_memory_bytes": mem}
+
+
+def emulated_tp2(cfg, layers=4, steps=5):
+    """TMP=2 emulated in-process on this GPU (local_workers=2): both ranks' kernels on the
+    compute stream, the worker-order AllReduce kernel on the comm stream, so the exposed-
+    communication accounting (exposed_comm_time on cudaEvent intervals) runs on real comm-
+    stream work. Not a multi-GPU number: the two ranks share one GPU."""
+    from paper_2305_16121_b200.runtime import Context, LayerStack, ModelConfig, plan_for
+
+    c = dict(cfg, layers=layers)
+    mc = ModelConfig(dtype="bf16", hidden_dropout=0.1, attention_dropout=0.1, **c)
+    out = {}
+    for variant in ("Oases", "CrossPass", "Default"):
+        ctx = Context(tp=2, local_workers=2)
+        st = LayerStack(ctx, mc)
+        st.init_random(1234)
+        st.bind(plan_for(mc, variant))
+        st.step(trace=True)
+        rs = [st.step(trace=True) for _ in range(steps)]
+        out[variant] = {"makespan_ms": statistics.mean(r.makespan for r in rs) * 1e3,
+                        "comm_exposed_ms": statistics.mean(r.comm_exposed for r in rs) * 1e3,
+                        "exposed_comm_pct": 100.0 * statistics.mean(r.comm_exposed / r.makespan for r in rs),
+                        "comm_ops": sum(1 for e in rs[-1].events if e[1] == 1)}
+        st.close()
+        ctx.close()
+    return {"config": f"{c['hidden']}h s{c['seq']} b{c['batch']} L{layers}, TMP=2 as 2 in-process workers",
+            "variants": out}
 
 
 def main():
@@ -184,7 +288,8 @@ def main():
     ap.add_argument("--dropout", type=float, default=0.1)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-seconds", type=float, default=3.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the C3 line and the emulated-TP2 exposure")
+    ap.add_argument("--ref-batch", type=int, default=2, help="sequences per reference-arm sample")
     ap.add_argument("--trace-out", default="")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -192,15 +297,20 @@ def main():
         cfg["layers"] = args.layers
     if args.warmup < 3:
         args.warmup = 3
+    world_env = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and world_env is None:
+        return self_launch(args)  # one process per GPU
+    world = int(world_env or "1")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or omit WORLD_SIZE to self-launch")
 
-    import numpy as np
     import torch
 
     from paper_2305_16121_b200.runtime import Context, LayerStack, ModelConfig, plan_for, unique_id
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -234,29 +344,34 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    launches0 = stack.kernel_launches()
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
     for _ in range(args.warmup):
         stack.step(trace=False)
     barrier()
+    launches0 = stack.kernel_launches()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         dev = [stack.step(trace=False).makespan for _ in range(args.steps)]
         wall = time.perf_counter() - t0
     barrier()
-    total = sum(dev)
-    if dist:
-        t = torch.tensor([total], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total = t.item()
+    # our kernels launched inside the timed region: counted by the library per issued
+    # launch (a graph replay issues the kernels its capture counted once)
+    launched = stack.kernel_launches() - launches0
+    total = max_over_ranks(sum(dev))
     ms_per_step = total / args.steps * 1e3
     value = mc.batch / (total / args.steps)
-    # kernels launched by our library inside the timed region (graph replays issue the same kernels)
-    per_step_launches = (stack.kernel_launches() - launches0) / max(1, args.warmup) if args.no_graph else None
 
     # one traced step: measured SimResult (exposed comm, compute busy)
     traced = stack.step(trace=True)
-    launches_per_step = per_step_launches or 0
-    if not launches_per_step:
+    if args.no_graph:
+        launches_per_step = launched / args.steps
+    else:
         before = stack.kernel_launches()
         stack.step(trace=True)
         launches_per_step = stack.kernel_launches() - before
@@ -264,11 +379,14 @@ def main():
         import paper_2305_16121_b200.tmpsim as tm
 
         tm.write_chrome_trace(traced.sim_result(), plan, args.trace_out)
-    # live GEMM timings for the roofline (one eager step with per-launch events)
-    stack.set_kernel_timing(True)
-    stack.step(trace=True)  # eager issue (graph replays bypass the per-launch events)
-    ks = stack.kernel_stats()
-    stack.set_kernel_timing(False)
+        tm.write_svg_timeline(traced.sim_result(), plan, os.path.splitext(args.trace_out)[0] + ".svg")
+    # live GEMM timings for the roofline, measured inside a replay of the captured step
+    ks = stack.graph_kernel_stats() if not args.no_graph else None
+    if ks is None:
+        stack.set_kernel_timing(True)
+        stack.step(trace=True)
+        ks = stack.kernel_stats()
+        stack.set_kernel_timing(False)
 
     # e2e: public API with the input copied from pinned host memory + loss read back every step
     T = mc.batch * mc.seq
@@ -278,13 +396,20 @@ def main():
     for _ in range(args.steps):
         stack.step(input=host_in, trace=False)
     barrier()
-    e2e_wall = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_wall], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_wall = t.item()
+    e2e_wall = max_over_ranks(time.perf_counter() - t0)
     e2e = {"value": mc.batch * args.steps / e2e_wall, "unit": "samples/s",
            "h2d_bytes_per_step": T * mc.hidden * 2, "d2h_bytes_per_step": 8}
+    stack.close()
+    ctx.close()
+
+    # the north-star config at the target degree: real TMP=8 on 8 GPUs, else one rank's slice
+    c3 = None
+    if not args.no_extras and args.config == "c2":
+        if tp == 8:
+            c3 = c3_full_tp8(dist, rank, local, uid_fn=unique_id, reserve=reserve, sms=sms, steps=args.steps)
+        elif tp == 1 and rank == 0:
+            c3 = c3_rank_slice()
+    emu = emulated_tp2(cfg) if (not args.no_extras and tp == 1 and rank == 0) else None
 
     if rank != 0:
         if dist:
@@ -296,8 +421,8 @@ def main():
     step_tf = step_flops(cfg, args.variant) / tp / (total / args.steps) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "ms_per_step_sd": statistics.pstdev(dev) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (device Philox U(-1,1) input, U(+-1/sqrt(fan_in)) weights, numerics.cpp conventions)",
         "config": {"workload": f"{args.config}: GPT layer stack h{cfg['hidden']} a{cfg['heads']} s{cfg['seq']} "
                                f"b{cfg['batch']} L{cfg['layers']}, TMP={tp}, {args.variant} schedule",
@@ -312,15 +437,21 @@ def main():
                          "peak_memory_bytes": traced.peak_memory},
         "step_tflops_per_gpu": step_tf,
         "step_roofline_frac": step_tf / peak,
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 linear-layer GEMMs, all launches of a step)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "gemm_tc (tcgen05 linear-layer GEMMs, all launches of one graph-replayed step)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else 0,
                      "peak_source": f"{PEAKS['source']} bf16_tflops_sustained",
-                     "gemm_launches": ks["gemm_launches"], "traffic": traffic},
-        "gpu_launches": int(launches_per_step * args.steps),
+                     "gemm_launches": ks["gemm_launches"], "traffic": traffic,
+                     "traffic_source": "ncu --set full capture of the FC1 forward GEMM (profiles/ncu_summary.json)"},
+        "gpu_launches": int(round(launches_per_step * args.steps)),
         "clocks": clk.summary(),
         "wall_s_timed": wall,
         "e2e": e2e,
     }
+    if c3:
+        line["c3_tp8"] = c3
+    if emu:
+        line["emulated_tp2_exposure"] = emu
     if not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg)
@@ -329,7 +460,40 @@ def main():
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-    del np
+
+
+def c3_full_tp8(dist, rank, local, uid_fn, reserve, sms, steps=10, warmup=3):
+    """C3 (h4096, 32 heads, s2048, b8, 24 layers) at TMP=8 over NCCL, Oases plan: the
+    north-star target, measured when the bench runs on 8 GPUs."""
+    from paper_2305_16121_b200.runtime import Context, LayerStack, ModelConfig, plan_for
+    import torch
+
+    cfg = dict(CONFIGS["c3"])
+    obj = [uid_fn() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    mc = ModelConfig(dtype="bf16", hidden_dropout=0.1, attention_dropout=0.1, **cfg)
+    ctx = Context(tp=8, rank=rank, device=local, unique_id=obj[0], nccl_max_ctas=reserve,
+                  gemm_max_ctas=(sms - reserve) // 2 * 2)
+    st = LayerStack(ctx, mc)
+    st.init_random(1234)
+    st.bind(plan_for(mc, "Oases"))
+    st.capture_graph()
+    for _ in range(warmup):
+        st.step(trace=False)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = [st.step(trace=False).makespan * 1e3 for _ in range(steps)]
+    t = torch.tensor([sum(ms)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tr = st.step(trace=True)
+    st.close()
+    ctx.close()
+    mean = t.item() / steps
+    tf = step_flops(cfg) / 8 / (mean * 1e-3) / 1e12
+    return {"config": "c3 (h4096 a32 s2048 b8 L24), TMP=8 over NCCL", "value": cfg["batch"] / (mean * 1e-3),
+            "unit": "samples/s", "ms_per_step": mean, "tflops_per_gpu": tf,
+            "frac_of_sustained_peak": tf / PEAKS["bf16_tflops_sustained"],
+            "exposed_comm_pct": 100.0 * tr.comm_exposed / tr.makespan if tr.makespan else 0.0}
 
 
 if __name__ == "__main__":

@@ -385,6 +385,10 @@ typedef struct {
 } oases_kernel_stats;
 oases_status oases_stack_set_kernel_timing(oases_stack* s, int on);
 oases_status oases_stack_kernel_stats(oases_stack* s, oases_kernel_stats* out);
+/* The same GEMM statistics measured inside a replay of the captured step: the
+ * timing events become graph nodes of a separately captured copy of the step,
+ * which is replayed twice; the second replay's timings are returned. */
+oases_status oases_stack_graph_kernel_stats(oases_stack* s, oases_kernel_stats* out);
 
 #ifdef __cplusplus
 }

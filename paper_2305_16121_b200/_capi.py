@@ -245,6 +245,7 @@ _SIGNATURES = [
     ("oases_stack_kernel_launches", C.c_int, [C.c_void_p]),
     ("oases_stack_set_kernel_timing", C.c_int, [C.c_void_p, C.c_int]),
     ("oases_stack_kernel_stats", C.c_int, [C.c_void_p, C.POINTER(KernelStats)]),
+    ("oases_stack_graph_kernel_stats", C.c_int, [C.c_void_p, C.POINTER(KernelStats)]),
 ]
 
 SYMBOLS = [name for name, _, _ in _SIGNATURES]

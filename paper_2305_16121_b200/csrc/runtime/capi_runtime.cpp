@@ -241,6 +241,20 @@ oases_status oases_stack_kernel_stats(oases_stack* s, oases_kernel_stats* out) {
   });
 }
 
+oases_status oases_stack_graph_kernel_stats(oases_stack* s, oases_kernel_stats* out) {
+  return guarded([&] {
+    if (!out) throw ConfigError("null output");
+    S(s);
+    if (!s->exec) throw ConfigError("graph_kernel_stats: no plan bound");
+    s->exec->timed_graph_replay();
+    std::memset(out, 0, sizeof(*out));
+    int n = 0;
+    S(s).kernel_stats(&out->gemm_ms, &out->gemm_flops, &n);
+    out->gemm_launches = n;
+    S(s).reset_kernel_stats();
+  });
+}
+
 int oases_stack_kernel_launches(const oases_stack* s) {
   return (s && s->stack) ? static_cast<int>(s->stack->kernel_launches()) : 0;
 }

@@ -270,6 +270,32 @@ bool Executor::capture_graph() {
   return true;
 }
 
+void Executor::timed_graph_replay() {
+  Context& c = stack_.ctx();
+  check_cuda(cudaStreamSynchronize(c.compute), "sync");
+  stack_.set_kernel_timing(true);
+  stack_.reset_kernel_stats();
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  check_cuda(cudaStreamBeginCapture(c.compute, cudaStreamCaptureModeRelaxed), "begin capture");
+  try {
+    issue(false);
+  } catch (...) {
+    cudaStreamEndCapture(c.compute, &g);
+    if (g) cudaGraphDestroy(g);
+    stack_.set_kernel_timing(false);
+    throw;
+  }
+  stack_.set_kernel_timing(false);
+  check_cuda(cudaStreamEndCapture(c.compute, &g), "end capture");
+  check_cuda(cudaGraphInstantiateWithFlags(&ge, g, static_cast<unsigned long long>(cudaGraphInstantiateFlagUseNodePriority)),
+             "instantiate");
+  for (int rep = 0; rep < 2; ++rep) check_cuda(cudaGraphLaunch(ge, c.compute), "graph launch");
+  check_cuda(cudaStreamSynchronize(c.compute), "sync");
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+}
+
 tmpsim::SimResult Executor::step(bool trace) {
   Context& c = stack_.ctx();
   tmpsim::SimResult r;

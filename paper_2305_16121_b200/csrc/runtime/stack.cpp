@@ -400,6 +400,17 @@ void Stack::begin_step() {
   std::fill(loss_touched_.begin(), loss_touched_.end(), false);
 }
 
+// GEMM timing events: plain records when issued eagerly; external event-record
+// nodes when the step is being captured (graph_kernel_stats), so a replay of the
+// captured step re-records them.
+cudaError_t Stack::record_timing(cudaEvent_t e) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const cudaError_t q = cudaStreamIsCapturing(ctx_.compute, &cs);
+  if (q != cudaSuccess) return q;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, ctx_.compute, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, ctx_.compute);
+}
+
 void Stack::gemm(const oases_gemm_desc& d0) {
   oases_gemm_desc d = d0;
   d.dtype = dtype();
@@ -413,7 +424,7 @@ void Stack::gemm(const oases_gemm_desc& d0) {
     }
     if (tflops_.size() < timed_ + 1) tflops_.resize(timed_ + 1);
     tflops_[timed_] = 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K);
-    check_cuda(cudaEventRecord(tev_[2 * timed_], ctx_.compute), "record");
+    check_cuda(record_timing(tev_[2 * timed_]), "record");
   }
   GemmStatus st = d.dtype == OASES_BF16 ? gemm_tc(d, ctx_.compute) : gemm_simt(d, ctx_.compute);
   if (!st.ok) {
@@ -421,7 +432,7 @@ void Stack::gemm(const oases_gemm_desc& d0) {
     throw ConfigError(st.err);
   }
   if (timed) {
-    check_cuda(cudaEventRecord(tev_[2 * timed_ + 1], ctx_.compute), "record");
+    check_cuda(record_timing(tev_[2 * timed_ + 1]), "record");
     ++timed_;
   }
   ++launches_;
@@ -451,7 +462,7 @@ void Stack::gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1) {
     tflops_[timed_] = 0.0;
     for (const auto& x : d)
       tflops_[timed_] += 2.0 * static_cast<double>(x.M) * static_cast<double>(x.N) * static_cast<double>(x.K);
-    check_cuda(cudaEventRecord(tev_[2 * timed_], ctx_.compute), "record");
+    check_cuda(record_timing(tev_[2 * timed_]), "record");
   }
   GemmStatus st = gemm_tc_group(d, 2, ctx_.compute);
   if (!st.ok) {
@@ -459,7 +470,7 @@ void Stack::gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1) {
     throw ConfigError(st.err);
   }
   if (timed) {
-    check_cuda(cudaEventRecord(tev_[2 * timed_ + 1], ctx_.compute), "record");
+    check_cuda(record_timing(tev_[2 * timed_ + 1]), "record");
     ++timed_;
   }
   launches_ += 1;

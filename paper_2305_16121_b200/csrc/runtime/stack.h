@@ -166,6 +166,7 @@ class Stack {
  private:
   void alloc_all();
   void gemm(const oases_gemm_desc& d);
+  cudaError_t record_timing(cudaEvent_t e);
   void gemm2(const oases_gemm_desc& d0, const oases_gemm_desc& d1);
   void fork_side();  // side stream waits for the compute stream's current tail
   void join_side();  // compute stream waits for the side stream's current tail
@@ -222,6 +223,10 @@ class Executor {
   // One step; returns measured SimResult (trace when `trace`).
   tmpsim::SimResult step(bool trace);
   bool capture_graph();
+  // Captures a separate graph of the step with the per-GEMM timing events as
+  // graph nodes, replays it twice and leaves the second replay's GEMM timings
+  // in the stack's kernel stats (the roofline of the graph-replayed step).
+  void timed_graph_replay();
   const tmpsim::SchedulePlan& plan() const { return plan_; }
   const std::vector<oases_trace_event>& events() const { return events_; }
 

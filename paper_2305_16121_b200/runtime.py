@@ -304,6 +304,13 @@ class LayerStack:
     def set_kernel_timing(self, on=True):
         check(capi.lib().oases_stack_set_kernel_timing(self._h, int(on)))
 
+    def graph_kernel_stats(self):
+        """Linear-GEMM timings measured inside a replay of the captured step (timing
+        events as graph nodes of a separately captured copy of the step)."""
+        k = capi.KernelStats()
+        check(capi.lib().oases_stack_graph_kernel_stats(self._h, C.byref(k)))
+        return {"gemm_ms": k.gemm_ms, "gemm_flops": k.gemm_flops, "gemm_launches": k.gemm_launches}
+
     def kernel_stats(self):
         k = capi.KernelStats()
         check(capi.lib().oases_stack_kernel_stats(self._h, C.byref(k)))

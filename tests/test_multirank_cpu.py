@@ -95,3 +95,26 @@ def test_two_rank_partition_and_allreduce():
     for p in procs:
         p.join(timeout=60)
     assert results == {0: True, 1: True}, results
+
+
+def test_bench_launches_one_rank_per_gpu():
+    """bench.py --gpus N outside torchrun re-executes itself as N ranks; inside a launcher
+    whose WORLD_SIZE disagrees with --gpus it refuses instead of silently running TMP=1."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["OASES_BENCH_PRINT_LAUNCH"] = "1"
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--steps", "2"],
+                         env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    cmd = json.loads(out.stdout.strip().splitlines()[-1])["launch"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+    env.pop("OASES_BENCH_PRINT_LAUNCH")
+    env["WORLD_SIZE"] = "1"
+    bad = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2"], env=env,
+                         capture_output=True, text=True, timeout=120)
+    assert bad.returncode != 0 and "WORLD_SIZE=1" in bad.stderr
