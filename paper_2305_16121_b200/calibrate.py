@@ -19,73 +19,40 @@ the kernels, shapes and memory traffic are exactly those of a real rank.
 """
 from __future__ import annotations
 
-import statistics
-
 from . import tmpsim as t
-from .runtime import Context, LayerStack, ModelConfig, plan_for
+from .runtime import ModelConfig, graph_for
 
 
-def measure_block_times(cfg: ModelConfig, degree: int, steps: int = 3, variant="Oases"):
-    """{block: (d_fwd, d_bwd)} seconds per sub-batch for one rank at `degree`."""
-    ctx = Context(tp=degree, comm_disabled=degree > 1)
-    st = LayerStack(ctx, cfg)
-    st.init_random(7)
-    plan = plan_for(cfg, variant)
-    st.bind(plan)
-    st.step(trace=False)  # warm-up
-    ops = list(plan.forward_ops) + list(plan.backward_ops)
-    fwd = {b: [] for b in range(st.num_blocks)}
-    bwd = {b: [] for b in range(st.num_blocks)}
-    for _ in range(steps):
-        res = st.step(trace=True)
-        per = {}
-        for op_id, _stream, s0, s1 in res.events:
-            if op_id >= len(ops):
-                continue
-            op = ops[op_id]
-            key = (op.block, op.sub_batch, op.pass_)
-            per[key] = per.get(key, 0.0) + (s1 - s0)
-        for (b, sb, ps), dur in per.items():
-            if ps == t.Pass.Forward:
-                fwd[b].append(dur)
-        for b in range(st.num_blocks):
-            for sb in (0, 1):
-                rec = per.get((b, sb, t.Pass.Recompute), 0.0)
-                bw = per.get((b, sb, t.Pass.Backward))
-                if bw is not None:
-                    bwd[b].append(rec + bw)
-    st.close()
-    ctx.close()
-    return {b: (statistics.median(fwd[b]), statistics.median(bwd[b])) for b in fwd}
+def _exec_options(cfg: ModelConfig, steps: int = 1):
+    o = t.ExecOptions()
+    o.spec = cfg.spec()
+    o.ffn_hidden, o.attention, o.layernorm, o.bias, o.residual = (cfg.ffn, cfg.attention, cfg.layernorm, cfg.bias,
+                                                                   cfg.residual)
+    o.hidden_dropout, o.attention_dropout, o.seed = cfg.hidden_dropout, cfg.attention_dropout, cfg.seed
+    o.steps = steps
+    return o
 
 
 def calibrate(cfg: ModelConfig, degrees, *, steps: int = 3, profile: "t.HardwareProfile | None" = None,
-              measured_allreduce=None):
-    """Measured-cost rows for every block of `cfg` and every degree in `degrees`.
+              measured_allreduce=None, device: int = 0):
+    """Measured-cost rows for every block of `cfg` and every degree in `degrees`
+    (the C++ tmpsim::calibrate of include/oases/runtime.hpp).
 
-    measured_allreduce: optional {degree: seconds} per half-batch AllReduce
-    (e.g. from an NCCL sweep on a multi-GPU box); otherwise the alpha-beta
-    model of `profile` (default: tmpsim.b200_profile) is used.
+    measured_allreduce: optional {degree: seconds} per half-batch AllReduce (e.g.
+    tools/nccl_sweep.py on a multi-GPU node); otherwise c_fwd / c_bwd are the
+    alpha-beta comm_time of `profile` (default: tmpsim.b200_profile).
     """
-    profile = profile or t.b200_profile(max(degrees))
-    spec = cfg.spec()
+    o = t.ContextOptions()
+    o.device = device
+    ctx = t.Context(o)
+    rows = list(t.calibrate(graph_for(cfg), cfg.spec(), ctx, list(degrees), _exec_options(cfg), steps))
     half_bytes = cfg.batch / 2 * cfg.seq * cfg.hidden * cfg.bytes_per_element
-    rows = []
-    for d in degrees:
-        times = measure_block_times(cfg, d, steps)
-        if d == 1:
-            c = 0.0
-        elif measured_allreduce and d in measured_allreduce:
-            c = measured_allreduce[d]
-        else:
-            c = t.comm_time(t.allreduce_volume(half_bytes, d), d, profile)
-        for b, (df, db) in times.items():
-            for field, v in (("d_fwd", df), ("d_bwd", db), ("c_fwd", c), ("c_bwd", c),
-                             ("m_saved", 2 * half_bytes)):
-                r = t.MeasuredRow()
-                r.block_index, r.degree, r.field, r.seconds_or_bytes = b, d, field, float(v)
-                rows.append(r)
-    del spec
+    for r in rows:
+        if r.field in ("c_fwd", "c_bwd") and r.degree > 1:
+            if measured_allreduce and r.degree in measured_allreduce:
+                r.seconds_or_bytes = float(measured_allreduce[r.degree])
+            elif profile is not None:
+                r.seconds_or_bytes = t.comm_time(t.allreduce_volume(half_bytes, r.degree), r.degree, profile)
     return rows
 
 

@@ -30,7 +30,7 @@ HardwareProfile b200_profile(int num_devices, double nvlink_bytes_per_s, double 
   HardwareProfile hp;
   hp.num_devices = num_devices;
   hp.memory_capacity = 180LL * 1000 * 1000 * 1000;
-  hp.compute_throughput = 0.5 * 1611.4e12;  // MAC/s at the measured bf16 dense burst (MEASURED_PEAKS.json)
+  hp.compute_throughput = 0.5 * 1696.6e12;  // MAC/s at the measured bf16 dense burst (MEASURED_PEAKS.json, round 2)
   for (int d = 1; d <= num_devices; d *= 2) {
     hp.candidate_degrees.push_back(d);
     if (d > 1) {
