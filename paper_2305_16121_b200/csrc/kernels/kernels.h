@@ -17,13 +17,15 @@ bool bdr_layernorm_supported(long long rows, int cols);
 cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
                                                 void* xout, const void* gamma, const void* beta, void* y,
                                                 long long rows, int cols, float eps, float p, uint64_t seed,
-                                                uint64_t offset, cudaStream_t st, uint16_t* keep_bits = nullptr);
+                                                uint64_t offset, cudaStream_t st, uint16_t* keep_bits = nullptr,
+                                                int max_sms = 0);
+// max_sms: SM cap of the persistent LayerNorm grid (0 = all; TMP > 1 leaves SMs to NCCL)
 cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, long long rows,
-                          int cols, float eps, cudaStream_t st);
+                          int cols, float eps, cudaStream_t st, int max_sms = 0);
 size_t layernorm_bwd_workspace(long long rows, int cols);
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,
                           float* dgamma, float* dbeta, int acc_params, void* workspace, long long rows, int cols,
-                          float eps, cudaStream_t st);
+                          float eps, cudaStream_t st, int max_sms = 0);
 // which: 1 = dx and row statistics (into workspace), 2 = dgamma/dbeta from those statistics
 // gout (optional, part 1 only): also write dropout'(dx) under (drop_p, seed,
 // offset) -- the bias-dropout-residual backward fused into the LN backward
@@ -34,6 +36,33 @@ cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* 
                                long long rows, int cols, float eps, cudaStream_t st, void* gout = nullptr,
                                float drop_p = 0.f, uint64_t seed = 0, uint64_t offset = 0,
                                const uint16_t* keep_bits = nullptr);
+// Persistent bulk-copy-pipelined LayerNorm (rowpipe.cu). Supported when
+// cols = 16 * TPR with TPR a power of two in [8, 512] (cols 128..8192).
+bool lnp_supported(long long rows, int cols);
+// Forward: xout == nullptr -> y = LN(in); else the fused bias-dropout-residual
+// xout = res + dropout(in + bias), y = LN(xout) (keep_bits: optional 1-bit
+// keep decisions). max_sms caps the SMs the persistent grid uses (0 = all).
+cudaError_t lnp_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res, void* xout,
+                              const void* gamma, const void* beta, void* y, long long rows, int cols, float eps,
+                              float p, uint64_t seed, uint64_t offset, uint16_t* keep_bits, int max_sms,
+                              cudaStream_t st);
+// Backward: dx (+)= LN'(dy); gout (optional) = dropout'(dx) under (p, seed,
+// offset) or keep_bits; part (optional) receives lnp_partial_rows(...) rows of
+// [3][cols] f32 column partials (sum dy*xhat, sum dy, sum of gout -- or of dx
+// when gout is null); stats (optional) the per-row (mean, rstd).
+cudaError_t lnp_layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,
+                              void* gout, float p, uint64_t seed, uint64_t offset, const uint16_t* keep_bits,
+                              float* part, float2* stats, long long rows, int cols, float eps, int max_sms,
+                              cudaStream_t st);
+// Persistent LayerNorm kernels in use: unless OASES_LNP=0 (A/B runs of the one-shot kernels).
+bool lnp_enabled();
+// Upper bound of lnp_partial_rows over dtypes, acc and SM caps (workspace sizing).
+long long lnp_partial_rows_max(long long rows, int cols);
+// Partial rows one lnp_layernorm_bwd launch of this shape writes (0 if unsupported).
+long long lnp_partial_rows(int dtype, long long rows, int cols, int acc_dx, int max_sms);
+// dgamma / dbeta / dbias (+)= fixed-order sums of prows partial rows (null outputs skipped).
+cudaError_t lnp_finalize(const float* part, long long prows, int cols, float* dgamma, float* dbeta, float* dbias,
+                         int acc_gamma, int acc_beta, int acc_bias, cudaStream_t st);
 // batch = n_samples * heads_local; rows are (sample, local head, query).
 cudaError_t softmax_fwd(int dtype, const void* s, void* p, void* pd, long long batch, int seq, float scale,
                         float dropout_p, uint64_t seed, uint64_t offset, int heads_local, int heads_total,

@@ -1024,19 +1024,27 @@ cudaError_t ln_fwd_t(const void* x, const void* gamma, const void* beta, void* y
 
 size_t layernorm_bwd_workspace(long long rows, int cols) {
   const ParamSplit a = param_split<float>(rows, cols), b = param_split<__nv_bfloat16>(rows, cols);
-  int chunks = a.chunks > b.chunks ? a.chunks : b.chunks;
+  long long chunks = a.chunks > b.chunks ? a.chunks : b.chunks;
   if (param_split16(rows, cols).chunks > chunks) chunks = param_split16(rows, cols).chunks;
+  // the persistent kernel's [prows][3][cols] partials (rowpipe.cu)
+  const long long lnp3 = 3 * lnp_partial_rows_max(rows, cols);
+  if ((lnp3 + 1) / 2 > chunks) chunks = (lnp3 + 1) / 2;
   return ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)) +
          static_cast<size_t>(chunks) * 2 * cols * sizeof(float) + 256;
 }
 
 cudaError_t layernorm_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, long long rows,
-                          int cols, float eps, cudaStream_t st) {
+                          int cols, float eps, cudaStream_t st, int max_sms) {
+  if (lnp_enabled() && lnp_supported(rows, cols))
+    return lnp_layernorm_fwd(dtype, x, nullptr, nullptr, nullptr, gamma, beta, y, rows, cols, eps, 0.f, 0, 0, nullptr,
+                             max_sms, st);
   if (dtype == OASES_BF16) return ln_fwd_t<__nv_bfloat16>(x, gamma, beta, y, rows, cols, eps, st);
   return ln_fwd_t<float>(x, gamma, beta, y, rows, cols, eps, st);
 }
 
-bool bdr_layernorm_supported(long long rows, int cols) { return ln_rows_nv(cols) && rows < (1LL << 31); }
+bool bdr_layernorm_supported(long long rows, int cols) {
+  return (lnp_enabled() && lnp_supported(rows, cols)) || (ln_rows_nv(cols) && rows < (1LL << 31));
+}
 
 bool ln_bwd_dropout_supported(int dtype, long long rows, int cols) {
   const int nv = dtype == OASES_BF16 ? block_nvec<__nv_bfloat16>(cols) : block_nvec<float>(cols);
@@ -1046,7 +1054,10 @@ bool ln_bwd_dropout_supported(int dtype, long long rows, int cols) {
 cudaError_t bias_dropout_residual_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res,
                                                 void* xout, const void* gamma, const void* beta, void* y,
                                                 long long rows, int cols, float eps, float p, uint64_t seed,
-                                                uint64_t offset, cudaStream_t st, uint16_t* keep_bits) {
+                                                uint64_t offset, cudaStream_t st, uint16_t* keep_bits, int max_sms) {
+  if (lnp_enabled() && lnp_supported(rows, cols))
+    return lnp_layernorm_fwd(dtype, in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset, keep_bits,
+                             max_sms, st);
   if (!bdr_layernorm_supported(rows, cols)) return cudaErrorNotSupported;
   if (dtype == OASES_BF16)
     return ln_rows_launch<__nv_bfloat16, true>(in, bias, res, xout, gamma, beta, y, rows, cols, eps, p, seed, offset,
@@ -1068,7 +1079,19 @@ cudaError_t layernorm_bwd_part(int which, int dtype, const void* x, const void* 
 
 cudaError_t layernorm_bwd(int dtype, const void* x, const void* gamma, const void* dy, void* dx, int acc_dx,
                           float* dgamma, float* dbeta, int acc_params, void* workspace, long long rows, int cols,
-                          float eps, cudaStream_t st) {
+                          float eps, cudaStream_t st, int max_sms) {
+  if (lnp_enabled() && lnp_supported(rows, cols)) {
+    // the persistent kernel: column partials of the parameter gradients in the workspace, then
+    // one fixed-order finalize
+    float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) +
+                                           ((static_cast<size_t>(rows) * sizeof(float2) + 255) & ~size_t(255)));
+    const bool params = dgamma || dbeta;
+    cudaError_t e = lnp_layernorm_bwd(dtype, x, gamma, dy, dx, acc_dx, nullptr, 0.f, 0, 0, nullptr,
+                                      params ? part : nullptr, nullptr, rows, cols, eps, max_sms, st);
+    if (e != cudaSuccess || !params) return e;
+    return lnp_finalize(part, lnp_partial_rows(dtype, rows, cols, acc_dx, max_sms), cols, dgamma, dbeta, nullptr,
+                        acc_params, acc_params, 0, st);
+  }
   if (dtype == OASES_BF16)
     return ln_bwd_t<__nv_bfloat16>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st);
   return ln_bwd_t<float>(x, gamma, dy, dx, acc_dx, dgamma, dbeta, acc_params, workspace, rows, cols, eps, st);

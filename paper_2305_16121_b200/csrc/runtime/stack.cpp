@@ -178,10 +178,12 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
     fuse_bdr_ln_ = !(e && e[0] == '0');
   }
   // the fused forward kernel caches the hidden-dropout decisions for the backward
+  // persistent LayerNorm backward with the parameter / row-bias column sums folded in (rowpipe.cu)
+  lnp_bwd_ = cfg.ln && lnp_enabled() && lnp_supported(static_cast<int64_t>(cfg.b / 2) * cfg.s, static_cast<int>(cfg.h));
   hbits_ = cfg.ln && fuse_bdr_ln_ && cfg.p_hidden > 0.f && cfg.h % 16 == 0 &&
            bdr_layernorm_supported(static_cast<int64_t>(cfg.b / 2) * cfg.s, static_cast<int>(cfg.h)) &&
-           ln_bwd_dropout_supported(cfg.bytes == 2 ? OASES_BF16 : OASES_F32, static_cast<int64_t>(cfg.b / 2) * cfg.s,
-                                    static_cast<int>(cfg.h));
+           (lnp_bwd_ || ln_bwd_dropout_supported(cfg.bytes == 2 ? OASES_BF16 : OASES_F32,
+                                                 static_cast<int64_t>(cfg.b / 2) * cfg.s, static_cast<int>(cfg.h)));
   // FFN column-bias gradient from the FC2 dgrad epilogue's partials unless OASES_FUSED_COLSUM=0
   {
     const char* e = std::getenv("OASES_FUSED_COLSUM");
@@ -323,6 +325,10 @@ void Stack::alloc_all() {
     w.y = arena_.alloc(static_cast<size_t>(2 * Ts * h) * es);
     // row statistics of both sub-batches (the parameter pass runs once over 2 T_sub rows)
     w.ln_ws = arena_.alloc(layernorm_bwd_workspace(2 * Ts, static_cast<int>(h)));
+    // [2 sub-batches][partial rows][3][h] column partials of the persistent LayerNorm backward
+    if (lnp_bwd_)
+      w.lnp_part = static_cast<float*>(arena_.alloc(
+          static_cast<size_t>(2 * lnp_partial_rows_max(Ts, static_cast<int>(h)) * 3 * h) * sizeof(float)));
     w.col_ws = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
                                      colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
     w.col_ws2 = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
@@ -503,7 +509,7 @@ void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, v
     check_cuda(bias_dropout_residual_layernorm_fwd(dtype(), ar, bias, res, x, bp.p[OASES_P_LN_GAMMA],
                                                    bp.p[OASES_P_LN_BETA], ln, Ts, static_cast<int>(h), cfg_.eps,
                                                    cfg_.p_hidden, cfg_.seed, drop_offset(block - 1, sb, 0),
-                                                   ctx_.compute, bits),
+                                                   ctx_.compute, bits, ctx_.gemm_max_ctas),
                "bdr + layernorm");
     ++launches_;
     return;
@@ -516,7 +522,8 @@ void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, v
 }
 
 void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y) {
-  check_cuda(layernorm_fwd(dtype(), x, g, b, y, tokens_sub(), cfg_.h, cfg_.eps, ctx_.compute), "layernorm_fwd");
+  check_cuda(layernorm_fwd(dtype(), x, g, b, y, tokens_sub(), cfg_.h, cfg_.eps, ctx_.compute, ctx_.gemm_max_ctas),
+             "layernorm_fwd");
   ++launches_;
 }
 
@@ -951,7 +958,7 @@ void Stack::backward(int wi, int block, int sb) {
   bwd_seen_[static_cast<size_t>(wi)][static_cast<size_t>(block)] = true;
   // 1. gradient arriving at x_{b+1}; with LayerNorm the same pass also writes
   //    g_ar = dropout'(g) (step 2) when the row-group kernel covers the width
-  bool gar_done = false;
+  bool gar_done = false, row_bias_done = false;
   if (block == nblocks_ - 1) {
     const BlockParams& bp = w.params[static_cast<size_t>(block)];
     void* y = half(w.y, sb, h);
@@ -966,7 +973,35 @@ void Stack::backward(int wi, int block, int sb) {
   } else {
     const BlockParams& nxt = w.params[static_cast<size_t>(block + 1)];
     const void* dln = w.bwd_ar[(block + 1) % 2][usb];
-    if (cfg_.ln) {
+    if (cfg_.ln && lnp_bwd_) {
+      // one persistent pass: dx (+ residual), g_ar = dropout'(dx) and this sub-batch's column
+      // partials of dgamma/dbeta (block b+1) and of the row-bias gradient (block b)
+      const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
+      const bool drop = cfg_.p_hidden > 0.f;
+      const int acc_dx = cfg_.residual ? 1 : 0;
+      const long long prows = lnp_partial_rows(dtype(), Ts, hi, acc_dx, ctx_.gemm_max_ctas);
+      check_cuda(lnp_layernorm_bwd(dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, acc_dx, drop ? gar_sb : nullptr,
+                                   cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0),
+                                   drop && hbits_ ? w.hbits[static_cast<size_t>(block)][usb] : nullptr,
+                                   w.lnp_part + static_cast<int64_t>(sb) * prows * 3 * h, nullptr, Ts, hi, cfg_.eps,
+                                   ctx_.gemm_max_ctas, ctx_.compute),
+                 "layernorm_bwd (persistent)");
+      gar_done = drop;
+      row_bias_done = true;
+      ++launches_;
+      if (wgrad_now) {
+        // dgamma/dbeta and the row-bias gradient over both sub-batches' partials: side stream
+        const bool acc_ln = touch(w, block + 1, OASES_P_LN_GAMMA);
+        const bool acc_b = cfg_.bias ? touch(w, block, OASES_P_B_ROW) : false;
+        BlockParams& cur = w.params[static_cast<size_t>(block)];
+        fork_side();
+        check_cuda(lnp_finalize(w.lnp_part, 2 * prows, hi, nxt.g[OASES_P_LN_GAMMA], nxt.g[OASES_P_LN_BETA],
+                                cfg_.bias ? cur.g[OASES_P_B_ROW] : nullptr, acc_ln ? 1 : 0, acc_ln ? 1 : 0,
+                                acc_b ? 1 : 0, ctx_.side),
+                   "layernorm params + row bias finalize");
+        ++launches_;
+      }
+    } else if (cfg_.ln) {
       const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
       const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && ln_bwd_dropout_supported(dtype(), Ts, hi);
       // this sub-batch's row statistics land in rows [sb T_sub, (sb+1) T_sub) of the workspace
@@ -1007,7 +1042,7 @@ void Stack::backward(int wi, int block, int sb) {
     }
     gar = gar_sb;
   }
-  if (cfg_.bias && wgrad_now) {
+  if (cfg_.bias && wgrad_now && !row_bias_done) {
     // row-bias gradient = column sums of g_ar over both sub-batches: side stream, under the row GEMMs
     const bool acc = touch(w, block, OASES_P_B_ROW);
     fork_side();
@@ -1123,7 +1158,7 @@ void Stack::tail(int wi, int sb) {
     const bool acc = touch(w, 0, OASES_P_LN_GAMMA);
     check_cuda(layernorm_bwd(dtype(), w.xs[0][usb], bp.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0,
                              bp.g[OASES_P_LN_GAMMA], bp.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, Ts,
-                             static_cast<int>(h), cfg_.eps, ctx_.compute),
+                             static_cast<int>(h), cfg_.eps, ctx_.compute, ctx_.gemm_max_ctas),
                "layernorm_bwd (tail)");
     launches_ += 3;
   } else {

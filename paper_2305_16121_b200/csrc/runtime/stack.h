@@ -107,6 +107,7 @@ struct Worker {
   std::vector<std::array<uint16_t*, 2>> hbits;
   void* y = nullptr;     // [2][T_sub, h] final output x_B (per sub-batch half) for the loss head
   void* ln_ws = nullptr;
+  float* lnp_part = nullptr;  // persistent LayerNorm backward column partials [2][prows][3][h]
   void* col_ws = nullptr;
   void* col_ws2 = nullptr;  // side-stream column sums (bias gradients)
   float* col_part = nullptr;  // FC2 dgrad epilogue's 32-row column-sum partials (FFN column bias)
@@ -188,6 +189,7 @@ class Stack {
   bool fused_attn_ = false;  // tcgen05 flash attention (attention.cu) instead of QK^T / softmax / PV
   bool fuse_bdr_ln_ = true;
   bool rowdot_ = false;  // attention D = rowsum(dO o O) comes from the proj dgrad epilogue
+  bool lnp_bwd_ = false;  // persistent LayerNorm backward with folded column sums (rowpipe.cu)
   bool hbits_ = false;   // hidden-dropout keep bits cached (fused forward kernel covers the shape)
   bool colsum_ = false;  // FFN column-bias gradient partials come from the FC2 dgrad (MUL) epilogue
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;

@@ -1,0 +1,66 @@
+"""Warm timing of the LayerNorm row kernels through the C-ABI at a block's sub-batch
+shape, working set rotated over several buffer sets so it exceeds the 126 MB L2
+(CUDA events around a CUDA graph of back-to-back launches).
+
+    OASES_LNP=0|1 python tools/ln_bench.py [T] [h]     (default: C3 TMP=8 rank, T=8192 h=4096)
+Bandwidth is algorithmic bytes / time against MEASURED_PEAKS.json hbm_gbs.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2305_16121_b200 import ops  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+try:
+    HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
+except (OSError, KeyError):
+    HBM = 6531.9e9
+T = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+h = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+bf = torch.bfloat16
+B = 2
+tensor_bytes = T * h * B
+nsets = max(2, int(600e6 // (4 * tensor_bytes)) + 1)
+sets = []
+for _ in range(nsets):
+    sets.append({k: (torch.randn(T, h, device="cuda") * 0.5 + 0.1).to(bf) for k in ("x", "r", "y", "z")})
+g = (torch.rand(h, device="cuda") + 0.5).to(bf)
+b = (torch.randn(h, device="cuda") * 0.1).to(bf)
+dg = torch.zeros(h, device="cuda")
+dbe = torch.zeros(h, device="cuda")
+res = {}
+
+
+def timeit(fn, nbytes, name, rep=None):
+    rep = rep or 4 * nsets
+    for i in range(nsets):
+        fn(sets[i])
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for i in range(rep):
+            fn(sets[i % nsets])
+    gr.replay()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    gr.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) / rep * 1e3
+    res[name] = {"us": us, "alg_bytes": nbytes, "gbs": nbytes / us / 1e3, "frac_hbm": nbytes / (us * 1e-6) / HBM}
+    print(f"{name:40s} {us:8.2f} us  {nbytes / us / 1e3:7.0f} GB/s  ({nbytes / (us * 1e-6) / HBM:4.2f} of HBM)",
+          flush=True)
+
+
+timeit(lambda d: ops.layernorm_fwd(d["x"], g, b, d["y"]), 2 * tensor_bytes, "layernorm_fwd")
+timeit(lambda d: ops.bias_dropout_residual_layernorm_fwd(d["x"], b, d["r"], d["y"], g, b, d["z"], dropout_p=0.1,
+                                                          seed=1, offset=2),
+       4 * tensor_bytes, "bdr + layernorm_fwd p=0.1")
+timeit(lambda d: ops.layernorm_bwd(d["x"], g, d["r"], d["y"], dg, dbe, accumulate_dx=True), 4 * tensor_bytes,
+       "layernorm_bwd acc (+dgamma/dbeta)")
+print(json.dumps({"T": T, "h": h, "lnp": os.environ.get("OASES_LNP", "1"), "kernels": res}))
