@@ -29,6 +29,8 @@
 // tests compare against).
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -36,6 +38,18 @@ namespace oases {
 namespace {
 
 constexpr int kStagesMax = 8;
+// CTAs per cluster of the LayerNorm backward (column partials reduced through
+// DSMEM): 2 unless OASES_LNP_CLUSTER (1, 2, 4 or 8) says otherwise (measured at
+// C2/C3 sub-batch shapes: 1 and 2 equal, 4 and 8 slower -- fewer co-resident clusters).
+int lnp_cluster() {
+  static int c = 0;
+  if (!c) {
+    const char* e = std::getenv("OASES_LNP_CLUSTER");
+    c = e ? std::atoi(e) : 2;
+    if (c != 1 && c != 2 && c != 4 && c != 8) c = 2;
+  }
+  return c;
+}
 
 template <typename T>
 struct Lnp {
@@ -478,29 +492,59 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
     for (int i = 0; i < 8; ++i) po[i] = __fadd2_rn(po[i], o[i]);
   }
   if (!a.part) return;
-  float* p = a.part + (static_cast<long long>(blockIdx.x) * RB + r) * 3 * cols + c;
+  // Column partials: the RB row slots of the CTA are summed in slot order into
+  // shared memory (the ring is idle now), then the CTAs of the cluster reduce
+  // them through distributed shared memory -- CTA rank q sums column chunk q of
+  // every rank's partials in rank order -- and write one [3][cols] partial row
+  // per cluster (lnp_cluster() times fewer rows for the finalize to read).
+  float* psm = reinterpret_cast<float*>(dsm);  // [3][cols]
+  for (int rr = 0; rr < RB; ++rr) {
+    if (r == rr) {
+      float* q0 = psm + c;
 #pragma unroll
-  for (int i = 0; i < 8; i += 2) {
-    *reinterpret_cast<float4*>(p + 2 * i) = make_float4(pg[i].x, pg[i].y, pg[i + 1].x, pg[i + 1].y);
-    *reinterpret_cast<float4*>(p + cols + 2 * i) = make_float4(pb[i].x, pb[i].y, pb[i + 1].x, pb[i + 1].y);
-    *reinterpret_cast<float4*>(p + 2 * cols + 2 * i) = make_float4(po[i].x, po[i].y, po[i + 1].x, po[i + 1].y);
+      for (int i = 0; i < 8; ++i) {
+        float2* d0 = reinterpret_cast<float2*>(q0 + 2 * i);
+        float2* d1 = reinterpret_cast<float2*>(q0 + cols + 2 * i);
+        float2* d2 = reinterpret_cast<float2*>(q0 + 2 * cols + 2 * i);
+        *d0 = rr ? __fadd2_rn(*d0, pg[i]) : pg[i];
+        *d1 = rr ? __fadd2_rn(*d1, pb[i]) : pb[i];
+        *d2 = rr ? __fadd2_rn(*d2, po[i]) : po[i];
+      }
+    }
+    __syncthreads();
   }
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const int ncl = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  const int nf4 = 3 * cols / 4, chunk = (nf4 + ncl - 1) / ncl;
+  const int f0 = rank * chunk, f1 = f0 + chunk < nf4 ? f0 + chunk : nf4;
+  float4* out = reinterpret_cast<float4*>(a.part + static_cast<long long>(blockIdx.x / ncl) * 3 * cols);
+  for (int f = f0 + tid; f < f1; f += G::THREADS) {
+    float4 t = reinterpret_cast<const float4*>(cl.map_shared_rank(psm, 0))[f];
+    for (int q = 1; q < ncl; ++q) {
+      const float4 u = reinterpret_cast<const float4*>(cl.map_shared_rank(psm, q))[f];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    out[f] = t;
+  }
+  cl.sync();  // the peers' shared memory stays valid until every rank has read it
 }
 
 // out_q[c] (+)= sum_p part[p][q][c] (null outputs skipped): block (x, q)
 // covers 128 columns of quantity q with 32 lanes x 4 columns (16-byte loads) x
-// 16 partial-row groups; group g sums rows g, g+16, ... (2 loads in flight) and
-// the 16 group sums are combined in g order (fixed order, bit-reproducible).
-__global__ void __launch_bounds__(512) lnp_finalize_kernel(const float* __restrict__ part, int prows, int cols,
-                                                           float* o0, float* o1, float* o2, int acc0, int acc1,
-                                                           int acc2) {
+// 32 partial-row groups; group g sums rows g, g+32, ... (4 loads in flight) and
+// the 32 group sums are combined in g order (fixed order, bit-reproducible).
+__global__ void __launch_bounds__(1024) lnp_finalize_kernel(const float* __restrict__ part, int prows, int cols,
+                                                            float* o0, float* o1, float* o2, int acc0, int acc1,
+                                                            int acc2) {
   pdl_trigger();
   const int q = blockIdx.y;
   float* out = q == 0 ? o0 : q == 1 ? o1 : o2;
   if (!out) return;
   const int acc = q == 0 ? acc0 : q == 1 ? acc1 : acc2;
   pdl_wait();
-  __shared__ float4 sm[16][32];
+  __shared__ float4 sm[32][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 128 + lane * 4;
   float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -508,13 +552,16 @@ __global__ void __launch_bounds__(512) lnp_finalize_kernel(const float* __restri
     const float* base = part + static_cast<long long>(q) * cols + c;
     const long long stride = 3LL * cols;
     int k = g;
-    for (; k + 16 < prows; k += 32) {
-      const float4 u = __ldg(reinterpret_cast<const float4*>(base + k * stride));
-      const float4 v = __ldg(reinterpret_cast<const float4*>(base + (k + 16) * stride));
-      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
-      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    for (; k + 96 < prows; k += 128) {
+      float4 u[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const float4*>(base + (k + 32 * i) * stride));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        t.x += u[i].x; t.y += u[i].y; t.z += u[i].z; t.w += u[i].w;
+      }
     }
-    for (; k < prows; k += 16) {
+    for (; k < prows; k += 32) {
       const float4 u = __ldg(reinterpret_cast<const float4*>(base + k * stride));
       t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
     }
@@ -524,7 +571,7 @@ __global__ void __launch_bounds__(512) lnp_finalize_kernel(const float* __restri
   if (g == 0 && c < cols) {
     float4 sacc = sm[0][lane];
 #pragma unroll
-    for (int w = 1; w < 16; ++w) {
+    for (int w = 1; w < 32; ++w) {
       const float4 u = sm[w][lane];
       sacc.x += u.x; sacc.y += u.y; sacc.z += u.z; sacc.w += u.w;
     }
@@ -625,11 +672,62 @@ cudaError_t fwd_tpr(Lnp<T> a, int max_sms, cudaStream_t st) {
 }
 
 // Geometry of a backward launch: the grid (and so the number of partial rows,
-// grid * RB) is a pure function of (element size, cols, acc, rows, max_sms).
+// grid / lnp_cluster()) is a pure function of (element size, cols, acc, rows,
+// max_sms): as many whole clusters as the occupancy calculator says can be
+// co-resident (a persistent grid must not spill into a second wave), capped
+// by the work.
 struct BwdGeo {
   Plan pl;
   int rb, threads, grid;
 };
+template <typename T, bool ACC>
+const void* bwd_kernel_ptr(int tpr) {
+  switch (tpr) {
+    case 8: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 8, ACC, false>);
+    case 16: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 16, ACC, false>);
+    case 32: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 32, ACC, false>);
+    case 64: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 64, ACC, false>);
+    case 128: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 128, ACC, false>);
+    case 256: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 256, ACC, false>);
+    default: return reinterpret_cast<const void*>(lnp_bwd_kernel<T, 512, ACC, false>);
+  }
+}
+// Co-resident clusters of the backward kernel (cached; all DROP variants share
+// the launch bounds and the shared-memory size, so the DROP=false instance stands in).
+int bwd_max_clusters(size_t esize, int tpr, bool acc, int threads, size_t smem) {
+  struct Key {
+    size_t e;
+    int t;
+    bool a;
+    size_t m;
+    int v;
+  };
+  static Key cache[32];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (cache[i].e == esize && cache[i].t == tpr && cache[i].a == acc && cache[i].m == smem) return cache[i].v;
+  const void* k = esize == 2 ? (acc ? bwd_kernel_ptr<__nv_bfloat16, true>(tpr) : bwd_kernel_ptr<__nv_bfloat16, false>(tpr))
+                             : (acc ? bwd_kernel_ptr<float, true>(tpr) : bwd_kernel_ptr<float, false>(tpr));
+  int v = 0;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) == cudaSuccess) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(lnp_cluster() * 64);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = lnp_cluster();
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&v, k, &cfg) != cudaSuccess) v = 0;
+  }
+  cudaGetLastError();
+  if (v < 1) v = 1;
+  if (n < 32) cache[n++] = {esize, tpr, acc, smem, v};
+  return v;
+}
 BwdGeo bwd_geo(size_t esize, int cols, bool acc, long long rows, int max_sms) {
   const int tpr = tpr_of(cols);
   const int rb = tpr >= 256 ? 1 : 256 / tpr;
@@ -638,7 +736,14 @@ BwdGeo bwd_geo(size_t esize, int cols, bool acc, long long rows, int max_sms) {
   // 2 CTAs per SM (the kernel's launch bounds guarantee the registers) up to 256 threads
   Plan pl = plan_with(stage, threads <= 256 ? 2 : 1);
   pl.smem += static_cast<size_t>(threads) * 16 * esize;  // private gamma slots
-  return {pl, rb, threads, grid_for_items((rows + rb - 1) / rb, pl.per_sm, max_sms)};
+  if (pl.smem < static_cast<size_t>(3) * cols * sizeof(float)) pl.smem = static_cast<size_t>(3) * cols * sizeof(float);
+  int sms = num_sms();
+  long long clusters = bwd_max_clusters(esize, tpr, acc, threads, pl.smem);
+  if (max_sms > 0 && max_sms < sms) clusters = clusters * max_sms / sms;  // leave the capped SMs' share
+  const long long need = ((rows + rb - 1) / rb + lnp_cluster() - 1) / lnp_cluster();  // whole clusters of work
+  if (clusters > need) clusters = need;
+  if (clusters < 1) clusters = 1;
+  return {pl, rb, threads, static_cast<int>(clusters) * lnp_cluster()};
 }
 
 template <typename T, int TPR, bool ACC, bool DROP>
@@ -648,7 +753,21 @@ cudaError_t bwd_tpr(Lnp<T> a, int max_sms, cudaStream_t st) {
   auto k = lnp_bwd_kernel<T, TPR, ACC, DROP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.pl.smem));
   if (e != cudaSuccess) return e;
-  e = launch_pdl(k, dim3(g.grid), dim3(g.threads), g.pl.smem, st, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(g.threads);
+  cfg.dynamicSmemBytes = g.pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = lnp_cluster();
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, k, a);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -713,7 +832,7 @@ bool lnp_enabled() {
 long long lnp_partial_rows(int dtype, long long rows, int cols, int acc_dx, int max_sms) {
   if (!lnp_supported(rows, cols)) return 0;
   const BwdGeo g = bwd_geo(dtype == OASES_BF16 ? 2 : 4, cols, acc_dx != 0, rows, max_sms);
-  return static_cast<long long>(g.grid) * g.rb;
+  return g.grid / lnp_cluster();
 }
 
 cudaError_t lnp_layernorm_fwd(int dtype, const void* in, const void* bias, const void* res, void* xout,
@@ -784,7 +903,7 @@ cudaError_t lnp_finalize(const float* part, long long prows, int cols, float* dg
                          int acc_gamma, int acc_beta, int acc_bias, cudaStream_t st) {
   if (!dgamma && !dbeta && !dbias) return cudaSuccess;
   if (cols % 4) return cudaErrorNotSupported;
-  launch_pdl(lnp_finalize_kernel, dim3((cols + 127) / 128, 3), dim3(512), 0, st, part, static_cast<int>(prows), cols,
+  launch_pdl(lnp_finalize_kernel, dim3((cols + 127) / 128, 3), dim3(1024), 0, st, part, static_cast<int>(prows), cols,
              dgamma, dbeta, dbias, acc_gamma, acc_beta, acc_bias);
   return cudaGetLastError();
 }
