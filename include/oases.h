@@ -159,6 +159,11 @@ typedef struct {
   uint32_t* mask_bits;
   int32_t mask_mode;
   int32_t dsum_ready; /* bwd: workspace already holds D = rowsum(dO o O) (e.g. an EPI_ROWDOT GEMM) */
+  /* dropout keys: sample n of this tensor is sample sample_offset + n of the
+   * keyed sub-batch (0 normally; data-parallel groups of a mixed-degree stack
+   * hold a slice of it) */
+  int32_t sample_offset;
+  int32_t pad_;
 } oases_attn_desc;
 
 int32_t oases_attention_supported(int dtype, int32_t head_dim, int32_t seq);
@@ -295,6 +300,16 @@ typedef struct {
 } oases_model_desc;
 
 oases_status oases_stack_create(oases_ctx* ctx, const oases_model_desc* model, oases_stack** out);
+/* Mixed per-block TMP degrees (the planner's non-uniform strategies,
+ * planner.hpp Strategy::degrees): block_degrees[b] divides the world size
+ * (ctx tp); a degree-d block runs data-parallel on tp/d groups of d ranks
+ * (group g owns samples [g*b*d/tp, (g+1)*b*d/tp) of the micro-batch), the
+ * executor inserts the resharding AllGathers between blocks of different
+ * degree (sim.cpp:101-175) and sums the data-parallel gradients at step end.
+ * Needs hidden_dropout == 0. */
+oases_status oases_stack_create_mixed(oases_ctx* ctx, const oases_model_desc* model, const int32_t* block_degrees,
+                                      int32_t num_blocks, oases_stack** out);
+int oases_stack_block_degree(const oases_stack* s, int block);
 oases_status oases_stack_destroy(oases_stack* stack);
 
 /* Parameter tensors per block, identified by (block, param id). Host f64

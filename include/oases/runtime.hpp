@@ -87,7 +87,9 @@ struct ExecOptions {
 // cudaEvent intervals as the trace (op_id = plan id; the two LN_0 tails get
 // ids total_ops() and total_ops() + 1), makespan, compute-busy fraction,
 // exposed communication by exposed_comm_time, device bytes as peak_memory.
-// strategy: every block at ctx.options().tp (mixed degrees: execute_mixed).
+// strategy: per-block degrees, each dividing ctx.options().tp (the world); a block
+// below the world degree runs data-parallel groups, with the resharding AllGathers
+// of simulate() between blocks of different degree.
 SimResult execute(const SchedulePlan& plan, const Strategy& strategy, Context& ctx, const ExecOptions& opts);
 
 // Per-block rows for every degree in `degrees`: d_fwd (forward op of a

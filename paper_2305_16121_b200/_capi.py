@@ -98,6 +98,8 @@ class AttnDesc(C.Structure):
         ("mask_bits", C.c_void_p),
         ("mask_mode", C.c_int32),
         ("dsum_ready", C.c_int32),
+        ("sample_offset", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -228,6 +230,9 @@ _SIGNATURES = [
     ("oases_ctx_create", C.c_int, [C.POINTER(CtxDesc), C.POINTER(C.c_void_p)]),
     ("oases_ctx_destroy", C.c_int, [C.c_void_p]),
     ("oases_stack_create", C.c_int, [C.c_void_p, C.POINTER(ModelDesc), C.POINTER(C.c_void_p)]),
+    ("oases_stack_create_mixed", C.c_int,
+     [C.c_void_p, C.POINTER(ModelDesc), C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_void_p)]),
+    ("oases_stack_block_degree", C.c_int, [C.c_void_p, C.c_int]),
     ("oases_stack_destroy", C.c_int, [C.c_void_p]),
     ("oases_stack_param_numel", C.c_int64, [C.c_void_p, C.c_int, C.c_int]),
     ("oases_stack_num_blocks", C.c_int, [C.c_void_p]),

@@ -71,6 +71,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 struct AttnParams {
   int seq, hl, hg, hoff, Z, nq;
+  int n0;  // dropout keys: first sample of this tensor in the keyed sub-batch
   int q_col, k_col, v_col;  // columns of head 0 of Q / K / V in the qkv (and dqkv) rows
   int do_col;               // column of head 0 in dout / out rows
   long long ld_out;         // fwd: ctx row stride; bwd: dqkv row stride
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int ob = k % C::NO;
       const uint32_t to = tl + C::O_COL + ob * DH + part * OC;  // this warp's columns of O
       const unsigned long long ebase =
-          (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i) *
+          (static_cast<unsigned long long>((n + p.n0) * p.hg + p.hoff + jl) * p.seq + i) *
               static_cast<unsigned long long>(p.seq) +
           c0;
       float m = -INFINITY, l = 0.f;
@@ -818,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int lim = it == 0 ? r - c0 : 1 << 20;  // keys c0 + k > r are masked on the diagonal tile
       asm volatile("" : "+r"(lim));
       const unsigned long long ebase =
-          (static_cast<unsigned long long>(n * p.hg + p.hoff + jl) * p.seq + i * kTile + r) *
+          (static_cast<unsigned long long>((n + p.n0) * p.hg + p.hoff + jl) * p.seq + i * kTile + r) *
               static_cast<unsigned long long>(p.seq) +
           static_cast<unsigned long long>(kt) * kTile + c0;
       // pass 1: P = exp2(S*sl2 - lse) (kept in registers as bf16), keep o P -> buffer
@@ -977,6 +978,7 @@ bool fill_common(AttnParams& p, const oases_attn_desc& d, std::string* err) {
   p.hl = d.heads_local;
   p.hg = d.heads_total;
   p.hoff = d.head_offset;
+  p.n0 = d.sample_offset;
   p.Z = d.samples * d.heads_local;
   p.nq = d.seq / kTile;
   p.q_col = 0;

@@ -640,6 +640,38 @@ cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cu
   return cudaGetLastError();
 }
 
+// In-process AllGather (1-GPU emulation of a TMP group's resharding
+// AllGather): w buffers, each holding chunk i (n elements at offset i*n) of
+// its own; afterwards every buffer holds all w chunks. blockIdx.y = (dst, src)
+// pair, 16-byte copies.
+__global__ void __launch_bounds__(kThreads) local_allgather_kernel(BufList b, int w, long long n16) {
+  const int pair = blockIdx.y, dst = pair / w, src = pair % w;
+  if (dst == src) return;
+  const uint4* s = reinterpret_cast<const uint4*>(b.p[src]) + src * n16;
+  uint4* d = reinterpret_cast<uint4*>(b.p[dst]) + src * n16;
+  for (long long i = blockIdx.x * static_cast<long long>(kThreads) + threadIdx.x; i < n16;
+       i += static_cast<long long>(gridDim.x) * kThreads)
+    d[i] = s[i];
+}
+
+cudaError_t local_allgather(int dtype, void* const* bufs, int w, long long n, cudaStream_t st) {
+  if (w < 1 || w > 8) return cudaErrorInvalidValue;
+  const long long bytes = n * (dtype == OASES_BF16 ? 2 : dtype == OASES_F64 ? 8 : 4);
+  BufList b{};
+  for (int i = 0; i < w; ++i) {
+    b.p[i] = bufs[i];
+    if ((reinterpret_cast<uintptr_t>(bufs[i]) & 15u) != 0) return cudaErrorMisalignedAddress;
+  }
+  if (bytes % 16) return cudaErrorInvalidValue;
+  if (w == 1) return cudaSuccess;
+  const long long n16 = bytes / 16;
+  long long gx = (n16 + kThreads * 4 - 1) / (kThreads * 4);
+  if (gx > 1184) gx = 1184;
+  local_allgather_kernel<<<dim3(static_cast<unsigned>(gx < 1 ? 1 : gx), static_cast<unsigned>(w * w)), kThreads, 0,
+                           st>>>(b, w, n16);
+  return cudaGetLastError();
+}
+
 cudaError_t fill_uniform(int dtype, void* p, long long n, float scale, uint64_t seed, uint64_t offset,
                          cudaStream_t st) {
   const unsigned g = grid_for(n, kThreads * 4);

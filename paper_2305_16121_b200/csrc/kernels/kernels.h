@@ -90,6 +90,9 @@ size_t loss_workspace();
 cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int acc, double* ws, long long n,
                          cudaStream_t st);
 cudaError_t local_allreduce(int dtype, void* const* bufs, int w, long long n, cudaStream_t st);
+// In-process AllGather: bufs[i] holds chunk i (n elements at offset i * n); afterwards every
+// buffer holds all w chunks (16-byte aligned buffers, n * element size % 16 == 0).
+cudaError_t local_allgather(int dtype, void* const* bufs, int w, long long n, cudaStream_t st);
 
 }  // namespace oases
 

@@ -136,6 +136,24 @@ oases_status oases_stack_create(oases_ctx* ctx, const oases_model_desc* model, o
   });
 }
 
+oases_status oases_stack_create_mixed(oases_ctx* ctx, const oases_model_desc* model, const int32_t* block_degrees,
+                                      int32_t num_blocks, oases_stack** out) {
+  return guarded([&] {
+    if (!ctx || !ctx->ctx || !model || !out || (num_blocks > 0 && !block_degrees)) throw ConfigError("null argument");
+    if (num_blocks < 0) throw ConfigError("num_blocks must be >= 0");
+    std::vector<int> deg(block_degrees, block_degrees + num_blocks);
+    auto h = std::make_unique<oases_stack>();
+    h->stack = std::make_unique<oases::Stack>(*ctx->ctx, to_cfg(*model), deg);
+    h->owner = ctx;
+    ++ctx->refs;
+    *out = h.release();
+  });
+}
+
+int oases_stack_block_degree(const oases_stack* s, int block) {
+  return (s && s->stack && block >= 0 && block < s->stack->num_blocks()) ? s->stack->degree(block) : 0;
+}
+
 oases_status oases_stack_destroy(oases_stack* s) {
   return guarded([&] {
     if (s) {

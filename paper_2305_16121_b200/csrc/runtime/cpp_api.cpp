@@ -26,6 +26,7 @@ struct Context::Impl {
   std::unique_ptr<oases::Stack> stack;
   std::tuple<int, int, int, int, int, int, int, int, int, int, int, int, double, double, std::uint64_t> key{};
   bool seeded = false;
+  std::vector<int> degrees;
 };
 
 namespace {
@@ -64,15 +65,16 @@ oases::ModelCfg to_cfg(const ModelSpec& s, const ExecOptions& o) {
   return c;
 }
 
-void check_uniform(const SchedulePlan& plan, const Strategy& st, int tp) {
+// The strategy's per-block degrees (each dividing the context's world size
+// ctx tp); mixed degrees run data-parallel groups with resharding AllGathers.
+std::vector<int> strategy_degrees(const SchedulePlan& plan, const Strategy& st, int tp) {
   int max_block = -1;
   for (int i = 0; i < plan.total_ops(); ++i) max_block = std::max(max_block, plan.op(i).block);
   if (static_cast<int>(st.degrees.size()) != max_block + 1)
     throw ConfigError("execute: strategy needs one degree per block (" + std::to_string(max_block + 1) + ")");
   for (int d : st.degrees)
-    if (d != tp)
-      throw ConfigError("execute: every block must run at the context's TMP degree " + std::to_string(tp) +
-                        " (mixed per-block degrees need a context per degree group)");
+    if (d < 1 || tp % d) throw ConfigError("execute: every block degree must divide the context's world size " + std::to_string(tp));
+  return st.degrees;
 }
 
 }  // namespace
@@ -97,15 +99,16 @@ Context::Impl& Context::impl() { return *impl_; }
 
 SimResult execute(const SchedulePlan& plan, const Strategy& strategy, Context& ctx, const ExecOptions& opts) {
   Context::Impl& I = ctx.impl();
-  check_uniform(plan, strategy, I.opts.tp);
+  const std::vector<int> degrees = strategy_degrees(plan, strategy, I.opts.tp);
   if (opts.steps < 1 || opts.warmup < 0) throw ConfigError("execute: steps >= 1 and warmup >= 0");
   const oases::ModelCfg c = to_cfg(opts.spec, opts);
   const auto key = std::make_tuple(c.h, c.f, c.heads, c.s, c.b, c.layers, c.bytes, int(c.recompute), int(c.attention),
                                    int(c.ln), int(c.bias), int(c.residual), double(c.p_hidden), double(c.p_attn),
                                    c.seed);
-  if (!I.stack || key != I.key) {
+  if (!I.stack || key != I.key || degrees != I.degrees) {
     I.stack.reset();
-    I.stack = std::make_unique<oases::Stack>(*I.ctx, c);
+    I.stack = std::make_unique<oases::Stack>(*I.ctx, c, degrees);
+    I.degrees = degrees;
     I.stack->init_random(c.seed);
     I.key = key;
   }

@@ -10,6 +10,7 @@
 // simulate() (sim.cpp:178-199), and the device bytes of the stack.
 #include <algorithm>
 #include <cstdlib>
+#include <deque>
 #include <map>
 #include <set>
 
@@ -124,7 +125,7 @@ Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stac
     const auto& op = plan.op(id);
     max_block = std::max(max_block, op.block);
     if (op.kind == OpKind::AllGather)
-      throw ConfigError("plan_bind: resharding AllGathers (mixed per-block degrees) are not executable yet");
+      throw ConfigError("plan_bind: AllGather ops are injected from the stack's per-block degrees, not planned");
     if (tmpsim::is_comm(op.kind) && op.pass == Pass::Recompute) rec_comm.emplace(op.block, op.sub_batch);
   }
   if (max_block + 1 != stack.num_blocks())
@@ -171,6 +172,7 @@ Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stac
     e.waits.assign(waits.begin(), waits.end());
     ops_.push_back(std::move(e));
   }
+  if (stack.mixed()) inject_reshards(n);
   // Residual-stream storage: x_b stays in its own HBM buffer unless the plan
   // rebuilds it from a replayed AllReduce (interior of a CrossPass unit).
   {
@@ -184,7 +186,9 @@ Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stac
     const auto& op = plan.op(id);
     if (op.pass == Pass::Backward && op.block == 0) tail_wait_[static_cast<size_t>(op.sub_batch)] = id;
   }
-  const int nev = n + 2;
+  stream_of_.assign(static_cast<size_t>(n + nreshard_), 0);
+  for (const ExecOp& e : ops_) stream_of_[static_cast<size_t>(e.id)] = e.stream;
+  const int nev = n + nreshard_ + 2;
   t0_.resize(static_cast<size_t>(nev));
   t1_.resize(static_cast<size_t>(nev));
   for (int i = 0; i < nev; ++i) {
@@ -194,6 +198,111 @@ Executor::Executor(Stack& stack, const tmpsim::SchedulePlan& plan) : stack_(stac
   check_cuda(cudaEventCreate(&begin_), "event");
   check_cuda(cudaEventCreate(&end_), "event");
   check_cuda(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "event");
+}
+
+void Executor::inject_reshards(int n) {
+  const int B = stack_.num_blocks();
+  std::vector<int> last_fwd_comm(static_cast<size_t>(B), -1), last_bwd_comm(static_cast<size_t>(B), -1),
+      last_bwd_compute(static_cast<size_t>(B), -1);
+  std::vector<std::array<int, 2>> first_fwd(static_cast<size_t>(B), {-1, -1}), first_bwd(static_cast<size_t>(B), {-1, -1});
+  for (int id = 0; id < n; ++id) {
+    const auto& op = plan_.op(id);
+    const size_t b = static_cast<size_t>(op.block), sb = static_cast<size_t>(op.sub_batch);
+    if (op.pass == Pass::Forward) {
+      if (tmpsim::is_comm(op.kind)) last_fwd_comm[b] = id;
+      if (op.kind == OpKind::ForwardCompute && first_fwd[b][sb] < 0) first_fwd[b][sb] = id;
+    } else if (op.pass == Pass::Backward) {
+      if (tmpsim::is_comm(op.kind)) last_bwd_comm[b] = id;
+      if (op.kind == OpKind::BackwardCompute) {
+        last_bwd_compute[b] = id;
+        if (first_bwd[b][sb] < 0) first_bwd[b][sb] = id;
+      }
+    }
+  }
+  for (const ExecOp& e : ops_)
+    if (e.kind == OpKind::RecomputeCompute && e.rebuild_x && e.block > 0 &&
+        stack_.degree(e.block) != stack_.degree(e.block - 1))
+      throw ConfigError("plan_bind: the recompute of block " + std::to_string(e.block) +
+                        " rebuilds x_b from a replayed AllReduce across a degree change (keep x_b: an Oases or "
+                        "policy plan storing it)");
+  struct Reshard {
+    int after;
+    std::array<int, 2> gates;
+    bool fwd;
+    int block;  // v (forward) or u (backward)
+  };
+  std::vector<Reshard> rs;
+  for (int v = 0; v + 1 < B; ++v) {
+    const int u = v + 1, dv = stack_.degree(v), du = stack_.degree(u);
+    if (dv == du) continue;
+    if (dv < du) {
+      if (last_fwd_comm[static_cast<size_t>(v)] >= 0)
+        rs.push_back({last_fwd_comm[static_cast<size_t>(v)], first_fwd[static_cast<size_t>(u)], true, v});
+    } else {
+      const int anchor = last_bwd_comm[static_cast<size_t>(u)] >= 0 ? last_bwd_comm[static_cast<size_t>(u)]
+                                                                     : last_bwd_compute[static_cast<size_t>(u)];
+      if (anchor >= 0) rs.push_back({anchor, first_bwd[static_cast<size_t>(v)], false, u});
+    }
+  }
+  nreshard_ = static_cast<int>(rs.size());
+  if (rs.empty()) return;
+  std::map<int, size_t> pos;  // plan id -> index in ops_
+  for (size_t i = 0; i < ops_.size(); ++i) pos[ops_[i].id] = i;
+  std::vector<std::vector<ExecOp>> after(ops_.size());
+  for (int r = 0; r < nreshard_; ++r) {
+    const Reshard& x = rs[static_cast<size_t>(r)];
+    ExecOp e;
+    e.id = n + r;
+    e.kind = OpKind::AllGather;
+    e.pass = x.fwd ? Pass::Forward : Pass::Backward;
+    e.stream = 1;
+    e.block = x.block;
+    if (ops_[pos[x.after]].stream == 0) e.waits.push_back(x.after);  // comm anchors: same stream, in order
+    after[pos[x.after]].push_back(e);
+    for (int g : x.gates) {
+      if (g < 0) continue;
+      ExecOp& go = ops_[pos[g]];
+      go.waits.push_back(n + r);
+    }
+    // F_u builds no x_u of its own; B_v starts from the gathered gradient
+    for (ExecOp& o : ops_) {
+      if (x.fwd && o.kind == OpKind::ForwardCompute && o.block == x.block + 1) o.with_bdr = false;
+      if (!x.fwd && o.kind == OpKind::BackwardCompute && o.block == x.block - 1) o.g_ready = true;
+    }
+  }
+  std::vector<ExecOp> merged;
+  for (size_t i = 0; i < ops_.size(); ++i) {
+    merged.push_back(ops_[i]);
+    for (ExecOp& e : after[i]) merged.push_back(e);
+  }
+  // Host issue order: a gated compute op can precede its AllGather's anchor in
+  // plan order (F_u^0 before AR_v^1 in the weave), and a stream wait needs the
+  // event recorded first. Re-interleave the two streams' in-order queues,
+  // taking at each step the earliest head whose waits are already issued; the
+  // order WITHIN each stream is the plan's.
+  std::deque<ExecOp> q[2];
+  for (size_t i = 0; i < merged.size(); ++i) {
+    merged[i].seq = static_cast<int>(i);
+    q[merged[i].stream].push_back(std::move(merged[i]));
+  }
+  std::set<int> issued;
+  ops_.clear();
+  auto ready = [&](const ExecOp& e) {
+    for (int d : e.waits)
+      if (!issued.count(d)) return false;
+    return true;
+  };
+  while (!q[0].empty() || !q[1].empty()) {
+    int pick = -1;
+    for (int st = 0; st < 2; ++st)
+      if (!q[st].empty() && ready(q[st].front()) &&
+          (pick < 0 || q[st].front().seq < q[pick].front().seq))
+        pick = st;
+    if (pick < 0) throw ConfigError("plan_bind: the resharding AllGathers make the stream dependencies cyclic");
+    issued.insert(q[pick].front().id);
+    ops_.push_back(std::move(q[pick].front()));
+    q[pick].pop_front();
+  }
 }
 
 Executor::~Executor() {
@@ -216,16 +325,19 @@ void Executor::issue(bool trace) {
     cudaStream_t s = op.stream ? c.comm : c.compute;
     for (int d : op.waits) check_cuda(cudaStreamWaitEvent(s, t1_[static_cast<size_t>(d)], 0), "wait");
     if (trace) check_cuda(cudaEventRecord(t0_[static_cast<size_t>(op.id)], s), "record");
-    if (op.stream == 1) {
+    if (op.kind == OpKind::AllGather) {
+      if (op.pass == Pass::Forward) stack_.reshard_fwd(op.block);
+      else stack_.reshard_bwd(op.block);
+    } else if (op.stream == 1) {
       stack_.allreduce(op.pass, op.block, op.sb, op.both_halves);
     } else {
       const int sb0 = op.both_halves ? 0 : op.sb, sb1 = op.both_halves ? 1 : op.sb;
       for (int w = 0; w < W; ++w) {
         for (int sb = sb0; sb <= sb1; ++sb) {
           switch (op.kind) {
-            case OpKind::ForwardCompute: stack_.forward(w, op.block, sb, true, true); break;
+            case OpKind::ForwardCompute: stack_.forward(w, op.block, sb, op.with_bdr, true); break;
             case OpKind::RecomputeCompute: stack_.recompute(w, op.block, sb, op.rebuild_x, op.with_row); break;
-            case OpKind::BackwardCompute: stack_.backward(w, op.block, sb); break;
+            case OpKind::BackwardCompute: stack_.backward(w, op.block, sb, op.g_ready); break;
             default: break;
           }
         }
@@ -233,15 +345,21 @@ void Executor::issue(bool trace) {
     }
     check_cuda(cudaEventRecord(t1_[static_cast<size_t>(op.id)], s), "record");
   }
-  const int n = static_cast<int>(ops_.size());
+  const int n = static_cast<int>(ops_.size());  // plan ops + injected reshards
   for (int k = 0; k < 2; ++k) {
     const int wait = plan_.split_batch ? tail_wait_[static_cast<size_t>(k)] : tail_wait_[0];
-    if (wait >= 0 && ops_[static_cast<size_t>(wait)].stream == 1)
+    if (wait >= 0 && stream_of_[static_cast<size_t>(wait)] == 1)
       check_cuda(cudaStreamWaitEvent(c.compute, t1_[static_cast<size_t>(wait)], 0), "wait tail");
     if (trace) check_cuda(cudaEventRecord(t0_[static_cast<size_t>(n + k)], c.compute), "record");
     if (stack_.num_blocks() > 0)  // an empty stack has no LN_0 to run backward through
       for (int w = 0; w < W; ++w) stack_.tail(w, k);
     check_cuda(cudaEventRecord(t1_[static_cast<size_t>(n + k)], c.compute), "record");
+  }
+  if (stack_.mixed()) {
+    // data-parallel gradient sums of the blocks below the world degree
+    check_cuda(cudaEventRecord(fork_, c.compute), "record");
+    check_cuda(cudaStreamWaitEvent(c.comm, fork_, 0), "fork");
+    stack_.dp_reduce_grads();
   }
   check_cuda(cudaEventRecord(fork_, c.comm), "record");
   check_cuda(cudaStreamWaitEvent(c.compute, fork_, 0), "join");
@@ -320,7 +438,7 @@ tmpsim::SimResult Executor::step(bool trace) {
       float a = 0.f, b = 0.f;
       check_cuda(cudaEventElapsedTime(&a, begin_, t0_[static_cast<size_t>(i)]), "elapsed");
       check_cuda(cudaEventElapsedTime(&b, begin_, t1_[static_cast<size_t>(i)]), "elapsed");
-      const int stream = i < n ? ops_[static_cast<size_t>(i)].stream : 0;
+      const int stream = i < n ? stream_of_[static_cast<size_t>(i)] : 0;
       const double s0 = a * 1e-3, s1 = std::max(a, b) * 1e-3;
       events_.push_back({i, stream, s0, s1});
       r.trace.push_back({i, stream ? tmpsim::Stream::Comm : tmpsim::Stream::Compute, s0, s1});

@@ -20,6 +20,7 @@
 // order; column reductions (bias, LN gamma/beta) are deterministic.
 #include "stack.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -139,7 +140,7 @@ oases_gemm_operand operand(const void* ptr, int64_t rows, int64_t cols, int64_t 
 }
 }  // namespace
 
-Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
+Stack::Stack(Context& ctx, const ModelCfg& cfg, const std::vector<int>& degrees) : ctx_(ctx), cfg_(cfg) {
   const int t = ctx.tp;
   if (cfg.h <= 0 || cfg.s <= 0 || cfg.b <= 0 || cfg.layers < 0) throw ConfigError("stack: sizes must be positive");
   if (cfg.b % 2) throw ConfigError("stack: global_batch must be even (two sub-batches)");
@@ -148,29 +149,51 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
   if (cfg.bytes == 8 && (cfg.attention || cfg.ln || cfg.p_hidden > 0.f || cfg.p_attn > 0.f))
     throw ConfigError("stack: f64 mode runs the reference's toy FFN blocks (numerics.hpp:35-60): no attention, "
                       "LayerNorm or dropout");
-  if (cfg.f % t) throw ConfigError("stack: ffn hidden must be divisible by tp");
-  if (cfg.attention) {
-    if (cfg.heads < 1 || cfg.h % cfg.heads || cfg.heads % t)
-      throw ConfigError("stack: hidden % heads and heads % tp must be 0");
-  }
   // 16-byte vector loads in LayerNorm / softmax rows
   if ((cfg.ln && cfg.h % 8) || (cfg.attention && (cfg.s % 8 || cfg.h % 8)))
     throw ConfigError("stack: hidden (with LayerNorm/attention) and seq must be multiples of 8");
   nblocks_ = cfg.layers * (cfg.attention ? 2 : 1);
+  // per-block degrees (F2): each divides the world; a degree-d block runs on N/d
+  // data-parallel groups, each with an even number of samples (two sub-batches)
+  if (degrees.empty()) {
+    deg_.assign(static_cast<size_t>(nblocks_), t);
+  } else {
+    if (static_cast<int>(degrees.size()) != nblocks_)
+      throw ConfigError("stack: one degree per block (" + std::to_string(nblocks_) + ")");
+    deg_ = degrees;
+  }
+  for (int d : deg_) {
+    if (d < 1 || t % d) throw ConfigError("stack: every block degree must divide the world size " + std::to_string(t));
+    if ((static_cast<int64_t>(cfg.b) * d) % (2LL * t))
+      throw ConfigError("stack: a degree-" + std::to_string(d) + " block splits the micro-batch over " +
+                        std::to_string(t / d) + " groups of two sub-batches: global_batch * d / world must be even");
+    if (d != t) mixed_ = true;
+  }
+  if (mixed_ && cfg.p_hidden > 0.f)
+    throw ConfigError("stack: mixed per-block degrees need hidden_dropout 0 (hidden-dropout masks are keyed per "
+                      "sub-batch tensor, which the degree changes re-slice)");
+  if (mixed_ && ctx.comm_disabled) throw ConfigError("stack: mixed per-block degrees need the collectives");
+  if (mixed_ && cfg.bytes == 8) throw ConfigError("stack: mixed per-block degrees run in bf16 or f32");
   hl_ = cfg.attention ? cfg.heads / t : 0;
   dh_ = cfg.attention ? cfg.h / cfg.heads : 0;
   ncol_attn_ = cfg.attention ? 3 * hl_ * dh_ : 0;
   nrow_attn_ = cfg.attention ? hl_ * dh_ : 0;
   ncol_ffn_ = cfg.f / t;
   nrow_ffn_ = cfg.f / t;
-  if (dtype() == OASES_BF16) {
-    // tcgen05 tiles: K extents must be multiples of 64 (TMA zero-fill only at
-    // buffer edges), attention sequences whole 128-row tiles.
-    const int64_t k_dims[] = {cfg.h, ncol_ffn_, tokens_sub()};
-    for (int64_t k : k_dims)
-      if (k % 64) throw ConfigError("stack: bf16 mode needs hidden, ffn/tp and tokens per sub-batch % 64 == 0");
-    if (cfg.attention && (cfg.s % 128 || dh_ % 64 || nrow_attn_ % 64))
-      throw ConfigError("stack: bf16 attention needs seq % 128 == 0 and head dim % 64 == 0");
+  for (int b = 0; b < nblocks_; ++b) {
+    const int d = degree(b);
+    if (cfg.f % d) throw ConfigError("stack: ffn hidden must be divisible by the block degree");
+    if (cfg.attention && (cfg.heads < 1 || cfg.h % cfg.heads || cfg.heads % d))
+      throw ConfigError("stack: hidden % heads and heads % degree must be 0");
+    if (dtype() == OASES_BF16) {
+      // tcgen05 tiles: K extents must be multiples of 64 (TMA zero-fill only at
+      // buffer edges), attention sequences whole 128-row tiles.
+      const int64_t k_dims[] = {cfg.h, cfg.f / d, ts(b)};
+      for (int64_t k : k_dims)
+        if (k % 64) throw ConfigError("stack: bf16 mode needs hidden, ffn/degree and tokens per sub-batch % 64 == 0");
+      if (cfg.attention && (cfg.s % 128 || dh_ % 64 || nrow(b) % 64))
+        throw ConfigError("stack: bf16 attention needs seq % 128 == 0 and head dim % 64 == 0");
+    }
   }
   // Fused bias-dropout-residual + LayerNorm unless OASES_FUSED_BDR_LN=0 (A/B runs).
   {
@@ -187,8 +210,9 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
   // FFN column-bias gradient from the FC2 dgrad epilogue's partials unless OASES_FUSED_COLSUM=0
   {
     const char* e = std::getenv("OASES_FUSED_COLSUM");
-    colsum_ = cfg.bias && cfg.bytes == 2 && (static_cast<int64_t>(cfg.b / 2) * cfg.s) % 32 == 0 &&
-              ncol_ffn_ % 32 == 0 && !(e && e[0] == '0');
+    colsum_ = cfg.bias && cfg.bytes == 2 && !(e && e[0] == '0');
+    for (int b = 0; b < nblocks_; ++b)
+      if (!is_attention(b) && (ts(b) % 32 || ncol(b) % 32)) colsum_ = false;
   }
   // Fused tcgen05 attention unless OASES_FUSED_ATTN=0 (A/B runs of the unfused chain).
   {
@@ -202,10 +226,27 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg) : ctx_(ctx), cfg_(cfg) {
   touched_.assign(static_cast<size_t>(W), std::vector<std::array<bool, OASES_P_COUNT>>(static_cast<size_t>(nblocks_)));
   bwd_seen_.assign(static_cast<size_t>(W), std::vector<bool>(static_cast<size_t>(nblocks_), false));
   loss_touched_.assign(static_cast<size_t>(W), false);
+  computed_at_.assign(static_cast<size_t>(nblocks_), {});
+  // NCCL sub-communicators of the mixed degrees, split in the same order on every rank
+  if (mixed_ && ctx.local_workers == 1 && ctx.nccl) {
+    std::vector<int> ds(deg_.begin(), deg_.end());
+    std::sort(ds.begin(), ds.end());
+    ds.erase(std::unique(ds.begin(), ds.end()), ds.end());
+    for (int d : ds) {
+      if (d == t) continue;
+      ncclComm_t c = nullptr;
+      check_nccl(ncclCommSplit(ctx.nccl, ctx.rank / d, ctx.rank % d, &c, nullptr), "ncclCommSplit (tp group)");
+      tp_comms_.emplace_back(d, c);
+      check_nccl(ncclCommSplit(ctx.nccl, ctx.rank % d, ctx.rank / d, &c, nullptr), "ncclCommSplit (dp group)");
+      dp_comms_.emplace_back(d, c);
+    }
+  }
 }
 
 Stack::~Stack() {
   for (cudaEvent_t e : tev_) cudaEventDestroy(e);
+  for (auto& c : tp_comms_) ncclCommDestroy(c.second);
+  for (auto& c : dp_comms_) ncclCommDestroy(c.second);
 }
 
 void Stack::kernel_stats(double* gemm_ms, double* gemm_flops, int* launches) {
@@ -231,25 +272,46 @@ void* Stack::half(void* base, int sb, int64_t cols) const {
   return static_cast<char*>(base) + static_cast<size_t>(sb) * tokens_sub() * cols * esize();
 }
 
+void* Stack::gp(void* base, const Worker& w, int b, int sb, int64_t cols) const {
+  return static_cast<char*>(base) + static_cast<size_t>(row0(w, b) + sb * ts(b)) * cols * esize();
+}
+
+void* Stack::lp(void* base, int b, int sb, int64_t cols) const {
+  return static_cast<char*>(base) + static_cast<size_t>(sb) * ts(b) * cols * esize();
+}
+
 void Stack::alloc_all() {
-  const int64_t Ts = tokens_sub(), T = 2 * Ts, h = cfg_.h;
+  const int64_t T = static_cast<int64_t>(cfg_.b) * cfg_.s, h = cfg_.h;
   const size_t es = esize();
-  const int64_t ncol_max = std::max(ncol_attn_, ncol_ffn_), nrow_max = std::max(nrow_attn_, nrow_ffn_);
+  // Per-rank extents: a block's tokens per sub-batch grow with its degree while
+  // its column widths shrink, so the workspaces are sized by the largest
+  // products over the blocks (all equal when the degrees are uniform).
+  int64_t Ts = 0, tcol = 0, trow = 0, tffn = 0;
+  for (int b = 0; b < nblocks_; ++b) {
+    Ts = std::max(Ts, ts(b));
+    tcol = std::max(tcol, ts(b) * ncol(b));
+    trow = std::max(trow, ts(b) * std::max<int64_t>(nrow(b), 1));
+    if (!is_attention(b)) tffn = std::max(tffn, ts(b) * ncol(b));
+  }
+  if (nblocks_ == 0) Ts = tokens_sub();
+  // the attention extents (samples x local heads) do not depend on the degree
   const int64_t bh = cfg_.b / 2;
   const int64_t prob = cfg_.attention ? bh * hl_ * cfg_.s * static_cast<int64_t>(cfg_.s) : 0;
   const int nslots = cfg_.recompute ? std::min(2, nblocks_) : nblocks_;
+  size_t colws = colsum_workspace(2 * Ts, static_cast<int>(h));
+  for (int b = 0; b < nblocks_; ++b)
+    colws = std::max(colws, colsum_workspace(2 * ts(b), static_cast<int>(std::max<int64_t>(ncol(b), 1))));
   for (Worker& w : workers_) {
     w.params.resize(static_cast<size_t>(nblocks_));
     for (int b = 0; b < nblocks_; ++b) {
       BlockParams& bp = w.params[static_cast<size_t>(b)];
-      const bool att = is_attention(b);
-      const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+      const int64_t nc = ncol(b), nr = nrow(b);
       bp.numel[OASES_P_LN_GAMMA] = cfg_.ln ? h : 0;
       bp.numel[OASES_P_LN_BETA] = cfg_.ln ? h : 0;
-      bp.numel[OASES_P_W_COL] = ncol * h;
-      bp.rows[OASES_P_W_COL] = static_cast<int>(ncol);
-      bp.numel[OASES_P_B_COL] = cfg_.bias ? ncol : 0;
-      bp.numel[OASES_P_W_ROW] = h * nrow;
+      bp.numel[OASES_P_W_COL] = nc * h;
+      bp.rows[OASES_P_W_COL] = static_cast<int>(nc);
+      bp.numel[OASES_P_B_COL] = cfg_.bias ? nc : 0;
+      bp.numel[OASES_P_W_ROW] = h * nr;
       bp.rows[OASES_P_W_ROW] = static_cast<int>(h);
       bp.numel[OASES_P_B_ROW] = cfg_.bias ? h : 0;
       for (int p = 0; p < OASES_P_COUNT; ++p) {
@@ -263,34 +325,28 @@ void Stack::alloc_all() {
     }
     w.input = arena_.alloc(static_cast<size_t>(T * h) * es);
     w.grad = arena_.alloc(static_cast<size_t>(T * h) * es);
-    // x_0 aliases the input; the other residual-stream buffers are placed by
+    // x_0 is the input; the other residual-stream buffers are placed by
     // bind_storage (all dedicated until a plan is bound)
-    w.xs.assign(static_cast<size_t>(nblocks_), {nullptr, nullptr});
-    w.x_own.assign(static_cast<size_t>(nblocks_), {nullptr, nullptr});
-    if (nblocks_ > 0) w.xs[0] = w.x_own[0] = {half(w.input, 0, h), half(w.input, 1, h)};
+    w.xbase.assign(static_cast<size_t>(nblocks_), nullptr);
+    w.x_own.assign(static_cast<size_t>(nblocks_), nullptr);
+    if (nblocks_ > 0) w.xbase[0] = w.x_own[0] = w.input;
     for (int par = 0; par < 2; ++par) {
-      void* f = arena_.alloc(static_cast<size_t>(T * h) * es);
-      void* bb = arena_.alloc(static_cast<size_t>(T * h) * es);
-      w.fwd_ar[par] = {half(f, 0, h), half(f, 1, h)};
-      w.bwd_ar[par] = {half(bb, 0, h), half(bb, 1, h)};
-      if (cfg_.recompute) {
-        void* r = arena_.alloc(static_cast<size_t>(T * h) * es);
-        w.rec_ar[par] = {half(r, 0, h), half(r, 1, h)};
-      }
+      w.fwd_ar[par] = arena_.alloc(static_cast<size_t>(T * h) * es);
+      w.bwd_ar[par] = arena_.alloc(static_cast<size_t>(T * h) * es);
+      if (cfg_.recompute) w.rec_ar[par] = arena_.alloc(static_cast<size_t>(T * h) * es);
     }
     w.ws.resize(static_cast<size_t>(nslots));
+    w.ln_full.assign(static_cast<size_t>(nslots), nullptr);
+    w.act_full.assign(static_cast<size_t>(nslots), nullptr);
     for (int slot = 0; slot < nslots; ++slot) {
       // the weight-gradient GEMMs read the two sub-batches' LN output and
       // activation as one [2 T_sub, .] operand: both halves of a slot are one
-      // allocation (slot parity == block parity, so its row width is fixed)
-      const int64_t slot_nrow = is_attention(slot) ? nrow_attn_ : nrow_ffn_;
-      void* ln_full = cfg_.ln ? arena_.alloc(static_cast<size_t>(2 * Ts * h) * es) : nullptr;
-      void* act_full = arena_.alloc(static_cast<size_t>(2 * Ts * std::max<int64_t>(slot_nrow, 1)) * es);
+      // allocation (ws_for points ws.ln / ws.act at the block's halves)
+      w.ln_full[static_cast<size_t>(slot)] = cfg_.ln ? arena_.alloc(static_cast<size_t>(2 * Ts * h) * es) : nullptr;
+      w.act_full[static_cast<size_t>(slot)] = arena_.alloc(static_cast<size_t>(2 * trow) * es);
       for (int sb = 0; sb < 2; ++sb) {
         Workspace& ws = w.ws[static_cast<size_t>(slot)][static_cast<size_t>(sb)];
-        ws.ln = ln_full ? half(ln_full, sb, h) : nullptr;
-        ws.col = arena_.alloc(static_cast<size_t>(Ts * ncol_max) * es);
-        ws.act = half(act_full, sb, slot_nrow);
+        ws.col = arena_.alloc(static_cast<size_t>(tcol) * es);
         if (prob && fused_attn_) {
           ws.lse = static_cast<float*>(arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float)));
         } else if (prob) {
@@ -300,8 +356,8 @@ void Stack::alloc_all() {
       }
     }
     w.gar = arena_.alloc(static_cast<size_t>(2 * Ts * h) * es);  // [sb][T_sub, h]
-    w.du = arena_.alloc(static_cast<size_t>(Ts * nrow_max) * es);
-    w.dcol = arena_.alloc(static_cast<size_t>(2 * Ts * ncol_max) * es);  // [sb][T_sub, ncol] of the block
+    w.du = arena_.alloc(static_cast<size_t>(trow) * es);
+    w.dcol = arena_.alloc(static_cast<size_t>(2 * tcol) * es);  // [sb][T_sub, ncol] of the block
     if (prob) w.dp = arena_.alloc(static_cast<size_t>(prob) * es);
     if (prob && fused_attn_) w.attn_ws = arena_.alloc(static_cast<size_t>(bh * hl_ * cfg_.s) * sizeof(float));
     if (hbits_) {
@@ -322,20 +378,18 @@ void Stack::alloc_all() {
         for (int sb = 0; sb < 2; ++sb)
           w.mask_bits[static_cast<size_t>(b / 2)][static_cast<size_t>(sb)] = static_cast<uint32_t*>(arena_.alloc(mbytes));
     }
-    w.y = arena_.alloc(static_cast<size_t>(2 * Ts * h) * es);
+    w.y = arena_.alloc(static_cast<size_t>(T * h) * es);
     // row statistics of both sub-batches (the parameter pass runs once over 2 T_sub rows)
     w.ln_ws = arena_.alloc(layernorm_bwd_workspace(2 * Ts, static_cast<int>(h)));
     // [2 sub-batches][partial rows][3][h] column partials of the persistent LayerNorm backward
     if (lnp_bwd_)
       w.lnp_part = static_cast<float*>(arena_.alloc(
           static_cast<size_t>(2 * lnp_partial_rows_max(Ts, static_cast<int>(h)) * 3 * h) * sizeof(float)));
-    w.col_ws = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
-                                     colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
-    w.col_ws2 = arena_.alloc(std::max(colsum_workspace(2 * Ts, static_cast<int>(h)),
-                                      colsum_workspace(2 * Ts, static_cast<int>(std::max<int64_t>(ncol_max, 1)))));
+    w.col_ws = arena_.alloc(colws);
+    w.col_ws2 = arena_.alloc(colws);
     // [2 T_sub / 32, ncol_ffn] partials of the fused FFN column-bias gradient (own buffer: the
     // attention blocks' side-stream column sums may run between the two sub-batches' FC2 dgrads)
-    w.col_part = colsum_ ? static_cast<float*>(arena_.alloc(static_cast<size_t>(2 * Ts / 32 * ncol_ffn_) * sizeof(float)))
+    w.col_part = colsum_ ? static_cast<float*>(arena_.alloc(static_cast<size_t>(2 * tffn / 32) * sizeof(float)))
                          : nullptr;
     w.loss = static_cast<double*>(arena_.alloc(sizeof(double)));
     w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
@@ -348,7 +402,7 @@ void Stack::alloc_all() {
 
 void Stack::bind_storage(const std::vector<bool>& stored) {
   if (static_cast<int>(stored.size()) != nblocks_) throw ConfigError("bind_storage: one flag per block");
-  const int64_t T = 2 * tokens_sub(), h = cfg_.h;
+  const int64_t T = static_cast<int64_t>(cfg_.b) * cfg_.s, h = cfg_.h;
   const size_t bytes = static_cast<size_t>(T * h) * esize();
   // buffers the previous plan needed and this one does not are freed, so the
   // reported device bytes are those of the bound plan (a rebound stack measures
@@ -358,44 +412,43 @@ void Stack::bind_storage(const std::vector<bool>& stored) {
   for (int b = 1; b < nblocks_; ++b) any_scratch = any_scratch || !stored[static_cast<size_t>(b)];
   for (Worker& w : workers_) {
     for (int b = 1; b < nblocks_; ++b) {
-      auto& own = w.x_own[static_cast<size_t>(b)];
+      void*& own = w.x_own[static_cast<size_t>(b)];
       if (stored[static_cast<size_t>(b)]) {
-        if (!own[0]) {
-          void* base = arena_.alloc(bytes);
-          own = {half(base, 0, h), half(base, 1, h)};
-        }
-        w.xs[static_cast<size_t>(b)] = own;
+        if (!own) own = arena_.alloc(bytes);
+        w.xbase[static_cast<size_t>(b)] = own;
       } else {
-        if (own[0]) {
-          arena_.release(own[0]);
-          own = {nullptr, nullptr};
+        if (own) {
+          arena_.release(own);
+          own = nullptr;
         }
-        if (!w.x_scratch[0]) {
-          void* base = arena_.alloc(bytes);
-          w.x_scratch = {half(base, 0, h), half(base, 1, h)};
-        }
-        w.xs[static_cast<size_t>(b)] = w.x_scratch;
+        if (!w.x_scratch) w.x_scratch = arena_.alloc(bytes);
+        w.xbase[static_cast<size_t>(b)] = w.x_scratch;
       }
     }
-    if (!any_scratch && w.x_scratch[0]) {
-      arena_.release(w.x_scratch[0]);
-      w.x_scratch = {nullptr, nullptr};
+    if (!any_scratch && w.x_scratch) {
+      arena_.release(w.x_scratch);
+      w.x_scratch = nullptr;
     }
   }
   x_stored_ = stored;
   if (nblocks_ > 0) x_stored_[0] = true;
 }
 
-Workspace& Stack::ws_for(Worker& w, int block, int sb) {
-  const size_t slot = cfg_.recompute ? static_cast<size_t>(block % 2) : static_cast<size_t>(block);
-  return w.ws[std::min(slot, w.ws.size() - 1)][static_cast<size_t>(sb)];
+Workspace Stack::ws_for(Worker& w, int block, int sb) {
+  size_t slot = cfg_.recompute ? static_cast<size_t>(block % 2) : static_cast<size_t>(block);
+  slot = std::min(slot, w.ws.size() - 1);
+  Workspace ws = w.ws[slot][static_cast<size_t>(sb)];
+  ws.ln = w.ln_full[slot] ? lp(w.ln_full[slot], block, sb, cfg_.h) : nullptr;
+  ws.act = lp(w.act_full[slot], block, sb, std::max<int64_t>(nrow(block), 1));
+  return ws;
 }
 
-bool Stack::touch(const Worker& w, int block, int p) {
+bool Stack::touch(const Worker& w, int block, int p, int computed_at) {
   const size_t wi = static_cast<size_t>(&w - workers_.data());
   bool& t = touched_[wi][static_cast<size_t>(block)][static_cast<size_t>(p)];
   const bool was = t;
   t = true;
+  computed_at_[static_cast<size_t>(block)][static_cast<size_t>(p)] = computed_at ? computed_at : degree(block);
   return was;
 }
 
@@ -404,6 +457,7 @@ void Stack::begin_step() {
     for (auto& a : per_worker) a.fill(false);
   for (auto& per_worker : bwd_seen_) std::fill(per_worker.begin(), per_worker.end(), false);
   std::fill(loss_touched_.begin(), loss_touched_.end(), false);
+  for (auto& a : computed_at_) a.fill(0);
 }
 
 // GEMM timing events: plain records when issued eagerly; external event-record
@@ -499,11 +553,11 @@ void Stack::join_side() {
 // fused HBM pass where the row-group kernel covers the shape (its LN is
 // bit-identical to ln_fwd of the stored x_b), else the two kernels.
 void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln, bool store_bits) {
-  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  const int64_t Ts = ts(block), h = cfg_.h;
   const BlockParams& prev = w.params[static_cast<size_t>(block - 1)];
   const BlockParams& bp = w.params[static_cast<size_t>(block)];
   const void* bias = cfg_.bias ? prev.p[OASES_P_B_ROW] : nullptr;
-  const void* res = cfg_.residual ? w.xs[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr;
+  const void* res = cfg_.residual ? gp(w.xbase[static_cast<size_t>(block - 1)], w, block, sb, h) : nullptr;
   if (cfg_.ln && fuse_bdr_ln_ && bdr_layernorm_supported(Ts, static_cast<int>(h))) {
     uint16_t* bits = store_bits && hbits_ ? w.hbits[static_cast<size_t>(block - 1)][static_cast<size_t>(sb)] : nullptr;
     check_cuda(bias_dropout_residual_layernorm_fwd(dtype(), ar, bias, res, x, bp.p[OASES_P_LN_GAMMA],
@@ -518,11 +572,11 @@ void Stack::bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, v
                                        drop_offset(block - 1, sb, 0), ctx_.compute),
              "bdr_fwd");
   ++launches_;
-  if (cfg_.ln) ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ln);
+  if (cfg_.ln) ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ln, Ts);
 }
 
-void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y) {
-  check_cuda(layernorm_fwd(dtype(), x, g, b, y, tokens_sub(), cfg_.h, cfg_.eps, ctx_.compute, ctx_.gemm_max_ctas),
+void Stack::ln_fwd(const void* x, const void* g, const void* b, void* y, int64_t rows) {
+  check_cuda(layernorm_fwd(dtype(), x, g, b, y, rows, cfg_.h, cfg_.eps, ctx_.compute, ctx_.gemm_max_ctas),
              "layernorm_fwd");
   ++launches_;
 }
@@ -593,11 +647,12 @@ void Stack::init_random(uint64_t seed) {
   // W_row U(+-1/sqrt(fan_in)); LN gamma 1, beta 0, biases 0.
   const int64_t T = 2 * tokens_sub();
   for (Worker& w : workers_) {
-    const uint64_t wr = static_cast<uint64_t>(w.rank);
     check_cuda(fill_uniform(dtype(), w.input, T * cfg_.h, 1.f, seed, 0x1000000, ctx_.compute), "init input");
     for (int b = 0; b < nblocks_; ++b) {
       BlockParams& bp = w.params[static_cast<size_t>(b)];
-      const uint64_t off = 0x2000000 + (static_cast<uint64_t>(b) * 64 + wr) * 8;
+      // the shard is keyed by the rank in the block's group: data-parallel groups of
+      // a lower-degree block hold identical replicas
+      const uint64_t off = 0x2000000 + (static_cast<uint64_t>(b) * 64 + static_cast<uint64_t>(rig(w, b))) * 8;
       check_cuda(fill_uniform(dtype(), bp.p[OASES_P_W_COL], bp.numel[OASES_P_W_COL],
                               1.f / std::sqrt(static_cast<float>(cfg_.h)), seed, off, ctx_.compute),
                  "init w_col");
@@ -669,7 +724,21 @@ void download(const void* dev, int dtype, int64_t n, double* host) {
 }
 }  // namespace
 
-void Stack::get_input_grad(double* host) { download(workers_[0].grad, dtype(), 2 * tokens_sub() * cfg_.h, host); }
+void Stack::get_input_grad(double* host) {
+  // dX rows of each data-parallel group of block 0 (its rank 0 holds them)
+  const int64_t h = cfg_.h;
+  if (nblocks_ == 0 || degree(0) == world() || workers_.size() == 1) {
+    download(workers_[0].grad, dtype(), 2 * tokens_sub() * h, host);
+    return;
+  }
+  const int64_t rows = 2 * ts(0);
+  for (const Worker& w : workers_) {
+    if (rig(w, 0) != 0) continue;
+    const int64_t r0 = row0(w, 0);
+    download(static_cast<const char*>(w.grad) + static_cast<size_t>(r0 * h) * esize(), dtype(), rows * h,
+             host + r0 * h);
+  }
+}
 
 void Stack::get_activation(int worker, int block, int sb, double* host) {
   if (block >= 0 && block < nblocks_ && !x_stored_[static_cast<size_t>(block)])
@@ -678,39 +747,64 @@ void Stack::get_activation(int worker, int block, int sb, double* host) {
   if (worker < 0 || worker >= num_workers() || block < 0 || block > nblocks_ || sb < 0 || sb > 1)
     throw ConfigError("get_activation: index out of range");
   Worker& w = workers_[static_cast<size_t>(worker)];
+  // rows of sub-batch sb of the block's group of this worker (T_sub of a uniform stack)
   if (block == nblocks_) {
-    download(half(w.y, sb, cfg_.h), dtype(), tokens_sub() * cfg_.h, host);  // x_B, the stack's output
+    const int last = nblocks_ - 1;  // x_B, the stack's output
+    download(gp(w.y, w, last, sb, cfg_.h), dtype(), ts(last) * cfg_.h, host);
     return;
   }
-  download(w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)], dtype(), tokens_sub() * cfg_.h, host);
+  download(gp(w.xbase[static_cast<size_t>(block)], w, block, sb, cfg_.h), dtype(), ts(block) * cfg_.h, host);
 }
 
 double Stack::read_loss() {
+  // in-process: one value per data-parallel group of the last block (its rank 0),
+  // summed; one rank per process: this rank's group's value
   double l = 0.0;
-  check_cuda(cudaMemcpy(&l, workers_[0].loss, sizeof(double), cudaMemcpyDeviceToHost), "loss D2H");
+  for (const Worker& w : workers_) {
+    if (workers_.size() > 1 && nblocks_ > 0 && rig(w, nblocks_ - 1) != 0) continue;
+    double v = 0.0;
+    check_cuda(cudaMemcpy(&v, w.loss, sizeof(double), cudaMemcpyDeviceToHost), "loss D2H");
+    l += v;
+    if (nblocks_ == 0) break;
+  }
   return l;
 }
 
 // ------------------------------------------------------------------ attention
+// Attention-dropout keys of a sub-batch tensor: the key
+// sub-batch is the half of the micro-batch holding its samples and sample
+// n of the tensor is sample n0 + n there, so the masks do not depend on the
+// block's degree (data-parallel groups of a mixed-degree stack hold slices).
+namespace {
+struct AttnKey {
+  int sb_key;
+  int n0;
+};
+}  // namespace
+static AttnKey attn_key(int64_t first_sample, int64_t half_batch) {
+  return {static_cast<int>(first_sample / half_batch), static_cast<int>(first_sample % half_batch)};
+}
+
 oases_attn_desc Stack::attn_desc(Worker& w, int block, int sb, const Workspace& ws) {
   oases_attn_desc a{};
+  const int64_t nc = ncol(block), nr = nrow(block);
   a.dtype = dtype();
-  a.samples = static_cast<int>(cfg_.b / 2);
-  a.heads_local = hl_;
+  a.samples = static_cast<int>(bsub(block));
+  a.heads_local = hl(block);
   a.heads_total = static_cast<int>(cfg_.heads);
-  a.head_offset = w.rank * hl_;
+  a.head_offset = rig(w, block) * hl(block);
   a.head_dim = dh_;
   a.seq = static_cast<int>(cfg_.s);
   a.max_ctas = ctx_.gemm_max_ctas;
   a.qkv = ws.col;
-  a.ld_qkv = ncol_attn_;
+  a.ld_qkv = nc;
   a.out = ws.act;
-  a.ld_out = nrow_attn_;
+  a.ld_out = nr;
   a.lse = ws.lse;
   a.dout = w.du;
-  a.ld_dout = nrow_attn_;
-  a.dqkv = half(w.dcol, sb, ncol_attn_);
-  a.ld_dqkv = ncol_attn_;
+  a.ld_dout = nr;
+  a.dqkv = lp(w.dcol, block, sb, nc);
+  a.ld_dqkv = nc;
   a.ds = w.dp;
   a.workspace = w.attn_ws;
   // keep-bit cache unless OASES_ATTN_MASK_CACHE=0 (A/B runs: Philox in every pass)
@@ -723,13 +817,19 @@ oases_attn_desc Stack::attn_desc(Worker& w, int block, int sb, const Workspace& 
   a.scale = 1.f / std::sqrt(static_cast<float>(dh_));
   a.dropout_p = cfg_.p_attn;
   a.seed = cfg_.seed;
-  a.offset = drop_offset(block, sb, 1);
+  const AttnKey k = attn_key(row0(w, block) / cfg_.s + sb * bsub(block), cfg_.b / 2);
+  a.offset = drop_offset(block, k.sb_key, 1);
+  a.sample_offset = k.n0;
   return a;
 }
 
 void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int mask_mode) {
-  const int64_t s = cfg_.s, Ts = tokens_sub(), bh = cfg_.b / 2, Z = bh * hl_, nc = ncol_attn_, nr = nrow_attn_;
-  const int64_t hd = static_cast<int64_t>(hl_) * dh_;
+  const int hlb = hl(block);
+  const int64_t s = cfg_.s, Ts = ts(block), bh = bsub(block), Z = bh * hlb, nc = ncol(block), nr = nrow(block);
+  const int64_t hd = static_cast<int64_t>(hlb) * dh_;
+  const AttnKey key = attn_key(row0(w, block) / cfg_.s + sb * bh, cfg_.b / 2);
+  // unfused softmax: the sample offset of the dropout keys folds into the head offset
+  const int hoff = key.n0 * cfg_.heads + rig(w, block) * hlb;
   const char* qkv = static_cast<const char*>(ws.col);
   const size_t es = esize();
   if (fused_attn_) {
@@ -748,23 +848,23 @@ void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = s; d.N = s; d.K = dh_;
-  d.batch = Z; d.batch_inner = hl_;
+  d.batch = Z; d.batch_inner = hlb;
   d.a = operand(qkv, Ts, nc, nc, false, s, 0, 0, dh_);
   d.b = operand(qkv + hd * es, Ts, nc - hd, nc, false, s, 0, 0, dh_);
-  d.c = ws.p; d.ldc = s; d.c_row_off[0] = hl_ * s; d.c_row_off[1] = s;
+  d.c = ws.p; d.ldc = s; d.c_row_off[0] = hlb * s; d.c_row_off[1] = s;
   d.alpha = 1.f; d.causal = OASES_CAUSAL_SKIP_UPPER;
   gemm(d);
   check_cuda(softmax_fwd(dtype(), ws.p, ws.p, cfg_.p_attn > 0.f ? ws.pd : nullptr, Z, static_cast<int>(s),
-                         1.f / std::sqrt(static_cast<float>(dh_)), cfg_.p_attn, cfg_.seed, drop_offset(block, sb, 1),
-                         hl_, cfg_.heads, w.rank * hl_, ctx_.compute),
+                         1.f / std::sqrt(static_cast<float>(dh_)), cfg_.p_attn, cfg_.seed, drop_offset(block, key.sb_key, 1),
+                         hlb, cfg_.heads, hoff, ctx_.compute),
              "softmax_fwd");
   ++launches_;
   // ctx = P_drop V  (K limited to the causal prefix of each 128-row tile)
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = s; d.N = dh_; d.K = s;
-  d.batch = Z; d.batch_inner = hl_;
-  d.a = operand(ws.pd, Z * s, s, s, false, hl_ * s, s);
+  d.batch = Z; d.batch_inner = hlb;
+  d.a = operand(ws.pd, Z * s, s, s, false, hlb * s, s);
   d.b = operand(qkv + 2 * hd * es, Ts, nc - 2 * hd, nc, true, s, 0, 0, dh_);
   d.c = ws.act; d.ldc = nr; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
   d.alpha = 1.f; d.causal = OASES_CAUSAL_K_UPTO_M;
@@ -772,11 +872,14 @@ void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int
 }
 
 void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
-  const int64_t s = cfg_.s, Ts = tokens_sub(), bh = cfg_.b / 2, Z = bh * hl_, nc = ncol_attn_, nr = nrow_attn_;
-  const int64_t hd = static_cast<int64_t>(hl_) * dh_;
+  const int hlb = hl(block);
+  const int64_t s = cfg_.s, Ts = ts(block), bh = bsub(block), Z = bh * hlb, nc = ncol(block), nr = nrow(block);
+  const int64_t hd = static_cast<int64_t>(hlb) * dh_;
+  const AttnKey key = attn_key(row0(w, block) / cfg_.s + sb * bh, cfg_.b / 2);
+  const int hoff = key.n0 * cfg_.heads + rig(w, block) * hlb;
   const size_t es = esize();
   const char* qkv = static_cast<const char*>(ws.col);
-  char* dqkv = static_cast<char*>(half(w.dcol, sb, ncol_attn_));
+  char* dqkv = static_cast<char*>(lp(w.dcol, block, sb, nc));
   if (fused_attn_) {
     oases_attn_desc a = attn_desc(w, block, sb, ws);
     a.mask_mode = 2;                // the forward pass stored the keep bits
@@ -793,25 +896,25 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   // dP_drop = dctx V^T
   d.c_dtype = dtype();
   d.M = s; d.N = s; d.K = dh_;
-  d.batch = Z; d.batch_inner = hl_;
+  d.batch = Z; d.batch_inner = hlb;
   d.a = operand(w.du, Ts, nr, nr, false, s, 0, 0, dh_);
   d.b = operand(qkv + 2 * hd * es, Ts, nc - 2 * hd, nc, false, s, 0, 0, dh_);
-  d.c = w.dp; d.ldc = s; d.c_row_off[0] = hl_ * s; d.c_row_off[1] = s;
+  d.c = w.dp; d.ldc = s; d.c_row_off[0] = hlb * s; d.c_row_off[1] = s;
   d.alpha = 1.f; d.causal = OASES_CAUSAL_SKIP_UPPER;
   gemm(d);
   // dV = P_drop^T dctx
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = s; d.N = dh_; d.K = s;
-  d.batch = Z; d.batch_inner = hl_;
-  d.a = operand(ws.pd, Z * s, s, s, true, hl_ * s, s);
+  d.batch = Z; d.batch_inner = hlb;
+  d.a = operand(ws.pd, Z * s, s, s, true, hlb * s, s);
   d.b = operand(w.du, Ts, nr, nr, true, s, 0, 0, dh_);
   d.c = dqkv + 2 * hd * es; d.ldc = nc; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
   d.alpha = 1.f; d.causal = OASES_CAUSAL_K_FROM_M;
   gemm(d);
   // dS (in place over dP)
   check_cuda(softmax_bwd(dtype(), ws.p, w.dp, w.dp, Z, static_cast<int>(s), 1.f / std::sqrt(static_cast<float>(dh_)),
-                         cfg_.p_attn, cfg_.seed, drop_offset(block, sb, 1), hl_, cfg_.heads, w.rank * hl_,
+                         cfg_.p_attn, cfg_.seed, drop_offset(block, key.sb_key, 1), hlb, cfg_.heads, hoff,
                          ctx_.compute),
              "softmax_bwd");
   ++launches_;
@@ -819,8 +922,8 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = s; d.N = dh_; d.K = s;
-  d.batch = Z; d.batch_inner = hl_;
-  d.a = operand(w.dp, Z * s, s, s, false, hl_ * s, s);
+  d.batch = Z; d.batch_inner = hlb;
+  d.a = operand(w.dp, Z * s, s, s, false, hlb * s, s);
   d.b = operand(qkv + hd * es, Ts, nc - hd, nc, true, s, 0, 0, dh_);
   d.c = dqkv; d.ldc = nc; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
   d.alpha = 1.f; d.causal = OASES_CAUSAL_K_UPTO_M;
@@ -829,8 +932,8 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
   d = oases_gemm_desc{};
   d.c_dtype = dtype();
   d.M = s; d.N = dh_; d.K = s;
-  d.batch = Z; d.batch_inner = hl_;
-  d.a = operand(w.dp, Z * s, s, s, true, hl_ * s, s);
+  d.batch = Z; d.batch_inner = hlb;
+  d.a = operand(w.dp, Z * s, s, s, true, hlb * s, s);
   d.b = operand(qkv, Ts, nc, nc, true, s, 0, 0, dh_);
   d.c = dqkv + hd * es; d.ldc = nc; d.c_row_off[0] = s; d.c_col_off[1] = dh_;
   d.alpha = 1.f; d.causal = OASES_CAUSAL_K_FROM_M;
@@ -840,17 +943,17 @@ void Stack::attention_bwd(Worker& w, int block, int sb, const Workspace& ws) {
 // ------------------------------------------------------------------ plan ops
 void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
   Worker& w = workers_[static_cast<size_t>(wi)];
-  const int64_t Ts = tokens_sub(), h = cfg_.h;
-  void* x = w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)];
-  Workspace& ws = ws_for(w, block, sb);
+  const int64_t Ts = ts(block), h = cfg_.h;
+  void* x = gp(w.xbase[static_cast<size_t>(block)], w, block, sb, h);
+  Workspace ws = ws_for(w, block, sb);
   const BlockParams& bp = w.params[static_cast<size_t>(block)];
   const bool att = is_attention(block);
-  const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+  const int64_t ncol = this->ncol(block), nrow = this->nrow(block);
   const void* ln = x;
   if (block > 0 && with_bdr) {
-    bdr_then_ln(w, block, sb, w.fwd_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln, true);
+    bdr_then_ln(w, block, sb, gp(w.fwd_ar[(block - 1) % 2], w, block, sb, h), x, ws.ln, true);
   } else if (cfg_.ln) {
-    ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
+    ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln, Ts);
   }
   if (cfg_.ln) ln = ws.ln;
   oases_gemm_desc d{};
@@ -886,7 +989,7 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
     d.batch = 1; d.batch_inner = 1;
     d.a = operand(ws.act, Ts, nrow, nrow, false);
     d.b = operand(bp.p[OASES_P_W_ROW], h, nrow, nrow, false);
-    d.c = w.fwd_ar[block % 2][static_cast<size_t>(sb)];
+    d.c = gp(w.fwd_ar[block % 2], w, block, sb, h);
     d.ldc = h;
     d.alpha = 1.f;
     gemm(d);
@@ -895,20 +998,20 @@ void Stack::forward(int wi, int block, int sb, bool with_bdr, bool with_row) {
 
 void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) {
   Worker& w = workers_[static_cast<size_t>(wi)];
-  const int64_t Ts = tokens_sub(), h = cfg_.h;
-  void* x = w.xs[static_cast<size_t>(block)][static_cast<size_t>(sb)];
+  const int64_t Ts = ts(block), h = cfg_.h;
+  void* x = gp(w.xbase[static_cast<size_t>(block)], w, block, sb, h);
   // Same kernels as the forward from the stored x_b (or x_b rebuilt from the
   // replayed AllReduce); the row GEMM only when this variant replays the
   // block's AllReduce.
-  Workspace& ws = ws_for(w, block, sb);
+  Workspace ws = ws_for(w, block, sb);
   const BlockParams& bp = w.params[static_cast<size_t>(block)];
   const bool att = is_attention(block);
-  const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+  const int64_t ncol = this->ncol(block), nrow = this->nrow(block);
   const void* ln = x;
   if (rebuild_x && block > 0) {
-    bdr_then_ln(w, block, sb, w.rec_ar[(block - 1) % 2][static_cast<size_t>(sb)], x, ws.ln, false);
+    bdr_then_ln(w, block, sb, gp(w.rec_ar[(block - 1) % 2], w, block, sb, h), x, ws.ln, false);
   } else if (cfg_.ln) {
-    ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln);
+    ln_fwd(x, bp.p[OASES_P_LN_GAMMA], bp.p[OASES_P_LN_BETA], ws.ln, Ts);
   }
   if (cfg_.ln) ln = ws.ln;
   oases_gemm_desc d{};
@@ -937,20 +1040,19 @@ void Stack::recompute(int wi, int block, int sb, bool rebuild_x, bool with_row) 
     d.batch = 1; d.batch_inner = 1;
     d.a = operand(ws.act, Ts, nrow, nrow, false);
     d.b = operand(bp.p[OASES_P_W_ROW], h, nrow, nrow, false);
-    d.c = w.rec_ar[block % 2][static_cast<size_t>(sb)];
+    d.c = gp(w.rec_ar[block % 2], w, block, sb, h);
     d.ldc = h;
     d.alpha = 1.f;
     gemm(d);
   }
 }
 
-void Stack::backward(int wi, int block, int sb) {
+void Stack::backward(int wi, int block, int sb, bool g_ready) {
   Worker& w = workers_[static_cast<size_t>(wi)];
-  const int64_t Ts = tokens_sub(), h = cfg_.h;
+  const int64_t Ts = ts(block), h = cfg_.h;
   const int hi = static_cast<int>(h);
-  void* g = half(w.grad, sb, h);
-  const size_t usb = static_cast<size_t>(sb);
-  void* gar_sb = half(w.gar, sb, h);
+  void* g = gp(w.grad, w, block, sb, h);
+  void* gar_sb = lp(w.gar, block, sb, h);
   // The weight gradients of a block are computed once per step, by its second
   // backward call (the other sub-batch's), over both sub-batches at once:
   // K = 2 T_sub, no f32 read-modify-write of dW between the sub-batches.
@@ -959,11 +1061,15 @@ void Stack::backward(int wi, int block, int sb) {
   // 1. gradient arriving at x_{b+1}; with LayerNorm the same pass also writes
   //    g_ar = dropout'(g) (step 2) when the row-group kernel covers the width
   bool gar_done = false, row_bias_done = false;
-  if (block == nblocks_ - 1) {
+  if (g_ready) {
+    // reshard_bwd already gathered g + LN_{b+1}'(dln_{b+1}) over this block's slice
+  } else if (block == nblocks_ - 1) {
     const BlockParams& bp = w.params[static_cast<size_t>(block)];
-    void* y = half(w.y, sb, h);
-    check_cuda(bias_dropout_residual_fwd(dtype(), w.fwd_ar[block % 2][usb], cfg_.bias ? bp.p[OASES_P_B_ROW] : nullptr,
-                                         cfg_.residual ? w.xs[static_cast<size_t>(block)][usb] : nullptr, y, Ts, hi,
+    void* y = gp(w.y, w, block, sb, h);
+    check_cuda(bias_dropout_residual_fwd(dtype(), gp(w.fwd_ar[block % 2], w, block, sb, h),
+                                         cfg_.bias ? bp.p[OASES_P_B_ROW] : nullptr,
+                                         cfg_.residual ? gp(w.xbase[static_cast<size_t>(block)], w, block, sb, h) : nullptr,
+                                         y, Ts, hi,
                                          cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0), ctx_.compute),
                "bdr_fwd (loss head)");
     const bool acc = loss_touched_[static_cast<size_t>(wi)];
@@ -972,17 +1078,17 @@ void Stack::backward(int wi, int block, int sb) {
     launches_ += 3;
   } else {
     const BlockParams& nxt = w.params[static_cast<size_t>(block + 1)];
-    const void* dln = w.bwd_ar[(block + 1) % 2][usb];
+    const void* dln = gp(w.bwd_ar[(block + 1) % 2], w, block, sb, h);
     if (cfg_.ln && lnp_bwd_) {
       // one persistent pass: dx (+ residual), g_ar = dropout'(dx) and this sub-batch's column
       // partials of dgamma/dbeta (block b+1) and of the row-bias gradient (block b)
-      const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
+      const void* xn = gp(w.xbase[static_cast<size_t>(block + 1)], w, block, sb, h);
       const bool drop = cfg_.p_hidden > 0.f;
       const int acc_dx = cfg_.residual ? 1 : 0;
       const long long prows = lnp_partial_rows(dtype(), Ts, hi, acc_dx, ctx_.gemm_max_ctas);
       check_cuda(lnp_layernorm_bwd(dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, acc_dx, drop ? gar_sb : nullptr,
                                    cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0),
-                                   drop && hbits_ ? w.hbits[static_cast<size_t>(block)][usb] : nullptr,
+                                   drop && hbits_ ? w.hbits[static_cast<size_t>(block)][static_cast<size_t>(sb)] : nullptr,
                                    w.lnp_part + static_cast<int64_t>(sb) * prows * 3 * h, nullptr, Ts, hi, cfg_.eps,
                                    ctx_.gemm_max_ctas, ctx_.compute),
                  "layernorm_bwd (persistent)");
@@ -991,7 +1097,7 @@ void Stack::backward(int wi, int block, int sb) {
       ++launches_;
       if (wgrad_now) {
         // dgamma/dbeta and the row-bias gradient over both sub-batches' partials: side stream
-        const bool acc_ln = touch(w, block + 1, OASES_P_LN_GAMMA);
+        const bool acc_ln = touch(w, block + 1, OASES_P_LN_GAMMA, degree(block));
         const bool acc_b = cfg_.bias ? touch(w, block, OASES_P_B_ROW) : false;
         BlockParams& cur = w.params[static_cast<size_t>(block)];
         fork_side();
@@ -1002,23 +1108,23 @@ void Stack::backward(int wi, int block, int sb) {
         ++launches_;
       }
     } else if (cfg_.ln) {
-      const void* xn = w.xs[static_cast<size_t>(block + 1)][usb];
+      const void* xn = gp(w.xbase[static_cast<size_t>(block + 1)], w, block, sb, h);
       const bool fuse = cfg_.p_hidden > 0.f && fuse_bdr_ln_ && ln_bwd_dropout_supported(dtype(), Ts, hi);
       // this sub-batch's row statistics land in rows [sb T_sub, (sb+1) T_sub) of the workspace
       void* stats_sb = static_cast<char*>(w.ln_ws) + static_cast<size_t>(sb) * Ts * 2 * sizeof(float);
       check_cuda(layernorm_bwd_part(1, dtype(), xn, nxt.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0, nullptr,
                                     nullptr, 0, stats_sb, Ts, hi, cfg_.eps, ctx_.compute, fuse ? gar_sb : nullptr,
                                     cfg_.p_hidden, cfg_.seed, drop_offset(block, sb, 0),
-                                    fuse && hbits_ ? w.hbits[static_cast<size_t>(block)][usb] : nullptr),
+                                    fuse && hbits_ ? w.hbits[static_cast<size_t>(block)][static_cast<size_t>(sb)] : nullptr),
                  "layernorm_bwd");
       gar_done = fuse;
       ++launches_;
       if (wgrad_now) {
         // dgamma/dbeta over both sub-batches: side stream, under this op's GEMMs (joined at the op's end)
-        const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA);
+        const bool acc = touch(w, block + 1, OASES_P_LN_GAMMA, degree(block));
         fork_side();
-        check_cuda(layernorm_bwd_part(2, dtype(), w.xs[static_cast<size_t>(block + 1)][0], nxt.p[OASES_P_LN_GAMMA],
-                                      w.bwd_ar[(block + 1) % 2][0], nullptr, 0, nxt.g[OASES_P_LN_GAMMA],
+        check_cuda(layernorm_bwd_part(2, dtype(), gp(w.xbase[static_cast<size_t>(block + 1)], w, block, 0, h),
+                                      nxt.p[OASES_P_LN_GAMMA], gp(w.bwd_ar[(block + 1) % 2], w, block, 0, h), nullptr, 0, nxt.g[OASES_P_LN_GAMMA],
                                       nxt.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, 2 * Ts, hi, cfg_.eps, ctx_.side),
                    "layernorm_bwd params");
         launches_ += 2;
@@ -1046,18 +1152,19 @@ void Stack::backward(int wi, int block, int sb) {
     // row-bias gradient = column sums of g_ar over both sub-batches: side stream, under the row GEMMs
     const bool acc = touch(w, block, OASES_P_B_ROW);
     fork_side();
-    check_cuda(col_pass(dtype(), gar == gar_sb ? w.gar : w.grad, nullptr, bp.g[OASES_P_B_ROW], acc ? 1 : 0, w.col_ws,
+    check_cuda(col_pass(dtype(), gar == gar_sb ? w.gar : gp(w.grad, w, block, 0, h), nullptr, bp.g[OASES_P_B_ROW],
+                        acc ? 1 : 0, w.col_ws,
                         2 * Ts, hi, 0.f, 0, 0, ctx_.side),
                "row bias grad");
     launches_ += 2;
   }
-  Workspace& ws = ws_for(w, block, sb);
+  Workspace ws = ws_for(w, block, sb);
   const bool att = is_attention(block);
-  const int64_t ncol = att ? ncol_attn_ : ncol_ffn_, nrow = att ? nrow_attn_ : nrow_ffn_;
+  const int64_t ncol = this->ncol(block), nrow = this->nrow(block);
   // 3. row-parallel GEMM: dW_row (+)= g_ar^T act over both sub-batches ; d(act) = g_ar W_row
   // (g_ar is the sub-batch half of w.gar unless the dropout is off and g_ar == g,
   // a half of w.grad: both hold the two sub-batches contiguously)
-  const void* gar_base = gar == gar_sb ? w.gar : w.grad;
+  const void* gar_base = gar == gar_sb ? w.gar : gp(w.grad, w, block, 0, h);
   oases_gemm_desc dw{};
   if (wgrad_now) {
     dw.c_dtype = gdtype();
@@ -1078,7 +1185,7 @@ void Stack::backward(int wi, int block, int sb) {
   if (att) {
     d.c = w.du; d.ldc = nrow;
     // ROWDOT: each 128-column epilogue stripe of the CTA-pair kernel holds whole heads
-    rowdot_ = fused_attn_ && nrow_attn_ > 128 && Ts > 128 && 128 % dh_ == 0;
+    rowdot_ = fused_attn_ && nrow > 128 && Ts > 128 && 128 % dh_ == 0;
     if (rowdot_) {
       // D = rowsum(dO o O) per head for the attention backward, from the dgrad epilogue
       d.epilogue = OASES_EPI_ROWDOT;
@@ -1086,7 +1193,7 @@ void Stack::backward(int wi, int block, int sb) {
       d.rowdot = static_cast<float*>(w.attn_ws);
       d.rowdot_group = dh_;
       d.rowdot_seq = static_cast<int>(cfg_.s);
-      d.rowdot_heads = hl_;
+      d.rowdot_heads = hl(block);
     }
     if (wgrad_now) gemm2(dw, d);
     else gemm(d);
@@ -1094,7 +1201,7 @@ void Stack::backward(int wi, int block, int sb) {
   } else {
     // dpre = (g_ar W_row) o gelu'(pre)   (hadamard + gelu_grad, numerics.cpp:203-204; gelu'(pre)
     // was stored by the FC1 epilogue that produced the activation)
-    d.c = half(w.dcol, sb, ncol); d.ldc = ncol;
+    d.c = lp(w.dcol, block, sb, ncol); d.ldc = ncol;
     d.epilogue = OASES_EPI_MUL;
     d.aux = ws.col;
     // column-bias gradient partials (32-row sums of dpre) from the same epilogue: this
@@ -1123,7 +1230,7 @@ void Stack::backward(int wi, int block, int sb) {
   }
   // 5. column-parallel GEMM: dW_col (+)= dcol^T ln over both sub-batches ; d_ln partial = dcol W_col
   //    -> AR_b (backward f)
-  const void* ln_base = cfg_.ln ? ws_for(w, block, 0).ln : w.xs[static_cast<size_t>(block)][0];
+  const void* ln_base = cfg_.ln ? ws_for(w, block, 0).ln : gp(w.xbase[static_cast<size_t>(block)], w, block, 0, h);
   dw = oases_gemm_desc{};
   if (wgrad_now) {
     dw.c_dtype = gdtype();
@@ -1138,9 +1245,9 @@ void Stack::backward(int wi, int block, int sb) {
   d.c_dtype = dtype();
   d.M = Ts; d.N = h; d.K = ncol;
   d.batch = 1; d.batch_inner = 1;
-  d.a = operand(half(w.dcol, sb, ncol), Ts, ncol, ncol, false);
+  d.a = operand(lp(w.dcol, block, sb, ncol), Ts, ncol, ncol, false);
   d.b = operand(bp.p[OASES_P_W_COL], ncol, h, h, true);
-  d.c = w.bwd_ar[block % 2][usb]; d.ldc = h;
+  d.c = gp(w.bwd_ar[block % 2], w, block, sb, h); d.ldc = h;
   d.alpha = 1.f;
   if (wgrad_now) gemm2(dw, d);
   else gemm(d);
@@ -1149,14 +1256,13 @@ void Stack::backward(int wi, int block, int sb) {
 
 void Stack::tail(int wi, int sb) {
   Worker& w = workers_[static_cast<size_t>(wi)];
-  const int64_t Ts = tokens_sub(), h = cfg_.h;
-  void* g = half(w.grad, sb, h);
-  const size_t usb = static_cast<size_t>(sb);
-  const void* dln = w.bwd_ar[0][usb];
+  const int64_t Ts = ts(0), h = cfg_.h;
+  void* g = gp(w.grad, w, 0, sb, h);
+  const void* dln = gp(w.bwd_ar[0], w, 0, sb, h);
   if (cfg_.ln) {
     const BlockParams& bp = w.params[0];
-    const bool acc = touch(w, 0, OASES_P_LN_GAMMA);
-    check_cuda(layernorm_bwd(dtype(), w.xs[0][usb], bp.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0,
+    const bool acc = touch(w, 0, OASES_P_LN_GAMMA, degree(0));
+    check_cuda(layernorm_bwd(dtype(), gp(w.xbase[0], w, 0, sb, h), bp.p[OASES_P_LN_GAMMA], dln, g, cfg_.residual ? 1 : 0,
                              bp.g[OASES_P_LN_GAMMA], bp.g[OASES_P_LN_BETA], acc ? 1 : 0, w.ln_ws, Ts,
                              static_cast<int>(h), cfg_.eps, ctx_.compute, ctx_.gemm_max_ctas),
                "layernorm_bwd (tail)");
@@ -1171,25 +1277,149 @@ void Stack::tail(int wi, int sb) {
 
 void Stack::allreduce(tmpsim::Pass pass, int block, int sb, bool both) {
   if (ctx_.comm_disabled || (ctx_.tp == 1 && !ctx_.nccl)) return;
-  const int par = block % 2;
+  const int par = block % 2, d = degree(block);
   auto pick = [&](Worker& w) -> void* {
-    auto& arr = pass == tmpsim::Pass::Forward ? w.fwd_ar[par] : pass == tmpsim::Pass::Recompute ? w.rec_ar[par] : w.bwd_ar[par];
-    return arr[both ? 0 : static_cast<size_t>(sb)];
+    void* base = pass == tmpsim::Pass::Forward ? w.fwd_ar[par] : pass == tmpsim::Pass::Recompute ? w.rec_ar[par] : w.bwd_ar[par];
+    return gp(base, w, block, both ? 0 : sb, cfg_.h);
   };
-  const int64_t count = tokens_sub() * cfg_.h * (both ? 2 : 1);
+  const int64_t count = ts(block) * cfg_.h * (both ? 2 : 1);
   if (ctx_.local_workers > 1) {
-    std::vector<void*> bufs;
-    for (Worker& w : workers_) bufs.push_back(pick(w));
-    check_cuda(local_allreduce(dtype(), bufs.data(), static_cast<int>(bufs.size()), count, ctx_.comm),
-               "local allreduce");
-    ++launches_;
+    // one literal sum per group of the block's degree (worker order inside the group)
+    if (d == 1) return;
+    for (int g0 = 0; g0 < num_workers(); g0 += d) {
+      std::vector<void*> bufs;
+      for (int k = 0; k < d; ++k) bufs.push_back(pick(workers_[static_cast<size_t>(g0 + k)]));
+      check_cuda(local_allreduce(dtype(), bufs.data(), d, count, ctx_.comm), "local allreduce");
+      ++launches_;
+    }
     return;
   }
+  if (d == 1 && ctx_.tp > 1) return;
   void* p = pick(workers_[0]);
   check_nccl(ncclAllReduce(p, p, static_cast<size_t>(count), dtype() == OASES_BF16 ? ncclBfloat16 : ncclFloat32,
-                           ncclSum, ctx_.nccl, ctx_.comm),
+                           ncclSum, group_comm(d), ctx_.comm),
              "ncclAllReduce");
   ++launches_;
+}
+
+// ------------------------------------------------------------------ mixed degrees (F2)
+// NCCL sub-communicators, split once per degree from the world communicator in
+// a fixed order on every rank (Stack construction): the TMP group of degree d
+// (color rank / d) and its data-parallel complement (color rank % d).
+ncclComm_t Stack::group_comm(int d) {
+  if (d == ctx_.tp) return ctx_.nccl;
+  for (auto& c : tp_comms_)
+    if (c.first == d) return c.second;
+  throw ConfigError("stack: no communicator for degree " + std::to_string(d));
+}
+
+ncclComm_t Stack::dp_comm(int d) {
+  for (auto& c : dp_comms_)
+    if (c.first == d) return c.second;
+  throw ConfigError("stack: no data-parallel communicator for degree " + std::to_string(d));
+}
+
+void Stack::gather_tokens(const std::vector<void*>& bases, int from_b, int to_b) {
+  // to_b's group (degree du) covers du / dv slices of from_b (degree dv); split
+  // its slice into du chunks: rank r of the group holds chunk r inside its own
+  // slice of from_b, so this is an in-place AllGather of one chunk per rank
+  const int du = degree(to_b);
+  const int64_t h = cfg_.h, chunk = 2 * ts(to_b) / du;  // rows
+  const int dt = dtype();
+  if (ctx_.local_workers > 1) {
+    for (int g0 = 0; g0 < num_workers(); g0 += du) {
+      std::vector<void*> bufs;
+      for (int k = 0; k < du; ++k) {
+        const Worker& w = workers_[static_cast<size_t>(g0 + k)];
+        bufs.push_back(static_cast<char*>(bases[static_cast<size_t>(g0 + k)]) +
+                       static_cast<size_t>(row0(w, to_b) * h) * esize());
+      }
+      check_cuda(local_allgather(dt, bufs.data(), du, chunk * h, ctx_.comm), "local allgather");
+      ++launches_;
+    }
+    return;
+  }
+  const Worker& w = workers_[0];
+  char* base = static_cast<char*>(bases[0]) + static_cast<size_t>(row0(w, to_b) * h) * esize();
+  const size_t cnt = static_cast<size_t>(chunk * h);
+  check_nccl(ncclAllGather(base + static_cast<size_t>(rig(w, to_b)) * cnt * esize(), base, cnt,
+                           dt == OASES_BF16 ? ncclBfloat16 : ncclFloat32, group_comm(du), ctx_.comm),
+             "ncclAllGather");
+  ++launches_;
+}
+
+void Stack::reshard_fwd(int v) {
+  const int u = v + 1;
+  const int64_t h = cfg_.h;
+  std::vector<void*> bases;
+  for (Worker& w : workers_) {
+    const BlockParams& pv = w.params[static_cast<size_t>(v)];
+    for (int sb = 0; sb < 2; ++sb) {
+      // x_u = x_v + AR_v + bias_v on block v's slice (mixed degrees run without hidden dropout)
+      check_cuda(bias_dropout_residual_fwd(dtype(), gp(w.fwd_ar[v % 2], w, v, sb, h),
+                                           cfg_.bias ? pv.p[OASES_P_B_ROW] : nullptr,
+                                           cfg_.residual ? gp(w.xbase[static_cast<size_t>(v)], w, v, sb, h) : nullptr,
+                                           gp(w.xbase[static_cast<size_t>(u)], w, v, sb, h), ts(v),
+                                           static_cast<int>(h), 0.f, 0, 0, ctx_.comm),
+                 "reshard bdr");
+      ++launches_;
+    }
+    bases.push_back(w.xbase[static_cast<size_t>(u)]);
+  }
+  gather_tokens(bases, v, u);
+}
+
+void Stack::reshard_bwd(int u) {
+  const int v = u - 1;
+  const int64_t h = cfg_.h, rows = 2 * ts(u);
+  std::vector<void*> bases;
+  for (Worker& w : workers_) {
+    // g_u = g + LN_u'(dln_u) (+ the residual) over both sub-batches of block u's slice
+    void* g = gp(w.grad, w, u, 0, h);
+    const void* dln = gp(w.bwd_ar[u % 2], w, u, 0, h);
+    if (cfg_.ln) {
+      const BlockParams& bp = w.params[static_cast<size_t>(u)];
+      const bool acc = touch(w, u, OASES_P_LN_GAMMA, degree(u));
+      check_cuda(layernorm_bwd(dtype(), gp(w.xbase[static_cast<size_t>(u)], w, u, 0, h), bp.p[OASES_P_LN_GAMMA], dln,
+                               g, cfg_.residual ? 1 : 0, bp.g[OASES_P_LN_GAMMA], bp.g[OASES_P_LN_BETA], acc ? 1 : 0,
+                               w.ln_ws, rows, static_cast<int>(h), cfg_.eps, ctx_.comm, 0),
+                 "reshard layernorm_bwd");
+      launches_ += 3;
+    } else {
+      check_cuda(bias_dropout_residual_fwd(dtype(), dln, nullptr, cfg_.residual ? g : nullptr, g, rows,
+                                           static_cast<int>(h), 0.f, 0, 0, ctx_.comm),
+                 "reshard residual grad");
+      ++launches_;
+    }
+    bases.push_back(w.grad);
+  }
+  gather_tokens(bases, u, v);
+}
+
+void Stack::dp_reduce_grads() {
+  if (!mixed_) return;
+  const int N = world();
+  for (int b = 0; b < nblocks_; ++b) {
+    for (int p = 0; p < OASES_P_COUNT; ++p) {
+      const int64_t n = workers_[0].params[static_cast<size_t>(b)].numel[p];
+      // LayerNorm beta follows gamma (one touch covers both)
+      const int d = computed_at_[static_cast<size_t>(b)][static_cast<size_t>(p == OASES_P_LN_BETA ? OASES_P_LN_GAMMA : p)];
+      if (!n || d == 0 || d == N) continue;
+      if (ctx_.local_workers > 1) {
+        for (int r = 0; r < d; ++r) {
+          std::vector<void*> bufs;
+          for (int k = r; k < N; k += d) bufs.push_back(workers_[static_cast<size_t>(k)].params[static_cast<size_t>(b)].g[p]);
+          check_cuda(local_allreduce(gdtype(), bufs.data(), N / d, n, ctx_.comm), "dp grad allreduce");
+          ++launches_;
+        }
+      } else {
+        float* gptr = workers_[0].params[static_cast<size_t>(b)].g[p];
+        check_nccl(ncclAllReduce(gptr, gptr, static_cast<size_t>(n), ncclFloat32, ncclSum, dp_comm(d), ctx_.comm),
+                   "dp grad allreduce");
+        ++launches_;
+      }
+    }
+  }
 }
 
 }  // namespace oases

@@ -69,6 +69,8 @@ struct BlockParams {
 };
 
 // Activations of one (block, sub-batch) forward/recompute instance.
+// (ws_for() returns a copy whose ln / act point at the sub-batch half of the
+// slot's [2 T_sub, .] allocations for the block's own T_sub and row width.)
 struct Workspace {
   void* ln = nullptr;   // [T_sub, h]  (aliases x when LN is off)
   void* col = nullptr;  // [T_sub, ncol]  qkv | pre
@@ -78,20 +80,26 @@ struct Workspace {
   float* lse = nullptr; // [bh*Hl*s] row log-sum-exp of the fused attention (log2 domain)
 };
 
+// Token-indexed ("global") buffers hold [T, h] rows of the whole micro-batch
+// (T = b * s); a block of degree d runs on N/d groups of d ranks (N = the
+// world), group g owning the contiguous sample slice g of the micro-batch, and
+// sub-batch sb of the block is half sb of that slice (Stack::gp). With every
+// block at degree N this is the plain TMP layout (one group, the halves of T).
 struct Worker {
-  int rank = 0;
+  int rank = 0;  // rank in the world (the in-process worker index, or the NCCL rank)
   std::vector<BlockParams> params;
-  // residual stream x_b per sub-batch (b = 0..nblocks-1), x_0 aliases input.
-  // Blocks whose x_b the bound plan keeps until backward own a buffer; the
-  // others (interior tensors of CrossPass-replayed layer units) share
+  // residual stream x_b (b = 0..nblocks-1), token-indexed [T, h]; x_0 is the
+  // input. Blocks whose x_b the bound plan keeps until backward own a buffer;
+  // the others (interior tensors of CrossPass-replayed layer units) share
   // x_scratch, rebuilt by their recompute (Stack::bind_storage).
-  std::vector<std::array<void*, 2>> xs;
-  std::vector<std::array<void*, 2>> x_own;  // dedicated buffers, allocated on first need
-  std::array<void*, 2> x_scratch = {};
-  std::array<void*, 2> fwd_ar[2] = {}, rec_ar[2] = {}, bwd_ar[2] = {};  // [block parity][sb]
+  std::vector<void*> xbase;
+  std::vector<void*> x_own;  // dedicated buffers, allocated on first need
+  void* x_scratch = nullptr;
+  void* fwd_ar[2] = {}, *rec_ar[2] = {}, *bwd_ar[2] = {};  // [block parity], token-indexed [T, h]
   std::vector<std::array<Workspace, 2>> ws;  // [slot][sb]
+  std::vector<void*> ln_full, act_full;      // [slot] [2 T_sub, .] bases of ws.ln / ws.act
   void* input = nullptr;                     // [T, h]
-  void* grad = nullptr;                      // [T, h] residual gradient g (halves per sb) == dX at the end
+  void* grad = nullptr;                      // [T, h] residual gradient g (token-indexed) == dX at the end
   // backward scratch (the compute stream serialises all B_b)
   void* gar = nullptr;   // [T_sub, h]  dropout'(g)
   void* du = nullptr;    // [T_sub, nmax] d(row GEMM input)
@@ -105,7 +113,7 @@ struct Worker {
   // written by the forward's fused bias-dropout-residual + LN of block b+1,
   // read by the backward's fused LN-backward + dropout'
   std::vector<std::array<uint16_t*, 2>> hbits;
-  void* y = nullptr;     // [2][T_sub, h] final output x_B (per sub-batch half) for the loss head
+  void* y = nullptr;     // [T, h] final output x_B (token-indexed) for the loss head
   void* ln_ws = nullptr;
   float* lnp_part = nullptr;  // persistent LayerNorm backward column partials [2][prows][3][h]
   void* col_ws = nullptr;
@@ -117,8 +125,14 @@ struct Worker {
 
 class Stack {
  public:
-  Stack(Context& ctx, const ModelCfg& cfg);
+  // degrees: per-block TMP degree (each divides the world size ctx.tp); empty =
+  // every block at ctx.tp. Mixed degrees: a block of
+  // degree d < N runs data-parallel over N/d groups of d ranks.
+  Stack(Context& ctx, const ModelCfg& cfg, const std::vector<int>& degrees = {});
   ~Stack();
+  int degree(int b) const { return deg_[static_cast<size_t>(b)]; }
+  int world() const { return ctx_.tp; }
+  bool mixed() const { return mixed_; }
 
   const ModelCfg& cfg() const { return cfg_; }
   Context& ctx() { return ctx_; }
@@ -149,8 +163,22 @@ class Stack {
   void forward(int worker, int block, int sb, bool with_bdr, bool with_row);
   // recompute: replay_input: -1 = saved x_b; else rebuild x_b from rec_ar of block-1
   void recompute(int worker, int block, int sb, bool rebuild_x, bool with_row);
-  void backward(int worker, int block, int sb);
+  // g_ready: the gradient at x_{b+1} (LN_{b+1} backward included) is already in
+  // the residual-gradient rows (gathered by reshard_bwd)
+  void backward(int worker, int block, int sb, bool g_ready = false);
   void tail(int worker, int sb);  // LN_0 backward after the last backward AR
+  // ---- resharding between blocks of different degree (the AllGathers of
+  //      sim.cpp:101-175), issued on ctx.comm for every worker ----
+  // degree grows at v -> v+1: x_{v+1} = x_v + AR_v + bias on each rank's slice of
+  // block v, then gathered over block v+1's groups (F_{v+1} skips its BDR)
+  void reshard_fwd(int v);
+  // degree shrinks at u-1 -> u: g + LN_u'(dln_u) on block u's slice, then
+  // gathered over block u-1's groups (B_{u-1} runs with g_ready)
+  void reshard_bwd(int u);
+  // sums every gradient computed data-parallel (on groups smaller than the
+  // world) over the groups, on ctx.comm: after it each rank holds the
+  // micro-batch gradient of its shard
+  void dp_reduce_grads();
   // ---- communication (issued on ctx.comm) ----
   void allreduce(tmpsim::Pass pass, int block, int sb, bool both_halves);
 
@@ -172,13 +200,32 @@ class Stack {
   void fork_side();  // side stream waits for the compute stream's current tail
   void join_side();  // compute stream waits for the side stream's current tail
   bool side_forked_ = false;
-  void ln_fwd(const void* x, const void* g, const void* b, void* y);
+  void ln_fwd(const void* x, const void* g, const void* b, void* y, int64_t rows);
   void bdr_then_ln(Worker& w, int block, int sb, const void* ar, void* x, void* ln, bool store_bits);
+  // bases[w]: a token-indexed [T, h] buffer per worker whose rows of block
+  // from_b's slice are valid; gathers the rows of block to_b's (larger) slice
+  // from the peers of to_b's group (ncclAllGather on the group communicator,
+  // or a copy kernel between the in-process workers)
+  void gather_tokens(const std::vector<void*>& bases, int from_b, int to_b);
+  ncclComm_t group_comm(int d);  // the TMP group communicator of degree d (NCCL mode)
+  ncclComm_t dp_comm(int d);     // ranks with the same rank-in-group of degree d
   oases_attn_desc attn_desc(Worker& w, int block, int sb, const Workspace& ws);
   void attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int mask_mode);
   void attention_bwd(Worker& w, int block, int sb, const Workspace& ws);
-  Workspace& ws_for(Worker& w, int block, int sb);
-  bool touch(const Worker& w, int block, int p);  // true if the gradient must accumulate (written this step)
+  Workspace ws_for(Worker& w, int block, int sb);
+  bool touch(const Worker& w, int block, int p, int computed_at = 0);  // true if the gradient must accumulate
+  // per-block geometry (degree-dependent)
+  int hl(int b) const { return cfg_.attention ? cfg_.heads / degree(b) : 0; }
+  int64_t ncol(int b) const { return is_attention(b) ? 3LL * hl(b) * dh_ : cfg_.f / degree(b); }
+  int64_t nrow(int b) const { return is_attention(b) ? static_cast<int64_t>(hl(b)) * dh_ : cfg_.f / degree(b); }
+  int64_t bsub(int b) const { return static_cast<int64_t>(cfg_.b) * degree(b) / world() / 2; }  // samples per sub-batch
+  int64_t ts(int b) const { return bsub(b) * cfg_.s; }  // tokens per sub-batch
+  int rig(const Worker& w, int b) const { return w.rank % degree(b); }  // rank in the block's group
+  int64_t row0(const Worker& w, int b) const { return static_cast<int64_t>(w.rank / degree(b)) * 2 * ts(b); }
+  // rows of sub-batch sb of block b (this worker's group) in a token-indexed buffer
+  void* gp(void* base, const Worker& w, int b, int sb, int64_t cols) const;
+  // half sb of a local [2 ts(b), cols] buffer
+  void* lp(void* base, int b, int sb, int64_t cols) const;
   void* half(void* base, int sb, int64_t cols) const;
 
   Context& ctx_;
@@ -194,6 +241,11 @@ class Stack {
   bool colsum_ = false;  // FFN column-bias gradient partials come from the FC2 dgrad (MUL) epilogue
   int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
+  // degree of the groups a gradient was computed on this step (0: untouched); < world -> dp_reduce_grads
+  std::vector<std::array<int, OASES_P_COUNT>> computed_at_;  // [block] (same on every worker)
+  std::vector<int> deg_;  // [block]
+  bool mixed_ = false;
+  std::vector<std::pair<int, ncclComm_t>> tp_comms_, dp_comms_;  // NCCL sub-communicators by degree
   std::vector<bool> loss_touched_;
   std::vector<std::vector<bool>> bwd_seen_;  // [worker][block] first backward call of the step done
   std::vector<bool> x_stored_;  // [block] x_b readable after a step (bind_storage)
@@ -215,6 +267,9 @@ struct ExecOp {
   bool both_halves = false;  // unsplit (Default) plans: one op covers both sub-batches
   bool rebuild_x = false;    // recompute restarts from a replayed comm (CrossPass inside a unit)
   bool with_row = false;     // recompute also runs the row-parallel GEMM (its AR is replayed)
+  bool with_bdr = true;      // forward: builds x_b itself (false after a degree-growing reshard)
+  bool g_ready = false;      // backward: a degree-shrinking reshard gathered its input gradient
+  int seq = 0;               // position in plan order (reshards right after their anchors)
   std::vector<int> waits;    // cross-stream deps (op ids)
 };
 
@@ -234,6 +289,10 @@ class Executor {
 
  private:
   void issue(bool trace);
+  // resharding AllGathers between blocks of different degree, at the anchors
+  // of sim.cpp:101-175 (after the upstream block's last forward comm when the
+  // degree grows; after the downstream block's backward tail when it shrinks)
+  void inject_reshards(int n);
   Stack& stack_;
   tmpsim::SchedulePlan plan_;
   std::vector<ExecOp> ops_;
@@ -241,6 +300,8 @@ class Executor {
   std::vector<cudaEvent_t> t0_, t1_;  // per op timing
   cudaEvent_t begin_ = nullptr, end_ = nullptr, fork_ = nullptr;
   std::array<int, 2> tail_wait_ = {-1, -1};  // last backward AR (per sb) the LN_0 tail waits for
+  std::vector<int> stream_of_;  // [op id] 0 compute / 1 comm (plan ops, then the injected reshards)
+  int nreshard_ = 0;            // injected AllGathers: op ids n .. n + nreshard_ - 1
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   std::vector<oases_trace_event> events_;

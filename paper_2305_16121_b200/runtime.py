@@ -179,12 +179,21 @@ class StepResult:
 class LayerStack:
     """The TMP layer stack of one process (one rank, or all ranks in-process)."""
 
-    def __init__(self, ctx: Context, cfg: ModelConfig):
+    def __init__(self, ctx: Context, cfg: ModelConfig, degrees=None):
+        """degrees: per-block TMP degree (each dividing ctx.tp, the world size) for a
+        planner-chosen mixed strategy (tmpsim Strategy.degrees); None = every block at
+        ctx.tp. A degree-d block runs data-parallel on tp/d groups of d ranks; the
+        executor inserts the resharding AllGathers and sums the data-parallel gradients."""
         self.ctx, self.cfg = ctx, cfg
         self._h = C.c_void_p()
         d = cfg.desc()
-        check(capi.lib().oases_stack_create(ctx._h, C.byref(d), C.byref(self._h)))
+        if degrees is None:
+            check(capi.lib().oases_stack_create(ctx._h, C.byref(d), C.byref(self._h)))
+        else:
+            deg = (C.c_int32 * len(degrees))(*[int(x) for x in degrees])
+            check(capi.lib().oases_stack_create_mixed(ctx._h, C.byref(d), deg, len(degrees), C.byref(self._h)))
         self.num_blocks = capi.lib().oases_stack_num_blocks(self._h)
+        self.degrees = [capi.lib().oases_stack_block_degree(self._h, b) for b in range(self.num_blocks)]
         self.num_workers = capi.lib().oases_stack_num_workers(self._h)
         self._plan = None
 
@@ -294,7 +303,11 @@ class LayerStack:
         return out
 
     def activation(self, worker, block, sb) -> np.ndarray:
-        out = np.empty((self.cfg.batch // 2 * self.cfg.seq, self.cfg.hidden), dtype=np.float64)
+        """x_block rows of sub-batch sb of the worker's group of that block (the last
+        block's for block == num_blocks): T_sub rows, or T_sub * degree / world with mixed degrees."""
+        b = min(block, self.num_blocks - 1)
+        rows = self.cfg.batch * self.degrees[b] // self.ctx.tp // 2 * self.cfg.seq if self.num_blocks else 0
+        out = np.empty((rows, self.cfg.hidden), dtype=np.float64)
         check(capi.lib().oases_stack_get_activation(self._h, worker, block, sb, out.ctypes.data_as(C.c_void_p)))
         return out
 
