@@ -169,6 +169,10 @@ typedef struct {
 int32_t oases_attention_supported(int dtype, int32_t head_dim, int32_t seq);
 oases_status oases_attention_fwd(const oases_attn_desc* desc, void* stream);
 size_t oases_attention_bwd_workspace(const oases_attn_desc* desc);
+/* Generates the keep bits of every causal-band element into desc->mask_bits
+ * (the Philox masks mask_mode 1 would store) with a separate fully parallel
+ * kernel, so the forward can run with mask_mode 2. Needs dropout_p > 0. */
+oases_status oases_attention_masks(const oases_attn_desc* desc, void* stream);
 size_t oases_attention_mask_bytes(const oases_attn_desc* desc);
 oases_status oases_attention_bwd(const oases_attn_desc* desc, void* stream);
 

@@ -198,6 +198,7 @@ _SIGNATURES = [
     ("oases_attention_supported", C.c_int32, [C.c_int, C.c_int32, C.c_int32]),
     ("oases_attention_fwd", C.c_int, [C.POINTER(AttnDesc), C.c_void_p]),
     ("oases_attention_mask_bytes", C.c_size_t, [C.POINTER(AttnDesc)]),
+    ("oases_attention_masks", C.c_int, [C.POINTER(AttnDesc), C.c_void_p]),
     ("oases_attention_bwd_workspace", C.c_size_t, [C.POINTER(AttnDesc)]),
     ("oases_attention_bwd", C.c_int, [C.POINTER(AttnDesc), C.c_void_p]),
     ("oases_layernorm_fwd", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,

@@ -36,6 +36,7 @@
 // parameters; the forward pass can store one bit per causal-band element
 // (mask_mode 1) which the recompute forward and the backward read (mode 2).
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -600,6 +601,368 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ forward, ping-pong
+// attn_fwd2_kernel: FA4-style forward. A work item is a PAIR of adjacent
+// 128-query tiles (2m, 2m+1) of one (sample, head), streaming the same K/V
+// tiles (both active on all but the last one, so the two softmax groups
+// overlap each other's MMAs; pairing (m, nq-1-m) balances the items but leaves
+// one tile running alone most of the time -- measured slower). Each
+// tile has its own softmax warpgroup (4 warps, one query row per thread, all
+// 128 key columns of the row in registers: the row max needs no cross-warp
+// exchange) and its own TMEM S/P (128 columns) and O (DH columns) regions, so
+// the tensor core alternates between the tiles: PV_A(j), S_A(j+1) run under
+// softmax B(j); PV_B(j), S_B(j+1) under softmax A(j+1).
+// Warps: 0-3 softmax of tile A (TMEM lane quarter w % 4), 4-7 softmax of tile
+// B, 8 TMA (Q pair, K/V stages), 9 MMA issuer + TMEM owner (10 warps; the
+// register file is split per SM sub-partition, so 3 warps on one of them cap
+// a thread at 168 registers).
+// Dropout keys, keep-bit cache layout (mask_word) and the conditional
+// rescaling are those of attn_fwd_kernel, so both kernels compute the same
+// softmax and either one's keep bits serve the other and attn_dkdv_kernel.
+template <int DH>
+struct Fwd2Cfg {
+  static constexpr int TILE_BYTES = kTile * DH * 2;
+  static constexpr int QA_OFF = 0, QB_OFF = TILE_BYTES;
+  static constexpr int K_OFF = 2 * TILE_BYTES;          // [2] stages
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;  // [2] stages
+  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256;
+  __host__ __device__ static constexpr uint32_t s_col(int x) { return x ? kTile : 0u; }
+  static constexpr uint32_t O_COL0 = 2 * kTile;  // O_A at O_COL0, O_B at O_COL0 + DH
+  static constexpr uint32_t TMEM_COLS = 512;
+  static_assert(2 * kTile + 2 * DH <= 512, "TMEM budget");
+};
+constexpr int kFwd2Threads = 320;
+
+template <int DH>
+__global__ void __launch_bounds__(kFwd2Threads, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tqkv, const AttnParams p) {
+  pdl_trigger();
+  using C = Fwd2Cfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars;        // Q pair loaded
+  uint64_t* q_empty = bars + 1;   // the item's last S MMAs done
+  uint64_t* k_full = bars + 2;    // [2]
+  uint64_t* k_empty = bars + 4;   // [2]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [tile] S in TMEM
+  uint64_t* p_full = bars + 12;   // [tile] P (bf16) written over S by the tile's 4 softmax warps
+  uint64_t* pv_done = bars + 14;  // [tile] PV done (S/P region reusable, O current)
+  uint64_t* o_free = bars + 16;   // [tile] epilogue drained O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = static_cast<int>(gridDim.x);
+  const int npair = (p.nq + 1) / 2;
+  const int total = p.Z * npair;
+  // item t -> (m, z): tiles A = 2m, B = 2m+1 (absent for the last of an odd
+  // count), heaviest first
+  auto item_of = [&](int t, int& m, int& z) {
+    m = npair - 1 - t / p.Z;
+    z = t % p.Z;
+  };
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
+      mbar_init(&pv_done[s], 1);
+      mbar_init(&o_free[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch(&tqkv);
+      int g = 0;
+      for (int r = 0, k = 0;; ++r, ++k) {
+        const int t = zigzag_item(r, G);
+        if (t >= total) break;
+        int m, z;
+        item_of(t, m, z);
+        const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
+        const int qtb = 2 * m + 1;
+        const bool hasb = qtb < p.nq;
+        const int nkv = hasb ? qtb + 1 : 2 * m + 1;
+        mbar_wait(q_empty, (k & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, (hasb ? 2 : 1) * C::TILE_BYTES);
+#pragma unroll
+        for (int gg = 0; gg < DH / 64; ++gg) {
+          tma_load_2d(smem + C::QA_OFF + gg * 16384, &tqkv, q_full, p.q_col + jl * DH + gg * 64,
+                      row0 + 2 * m * kTile);
+          if (hasb)
+            tma_load_2d(smem + C::QB_OFF + gg * 16384, &tqkv, q_full, p.q_col + jl * DH + gg * 64,
+                        row0 + qtb * kTile);
+        }
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int st = g & 1, ph = ((g >> 1) & 1) ^ 1;
+          mbar_wait(&k_empty[st], ph);
+          mbar_arrive_expect_tx(&k_full[st], C::TILE_BYTES);
+#pragma unroll
+          for (int gg = 0; gg < DH / 64; ++gg)
+            tma_load_2d(smem + C::K_OFF + st * C::TILE_BYTES + gg * 16384, &tqkv, &k_full[st],
+                        p.k_col + jl * DH + gg * 64, row0 + j * kTile);
+          mbar_wait(&v_empty[st], ph);
+          mbar_arrive_expect_tx(&v_full[st], C::TILE_BYTES);
+#pragma unroll
+          for (int gg = 0; gg < DH / 64; ++gg)
+            tma_load_2d(smem + C::V_OFF + st * C::TILE_BYTES + gg * 16384, &tqkv, &v_full[st],
+                        p.v_col + jl * DH + gg * 64, row0 + j * kTile);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = umma_idesc_bf16(kTile, kTile, 0, 0);
+      constexpr uint32_t id_o = umma_idesc_bf16(kTile, DH, 0, 1);  // A = P in TMEM (K-major), B = V (MN-major)
+      const uint32_t sb = smem_u32(smem);
+      int cnt[2] = {0, 0};  // S/PV iterations issued per tile (barrier phases)
+      int itc[2] = {0, 0};  // items processed per tile (o_free phases; odd pairs have no tile B)
+      int g = 0;
+      auto issue_s = [&](int x, int st, uint32_t qa) {
+        if (cnt[x] > 0) mbar_wait(&pv_done[x], (cnt[x] - 1) & 1);  // PV read the previous P from this region
+        tc_fence_after();
+        const uint32_t kb = sb + C::K_OFF + st * C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + C::s_col(x), umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(kb + off, 16, 1024),
+                    id_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int st, int j) {
+        if (j == 0) mbar_wait(&o_free[x], (itc[x]++ & 1) ^ 1);
+        mbar_wait(&p_full[x], cnt[x] & 1);
+        tc_fence_after();
+        const uint32_t vb = sb + C::V_OFF + st * C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {
+          const uint64_t bd = umma_desc_sw128(vb + kk * 2048, 16384, 1024);
+          umma_bf16_ts(tmem + C::O_COL0 + x * DH, tmem + C::s_col(x) + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&pv_done[x]);
+        ++cnt[x];
+      };
+      for (int r = 0, k = 0;; ++r, ++k) {
+        const int t = zigzag_item(r, G);
+        if (t >= total) break;
+        int m, z;
+        item_of(t, m, z);
+        const bool hasb = 2 * m + 1 < p.nq;
+        const int na = 2 * m + 1, nb = hasb ? 2 * m + 2 : 0, nkv = hasb ? nb : na;
+        const uint32_t qa = sb + C::QA_OFF, qb = sb + C::QB_OFF;
+        mbar_wait(q_full, k & 1);
+        // prologue: S_A(0), S_B(0)
+        mbar_wait(&k_full[g & 1], (g >> 1) & 1);
+        issue_s(0, g & 1, qa);
+        if (nb > 0) issue_s(1, g & 1, qb);
+        umma_commit(&k_empty[g & 1]);
+        if (nkv == 1) umma_commit(q_empty);
+        for (int j = 0; j < nkv; ++j) {
+          const int st = g & 1, gn = g + 1;
+          mbar_wait(&v_full[st], (g >> 1) & 1);
+          // PV_A(j), then S_A(j+1) under softmax B(j)
+          if (j < na) issue_pv(0, st, j);
+          const bool more = j + 1 < nkv;
+          if (more) mbar_wait(&k_full[gn & 1], (gn >> 1) & 1);
+          if (j + 1 < na) issue_s(0, gn & 1, qa);
+          // PV_B(j), then S_B(j+1) under softmax A(j+1)
+          if (j < nb) issue_pv(1, st, j);
+          umma_commit(&v_empty[st]);
+          if (j + 1 < nb) issue_s(1, gn & 1, qb);
+          if (more) {
+            umma_commit(&k_empty[gn & 1]);
+            if (j + 2 == nkv) umma_commit(q_empty);  // the item's last S MMAs were just issued
+          }
+          g = gn;
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------ softmax warpgroups
+    const int x = warp >> 2;  // 0: tile A (2m), 1: tile B (2m+1)
+    const int q = warp & 3;
+    const int rr = q * 32 + lane;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t ts = tl + C::s_col(x), to = tl + C::O_COL0 + x * DH;
+    int cnt = 0;
+    for (int r = 0, k = 0;; ++r, ++k) {
+      const int t = zigzag_item(r, G);
+      if (t >= total) break;
+      int m2, z;
+      item_of(t, m2, z);
+      const int qt = 2 * m2 + x;
+      if (qt >= p.nq) continue;  // no tile B in the last pair of an odd count
+      const int n = z / p.hl, jl = z - n * p.hl, row0 = n * p.seq;
+      const int i = qt * kTile + rr;
+      const bool cached = p.thr != 0;  // always cached in this kernel (mask_mode 2)
+      float mrun = -INFINITY, l4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j <= qt; ++j, ++cnt) {
+        // this tile's keep-bit words (the load flies while the S MMA completes)
+        uint4 bits4 = make_uint4(0u, 0u, 0u, 0u);
+        if (cached) bits4 = __ldg(reinterpret_cast<const uint4*>(p.mask_bits + mask_word(p, z, qt, j, rr, 0)));
+        mbar_wait(&s_full[x], cnt & 1);
+        tc_fence_after();
+        uint32_t u[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t (&uc)[32] = *reinterpret_cast<uint32_t(*)[32]>(u + 32 * c);
+          tmem_ld32(ts + 32 * c, uc);
+        }
+        tmem_wait_ld();
+        if (j == qt) {
+          int lim = rr;  // keys > row are masked on the diagonal tile
+          asm volatile("" : "+r"(lim));
+#pragma unroll
+          for (int kk = 0; kk < 128; ++kk)
+            if (kk > lim) u[kk] = __float_as_uint(-INFINITY);
+        }
+        float mp[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mp[kk] = __uint_as_float(u[kk]);
+#pragma unroll
+        for (int kk = 8; kk < 128; ++kk) mp[kk & 7] = fmaxf(mp[kk & 7], __uint_as_float(u[kk]));
+        const float mloc =
+            fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+        // conditional rescaling (attn_fwd_kernel): keep the running max unless the
+        // row max grew by more than 8 (log2 units)
+        const float cand = fmaxf(mrun, mloc * p.sl2);
+        const float mx = cand > mrun + 8.f ? cand : mrun;
+        const float alpha = ex2(mrun - mx);
+        const float2 sl2x2 = make_float2(p.sl2, p.sl2), nmx2 = make_float2(-mx, -mx);
+        // row sums kept per 32-column group, each accumulated exactly like one
+        // attn_fwd_kernel softmax warp's (same operation order), so both kernels
+        // produce the same bits
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float2 sp[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int kk = 32 * c; kk < 32 * c + 32; kk += 2) {
+            const float2 e = fma2(make_float2(__uint_as_float(u[kk]), __uint_as_float(u[kk + 1])), sl2x2, nmx2);
+            const float2 ab = make_float2(ex2(e.x), ex2(e.y));
+            sp[(kk >> 1) & 1] = add2(sp[(kk >> 1) & 1], ab);
+            u[kk >> 1] = pack_bf16(ab.x, ab.y);  // P pairs packed into u[0..63]
+          }
+          l4[c] = l4[c] * alpha + ((sp[0].x + sp[1].x) + (sp[0].y + sp[1].y));
+        }
+        mrun = mx;
+        if (p.thr) {  // cached keep bits (the launcher routes Philox-generating modes to attn_fwd_kernel)
+          const uint32_t w4[4] = {bits4.x, bits4.y, bits4.z, bits4.w};
+#pragma unroll
+          for (int gq = 0; gq < 8; ++gq) {
+            uint32_t km[8];
+            masks16_from_bits(w4[gq >> 1] >> (16 * (gq & 1)), km);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) u[gq * 8 + kk] &= km[kk];
+          }
+        }
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          // O holds P_{<j} V: PV(j-1) completed before S(j) was issued (issue_s waited on it)
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(to + 32 * c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) o[kk] = __float_as_uint(__uint_as_float(o[kk]) * alpha);
+            tmem_st32(to + 32 * c, o);
+          }
+          tmem_wait_st();
+        }
+        // P (bf16 pairs) over the first 64 columns of this tile's S region
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const uint32_t (&pc)[32] = *reinterpret_cast<const uint32_t(*)[32]>(u + 32 * c);
+          tmem_st32(ts + 32 * c, pc);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[x]);
+      }
+      // ---- epilogue: O / l -> ctx, lse
+      mbar_wait(&pv_done[x], (cnt - 1) & 1);
+      tc_fence_after();
+      const float l = (l4[0] + l4[1]) + (l4[2] + l4[3]);  // attn_fwd_kernel's combine order
+      const float inv = p.ks / l;
+      __nv_bfloat16* orow =
+          static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row0 + i) * p.ld_out + p.do_col + jl * DH;
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(to + 32 * c, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float* f = reinterpret_cast<const float*>(o + 8 * kk);
+          *reinterpret_cast<uint4*>(orow + 32 * c + kk * 8) =
+              make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                         pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[x]);
+      p.lse[static_cast<long long>(z) * p.seq + i] = mrun + log2f(l);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// Keep bits of every causal-band element (the attention-dropout masks of
+// DESIGN.md section 5), one 32-key word per thread: a separate, fully parallel
+// pass so that the forward's softmax warps -- the critical path of the fused
+// kernels -- only expand cached bits (mask_mode 2) instead of running Philox.
+__global__ void __launch_bounds__(256) attn_mask_kernel(const AttnParams p, long long nwords) {
+  pdl_trigger();
+  pdl_wait();
+  const long long ntile = static_cast<long long>(p.nq) * (p.nq + 1) / 2;
+  PhiloxLite ph;
+  philox_init(p, ph);
+  for (long long wd = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x; wd < nwords;
+       wd += static_cast<long long>(gridDim.x) * 256) {
+    const int w = static_cast<int>(wd & 3);
+    const int row = static_cast<int>((wd >> 2) & (kTile - 1));
+    const long long tile = wd >> 9;  // (z, causal tile) -- mask_word's order
+    const int z = static_cast<int>(tile / ntile);
+    int rem = static_cast<int>(tile - static_cast<long long>(z) * ntile);
+    int qt = 0;
+    while ((qt + 1) * (qt + 2) / 2 <= rem) ++qt;
+    const int kt = rem - qt * (qt + 1) / 2;
+    const int n = z / p.hl, jl = z - n * p.hl;
+    const int i = qt * kTile + row;
+    const unsigned long long e =
+        (static_cast<unsigned long long>((n + p.n0) * p.hg + p.hoff + jl) * p.seq + i) *
+            static_cast<unsigned long long>(p.seq) +
+        static_cast<unsigned long long>(kt) * kTile + 32 * w;
+    uint32_t km[8];
+    const uint32_t b0 = keep_masks16_bits(ph, p, e >> 4, km);
+    const uint32_t b1 = keep_masks16_bits(ph, p, (e + 16) >> 4, km);
+    p.mask_bits[wd] = b0 | (b1 << 16);
+  }
+}
+
 // D[z, i] = sum_d dO[i, d] * O[i, d] (head z's columns); DH/8 threads per row,
 // one 16-byte vector of each operand per thread.
 template <int DH>
@@ -1048,7 +1411,22 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
   p.out = d.out;
   p.ld_out = d.ld_out;
   p.lse = d.lse;
-  unsigned grid = static_cast<unsigned>(p.Z * p.nq);
+  static const bool fwd2_on = [] {
+    const char* e = std::getenv("OASES_ATTN_FWD2");
+    return !(e && e[0] == '0');
+  }();
+  // The ping-pong kernel reads cached keep bits only (the stack's mask pass,
+  // mask_mode 2), and needs enough tile pairs to balance its persistent grid:
+  // measured at the C2 sub-batch (256 pairs) 36.3 vs 38.8 us, at a C3 TMP=8
+  // rank (128 pairs of very unequal length) 46 vs 31 us.
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool fwd2 = fwd2_on && (!p.thr || p.mask_mode == 2) && 2LL * p.Z * ((p.nq + 1) / 2) >= 3LL * nsm;
+  unsigned grid = static_cast<unsigned>(fwd2 ? p.Z * ((p.nq + 1) / 2) : p.Z * p.nq);
   {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1058,7 +1436,15 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
     if (d.max_ctas > 0 && grid > static_cast<unsigned>(d.max_ctas)) grid = static_cast<unsigned>(d.max_ctas);
   }
   cudaError_t e;
-  if (d.head_dim == 128) {
+  if (fwd2 && d.head_dim == 128) {
+    static cudaError_t once = set_smem(attn_fwd2_kernel<128>, Fwd2Cfg<128>::SMEM);
+    if ((e = once) == cudaSuccess)
+      e = launch_pdl(attn_fwd2_kernel<128>, dim3(grid), dim3(kFwd2Threads), Fwd2Cfg<128>::SMEM, stream, tqkv, p);
+  } else if (fwd2) {
+    static cudaError_t once = set_smem(attn_fwd2_kernel<64>, Fwd2Cfg<64>::SMEM);
+    if ((e = once) == cudaSuccess)
+      e = launch_pdl(attn_fwd2_kernel<64>, dim3(grid), dim3(kFwd2Threads), Fwd2Cfg<64>::SMEM, stream, tqkv, p);
+  } else if (d.head_dim == 128) {
     static cudaError_t once = set_smem(attn_fwd_kernel<128>, FwdCfg<128>::SMEM);
     if ((e = once) == cudaSuccess) {
       e = launch_pdl(attn_fwd_kernel<128>, dim3(grid), dim3(kFwdThreads), FwdCfg<128>::SMEM, stream, tqkv, p);
@@ -1071,6 +1457,27 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
   }
   if (e != cudaSuccess) {
     st.err = std::string("attention_fwd launch: ") + cudaGetErrorString(e);
+    st.cuda = true;
+    return st;
+  }
+  st.ok = true;
+  return st;
+}
+
+GemmStatus attention_masks(const oases_attn_desc& d, cudaStream_t stream) {
+  GemmStatus st;
+  AttnParams p{};
+  if (!fill_common(p, d, &st.err)) return st;
+  if (!d.mask_bits || !p.thr) {
+    st.err = "attention_masks: needs mask_bits and dropout_p > 0";
+    return st;
+  }
+  const long long nwords = static_cast<long long>(attention_mask_bytes(d) / sizeof(uint32_t));
+  long long grid = (nwords + 255) / 256;
+  if (grid > 148LL * 8) grid = 148LL * 8;
+  const cudaError_t e = launch_pdl(attn_mask_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, stream, p, nwords);
+  if (e != cudaSuccess) {
+    st.err = std::string("attention_masks launch: ") + cudaGetErrorString(e);
     st.cuda = true;
     return st;
   }

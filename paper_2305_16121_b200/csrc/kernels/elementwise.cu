@@ -282,8 +282,50 @@ __global__ void __launch_bounds__(kThreads) gelu_sq_loss_kernel(const T* __restr
                                                                 double* __restrict__ part, long long n) {
   pdl_trigger();
   pdl_wait();
+  // 8 elements per step (16-byte bf16 vectors): f32 sum of the 8 terms, f64 across steps
+  constexpr int V = 8;
   double acc = 0.0;
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+  const long long nv = n / V;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < nv;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float v[V], o[V];
+    if constexpr (sizeof(T) == 2) {
+      vload(z + i * V, v);
+    } else {
+      float a[4], b[4];
+      vload(z + i * V, a);
+      vload(z + i * V + 4, b);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[e] = a[e];
+        v[4 + e] = b[e];
+      }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const float g = gelu_f(v[e]);
+      s += 0.5f * g * g;
+      o[e] = g * gelu_grad_f(v[e]);
+    }
+    acc += static_cast<double>(s);
+    if (dz) {
+      if constexpr (sizeof(T) == 2) {
+        vstore(dz + i * V, o);
+      } else {
+        float a[4], b[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          a[e] = o[e];
+          b[e] = o[4 + e];
+        }
+        vstore(dz + i * V, a);
+        vstore(dz + i * V + 4, b);
+      }
+    }
+  }
+  // scalar tail
+  for (long long i = nv * V + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const float v = to_f(z[i]);
     const float g = gelu_f(v);
@@ -615,8 +657,13 @@ size_t loss_workspace() { return 1024 * sizeof(double); }
 
 cudaError_t gelu_sq_loss(int dtype, const void* z, void* dz, double* loss, int acc, double* ws, long long n,
                          cudaStream_t st) {
-  unsigned g = grid_for(n, kThreads * 4);
+  unsigned g = grid_for(n, kThreads * 32);
   if (g > 1024) g = 1024;
+  // 16-byte vector path needs aligned buffers
+  const size_t es = dtype == OASES_BF16 ? 2 : (dtype == OASES_F64 ? 8 : 4);
+  if (dtype != OASES_F64 && ((reinterpret_cast<uintptr_t>(z) | reinterpret_cast<uintptr_t>(dz)) & 15u))
+    return cudaErrorMisalignedAddress;
+  (void)es;
   if (dtype == OASES_F64)
     gelu_sq_loss_f64_kernel<<<g, kThreads, 0, st>>>(static_cast<const double*>(z), static_cast<double*>(dz), ws, n);
   else if (dtype == OASES_BF16)

@@ -35,5 +35,7 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream);
 size_t attention_bwd_workspace(const oases_attn_desc& d);
 size_t attention_mask_bytes(const oases_attn_desc& d);
 GemmStatus attention_bwd(const oases_attn_desc& d, cudaStream_t stream);
+// keep bits of every causal-band element into d.mask_bits (read by mask_mode 2)
+GemmStatus attention_masks(const oases_attn_desc& d, cudaStream_t stream);
 
 }  // namespace oases

@@ -256,11 +256,8 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS) lnp_fwd_kernel(const Lnp<T>
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
   }
-  __syncthreads();
-  pdl_wait();
-  const T* src[NIN];
-  src[0] = a.in;
-  if constexpr (BDR) src[NIN - 1] = has_res ? a.res : a.in;  // no residual: a harmless re-read of in
+  // the per-column parameters are not produced inside the step: read them before
+  // the programmatic-dependency wait, under the previous kernel's tail
   const int c = j * 16;
   float2 g2[8], b2[8], bi2[8];
   ld16(a.gamma + c, g2);
@@ -271,6 +268,11 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS) lnp_fwd_kernel(const Lnp<T>
 #pragma unroll
       for (int i = 0; i < 8; ++i) bi2[i] = make_float2(0.f, 0.f);
   }
+  __syncthreads();
+  pdl_wait();
+  const T* src[NIN];
+  src[0] = a.in;
+  if constexpr (BDR) src[NIN - 1] = has_res ? a.res : a.in;  // no residual: a harmless re-read of in
   if (tid == 0)
     for (int s = 0; s < S; ++s) {
       const long long it = blockIdx.x + static_cast<long long>(s) * gridDim.x;
@@ -374,15 +376,10 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
   }
-  __syncthreads();
-  pdl_wait();
-  const T* src[NIN];
-  src[0] = a.x;
-  src[1] = a.dy;
-  if constexpr (ACC) src[NIN - 1] = a.dx;
   const int c = j * 16;
   // gamma: 16 elements per thread, parked in a private shared-memory slot (read
-  // back per row) so the register budget goes to the column partials
+  // back per row) so the register budget goes to the column partials; a
+  // parameter, so read before the programmatic-dependency wait
   uint4* gsm = reinterpret_cast<uint4*>(dsm + static_cast<size_t>(S) * stage_bytes) + tid * (Words16<T>::N / 4);
   {
     Words16<T> gw;
@@ -390,6 +387,12 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
 #pragma unroll
     for (int i = 0; i < Words16<T>::N / 4; ++i) gsm[i] = make_uint4(gw.w[4 * i], gw.w[4 * i + 1], gw.w[4 * i + 2], gw.w[4 * i + 3]);
   }
+  __syncthreads();
+  pdl_wait();
+  const T* src[NIN];
+  src[0] = a.x;
+  src[1] = a.dy;
+  if constexpr (ACC) src[NIN - 1] = a.dx;
   float2 pg[8], pb[8], po[8];  // column partials: dy * xhat, dy, out
 #pragma unroll
   for (int i = 0; i < 8; ++i) pg[i] = pb[i] = po[i] = make_float2(0.f, 0.f);

@@ -107,6 +107,14 @@ size_t oases_attention_bwd_workspace(const oases_attn_desc* d) {
 
 size_t oases_attention_mask_bytes(const oases_attn_desc* d) { return d ? oases::attention_mask_bytes(*d) : 0; }
 
+oases_status oases_attention_masks(const oases_attn_desc* d, void* stream) {
+  return guarded([&] {
+    if (!d) throw tmpsim::ConfigError("oases_attention_masks: null descriptor");
+    need_device();
+    gemm_status_throw(oases::attention_masks(*d, S(stream)));
+  });
+}
+
 oases_status oases_attention_bwd(const oases_attn_desc* d, void* stream) {
   return guarded([&] {
     if (!d) throw tmpsim::ConfigError("oases_attention_bwd: null descriptor");

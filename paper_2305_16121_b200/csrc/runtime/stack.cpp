@@ -835,6 +835,21 @@ void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int
   if (fused_attn_) {
     oases_attn_desc a = attn_desc(w, block, sb, ws);
     a.mask_mode = mask_mode;
+    // the forward's keep bits come from a separate fully parallel pass, so every
+    // fused-attention pass reads cached bits (OASES_ATTN_MASK_PASS=0: Philox in the kernel)
+    static const bool mask_pass = [] {
+      const char* e = std::getenv("OASES_ATTN_MASK_PASS");
+      return !(e && e[0] == '0');
+    }();
+    if (mask_mode == 1 && mask_pass && a.mask_bits && cfg_.p_attn > 0.f) {
+      const GemmStatus ms = oases::attention_masks(a, ctx_.compute);
+      if (!ms.ok) {
+        if (ms.cuda) throw CudaError(ms.err);
+        throw ConfigError(ms.err);
+      }
+      ++launches_;
+      a.mask_mode = 2;
+    }
     const GemmStatus st = oases::attention_fwd(a, ctx_.compute);
     if (!st.ok) {
       if (st.cuda) throw CudaError(st.err);
@@ -1324,6 +1339,7 @@ void Stack::gather_tokens(const std::vector<void*>& bases, int from_b, int to_b)
   // its slice into du chunks: rank r of the group holds chunk r inside its own
   // slice of from_b, so this is an in-place AllGather of one chunk per rank
   const int du = degree(to_b);
+  if (degree(from_b) >= du) throw ConfigError("gather_tokens: the target block's groups must be the larger ones");
   const int64_t h = cfg_.h, chunk = 2 * ts(to_b) / du;  // rows
   const int dt = dtype();
   if (ctx_.local_workers > 1) {

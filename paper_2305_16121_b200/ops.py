@@ -133,6 +133,15 @@ def attention_fwd(qkv, out, lse, samples, heads, head_dim, seq, scale, dropout_p
     check(capi.lib().oases_attention_fwd(C.byref(d), _stream(stream)))
 
 
+def attention_masks(qkv, samples, heads, head_dim, seq, dropout_p, seed, offset, mask_bits, heads_total=0,
+                    head_offset=0, stream=None):
+    """Keep bits of every causal-band element into mask_bits (what mask_mode 1 stores)."""
+    d = _attn_desc(qkv, samples, heads, head_dim, seq, 1.0, dropout_p, seed, offset, heads_total, head_offset)
+    d.ld_out = heads * head_dim  # (no ctx written; the shared descriptor checks want a valid stride)
+    d.mask_bits = _ptr(mask_bits)
+    check(capi.lib().oases_attention_masks(C.byref(d), _stream(stream)))
+
+
 def attention_bwd(qkv, out, lse, dout, dqkv, samples, heads, head_dim, seq, scale, dropout_p=0.0, seed=0, offset=0,
                   heads_total=0, head_offset=0, ds=None, stream=None, mask_bits=None, mask_mode=0):
     """Backward of attention_fwd: writes dQ | dK | dV into dqkv (dS scratch allocated when not given)."""

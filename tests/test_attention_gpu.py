@@ -39,6 +39,8 @@ CASES = [
     (2, 2, 2, 0, 128, 128, 0.0),
     (1, 2, 2, 0, 64, 256, 0.25),
     (1, 2, 2, 0, 128, 1024, 0.1),
+    (1, 2, 2, 0, 128, 640, 0.1),   # odd tile count: the forward's last tile pair has no second tile
+    (3, 1, 2, 1, 128, 128, 0.1),   # one tile per head
 ]
 
 
@@ -120,6 +122,11 @@ def test_keep_bit_cache_modes_bit_identical(cuda, dh, hl, hg, hoff, s):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     assert torch.equal(lses[0], lses[2])
     assert bits.abs().sum().item() > 0
+    # the separate mask pass writes exactly the bits the forward stored (mode 1)
+    bits2 = torch.zeros_like(bits)
+    ops.attention_masks(qkv, n, hl, dh, s, p, seed, off, bits2, heads_total=hg, head_offset=hoff)
+    torch.cuda.synchronize()
+    assert torch.equal(bits, bits2)
     dout = torch.randn(n * s, hd, device=cuda).bfloat16()
     grads = []
     for mode in (0, 2):
