@@ -934,33 +934,29 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
 // DESIGN.md section 5), one 32-key word per thread: a separate, fully parallel
 // pass so that the forward's softmax warps -- the critical path of the fused
 // kernels -- only expand cached bits (mask_mode 2) instead of running Philox.
-__global__ void __launch_bounds__(256) attn_mask_kernel(const AttnParams p, long long nwords) {
+__global__ void __launch_bounds__(512) attn_mask_kernel(const AttnParams p) {
+  // block = one causal tile (z, qt, kt) in mask_word's order; thread = (row, 32-key word)
   pdl_trigger();
   pdl_wait();
-  const long long ntile = static_cast<long long>(p.nq) * (p.nq + 1) / 2;
+  const int ntile = p.nq * (p.nq + 1) / 2;
+  const int tile = static_cast<int>(blockIdx.x);
+  const int z = tile / ntile, rem = tile - z * ntile;
+  int qt = static_cast<int>((sqrtf(8.f * rem + 1.f) - 1.f) * 0.5f);  // largest qt with qt(qt+1)/2 <= rem
+  if ((qt + 1) * (qt + 2) / 2 <= rem) ++qt;
+  if (qt * (qt + 1) / 2 > rem) --qt;
+  const int kt = rem - qt * (qt + 1) / 2;
+  const int n = z / p.hl, jl = z - n * p.hl;
+  const int row = threadIdx.x >> 2, w = threadIdx.x & 3;
+  const unsigned long long e =
+      (static_cast<unsigned long long>((n + p.n0) * p.hg + p.hoff + jl) * p.seq + qt * kTile + row) *
+          static_cast<unsigned long long>(p.seq) +
+      static_cast<unsigned long long>(kt) * kTile + 32 * w;
   PhiloxLite ph;
   philox_init(p, ph);
-  for (long long wd = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x; wd < nwords;
-       wd += static_cast<long long>(gridDim.x) * 256) {
-    const int w = static_cast<int>(wd & 3);
-    const int row = static_cast<int>((wd >> 2) & (kTile - 1));
-    const long long tile = wd >> 9;  // (z, causal tile) -- mask_word's order
-    const int z = static_cast<int>(tile / ntile);
-    int rem = static_cast<int>(tile - static_cast<long long>(z) * ntile);
-    int qt = 0;
-    while ((qt + 1) * (qt + 2) / 2 <= rem) ++qt;
-    const int kt = rem - qt * (qt + 1) / 2;
-    const int n = z / p.hl, jl = z - n * p.hl;
-    const int i = qt * kTile + row;
-    const unsigned long long e =
-        (static_cast<unsigned long long>((n + p.n0) * p.hg + p.hoff + jl) * p.seq + i) *
-            static_cast<unsigned long long>(p.seq) +
-        static_cast<unsigned long long>(kt) * kTile + 32 * w;
-    uint32_t km[8];
-    const uint32_t b0 = keep_masks16_bits(ph, p, e >> 4, km);
-    const uint32_t b1 = keep_masks16_bits(ph, p, (e + 16) >> 4, km);
-    p.mask_bits[wd] = b0 | (b1 << 16);
-  }
+  uint32_t km[8];
+  const uint32_t b0 = keep_masks16_bits(ph, p, e >> 4, km);
+  const uint32_t b1 = keep_masks16_bits(ph, p, (e + 16) >> 4, km);
+  p.mask_bits[static_cast<long long>(tile) * 512 + threadIdx.x] = b0 | (b1 << 16);
 }
 
 // D[z, i] = sum_d dO[i, d] * O[i, d] (head z's columns); DH/8 threads per row,
@@ -1472,10 +1468,8 @@ GemmStatus attention_masks(const oases_attn_desc& d, cudaStream_t stream) {
     st.err = "attention_masks: needs mask_bits and dropout_p > 0";
     return st;
   }
-  const long long nwords = static_cast<long long>(attention_mask_bytes(d) / sizeof(uint32_t));
-  long long grid = (nwords + 255) / 256;
-  if (grid > 148LL * 8) grid = 148LL * 8;
-  const cudaError_t e = launch_pdl(attn_mask_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, stream, p, nwords);
+  const long long tiles = static_cast<long long>(p.Z) * (p.nq * (p.nq + 1) / 2);
+  const cudaError_t e = launch_pdl(attn_mask_kernel, dim3(static_cast<unsigned>(tiles)), dim3(512), 0, stream, p);
   if (e != cudaSuccess) {
     st.err = std::string("attention_masks launch: ") + cudaGetErrorString(e);
     st.cuda = true;

@@ -835,11 +835,15 @@ void Stack::attention_fwd(Worker& w, int block, int sb, const Workspace& ws, int
   if (fused_attn_) {
     oases_attn_desc a = attn_desc(w, block, sb, ws);
     a.mask_mode = mask_mode;
-    // the forward's keep bits come from a separate fully parallel pass, so every
-    // fused-attention pass reads cached bits (OASES_ATTN_MASK_PASS=0: Philox in the kernel)
+    // OASES_ATTN_MASK_PASS=1: the forward's keep bits from the separate mask pass and
+    // every fused-attention pass reads cached bits. Off by default: the pass costs
+    // ~18 us per C2 sub-batch (Philox is issue-bound wherever it runs), as much as
+    // generating the bits inside the split-warp forward saves (A/B on one B200:
+    // 76.11 / 76.12 ms with the pass vs 75.81 / 76.14 without). The recompute and
+    // backward read the bits the forward stored either way.
     static const bool mask_pass = [] {
       const char* e = std::getenv("OASES_ATTN_MASK_PASS");
-      return !(e && e[0] == '0');
+      return e && e[0] == '1';
     }();
     if (mask_mode == 1 && mask_pass && a.mask_bits && cfg_.p_attn > 0.f) {
       const GemmStatus ms = oases::attention_masks(a, ctx_.compute);

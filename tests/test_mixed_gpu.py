@@ -70,6 +70,12 @@ def check(orc, loss, st, res, degrees, world, tol):
                     want = shard_parameter(p, full, tp=d, rank=w % d, attention=b % 2 == 0,
                                            heads=st.cfg.heads, hidden=st.cfg.hidden)
                     errs[f"g[b{b},w{w},p{p}]"] = rel(st.grad(w, b, p), np.asarray(want).ravel())
+    from tests.test_parity_baseline_gpu import log
+
+    log(f"mixed_world{world}_{st.cfg.dtype}{degrees}", dict(hidden=st.cfg.hidden, heads=st.cfg.heads, seq=st.cfg.seq,
+                                                          batch=st.cfg.batch, layers=st.cfg.layers,
+                                                          degrees=list(degrees)), st.cfg.dtype, tol, errs,
+        {"oracle_loss": loss, "gpu_loss": res.loss})
     bad = {k: v for k, v in errs.items() if not v <= tol}
     assert not bad, f"tolerance {tol} exceeded: {bad}"
     return errs
