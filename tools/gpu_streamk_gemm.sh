@@ -1,0 +1,2 @@
+O=gpurun_out/sk2; mkdir -p $O; rm -f $O/*
+for sh in 4096,2048,8192 4096,2048,2048 4096,6144,2048 4096,8192,2048; do for M in 0 1; do SHAPE=$sh OASES_STREAMK=$M timeout 120 python tools/gemm_time.py >> $O/t.log 2>&1; done; done
