@@ -169,7 +169,16 @@ def cpu_baseline(cfg):
 
 
 def load_traffic():
-    """dram bytes/launch of the dominant GEMM from the committed ncu summary, if any."""
+    """dram bytes/launch of the dominant GEMM (the FC1 forward) from the committed ncu
+    --set full summary of this round (profiles/r02_gemm_ncu.json), else round 1's."""
+    p2 = os.path.join(ROOT, "profiles", "r02_gemm_ncu.json")
+    try:
+        with open(p2) as f:
+            d = json.load(f)
+        k = d["kernels"][0]
+        return (k["dram_read_mb"] + k["dram_write_mb"]) * 1e6, d
+    except (OSError, ValueError, KeyError, IndexError):
+        pass
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
@@ -442,7 +451,7 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else 0,
                      "peak_source": f"{PEAKS['source']} bf16_tflops_sustained",
                      "gemm_launches": ks["gemm_launches"], "traffic": traffic,
-                     "traffic_source": "ncu --set full capture of the FC1 forward GEMM (profiles/ncu_summary.json)"},
+                     "traffic_source": "ncu --set full capture of the FC1 forward GEMM (profiles/r02_gemm_ncu.json)"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "clocks": clk.summary(),
         "wall_s_timed": wall,
