@@ -17,9 +17,6 @@ struct GemmStatus {
 
 // bf16 operands: tcgen05/TMEM/TMA persistent kernel (gemm_tc.cu).
 GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream);
-// Allocates the stream-K partial workspace of the CTA-pair GEMM (once per process; call
-// before capturing a graph -- launches during a capture without it run data-parallel only).
-cudaError_t gemm_streamk_reserve();
 // n independent bf16 problems in one persistent launch when they are all
 // CTA-pair shaped (n == 2), else one launch each.
 GemmStatus gemm_tc_group(const oases_gemm_desc* d, int n, cudaStream_t stream);

@@ -643,65 +643,7 @@ struct TcGroup {
   TcParams p[2];
   int a_mn[2], b_mn[2];
   int tiles0, total;
-  // stream-K tail (single problems): tiles [0, total - sk_r) run data-parallel,
-  // the last sk_r tiles' k-blocks are split evenly over the pairs; partial
-  // accumulators go through sk_ws ([2 x pairs][256 x 256] f32) with per-warp
-  // flags sk_flags ([2 x pairs][16]) and are summed by the pair owning the
-  // tile's last k-block, in ascending pair order (deterministic)
-  int sk_r;
-  float* sk_ws;
-  int* sk_flags;
 };
-
-// Work units of one pair: its data-parallel tiles, then its stream-K pieces
-// in REVERSE k order -- a pair's contributing pieces (a tile's first k-blocks)
-// precede its consuming piece (the end of the tile its range starts in), so no
-// pair waits on a pair that waits on it.
-struct SkUnit {
-  int t, kb0, kb1;
-  int role;  // 0 whole tile, 1 contributes a partial, 2 consumes the partials
-  int slot;  // contributor: partial slot 2 x pair + slot (0: the pair's range starts in the tile)
-};
-struct UnitIter {
-  int t, F0, npairs, KB;
-  long long s, e, ti, tmin;
-  __device__ __forceinline__ UnitIter(const TcGroup& g, int pair, int np) : t(pair), npairs(np) {
-    KB = g.p[0].kblocks;
-    F0 = g.total - g.sk_r;
-    if (g.sk_r > 0) {
-      const long long L = static_cast<long long>(g.sk_r) * KB;
-      s = static_cast<long long>(pair) * L / np;
-      e = static_cast<long long>(pair + 1) * L / np;
-      ti = e > s ? (e - 1) / KB : -1;
-      tmin = s / KB;
-    } else {
-      s = e = 0;
-      ti = -1;
-      tmin = 0;
-    }
-  }
-  __device__ __forceinline__ bool next(SkUnit& u) {
-    if (t < F0) {
-      u = SkUnit{t, 0, KB, 0, -1};
-      t += npairs;
-      return true;
-    }
-    if (ti < tmin) return false;
-    const long long t0 = ti * KB;
-    const int a = static_cast<int>((s > t0 ? s : t0) - t0);
-    const int b = static_cast<int>((e < t0 + KB ? e : t0 + KB) - t0);
-    const int role = (a == 0 && b == KB) ? 0 : (b == KB ? 2 : 1);
-    u = SkUnit{F0 + static_cast<int>(ti), a, b, role, -1};
-    u.slot = s >= t0 ? 0 : 1;  // + 2 x pair by the caller
-    --ti;
-    return true;
-  }
-};
-// The partial slot pair q wrote for stream-K tile ti (the q whose range covers it).
-__device__ __forceinline__ int sk_slot(long long L, int npairs, int q, long long t0) {
-  const long long sq = static_cast<long long>(q) * L / npairs;
-  return sq >= t0 ? 2 * q : 2 * q + 1;
-}
 
 __device__ __forceinline__ int group_tile(const TcGroup& g, int t, int& lt) {
   if (t < g.tiles0) {
@@ -783,6 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int total_tiles = g.total;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&ta0);
@@ -812,11 +755,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      UnitIter it(g, pair, npairs);
-      SkUnit u;
-      while (it.next(u)) {
+      for (int t = pair; t < total_tiles; t += npairs) {
         int lt;
-        const int pi = group_tile(g, u.t, lt);
+        const int pi = group_tile(g, t, lt);
         const TcParams& p = g.p[pi];
         int z, m0, n0;
         pair_decode(p, lt, z, m0, n0);
@@ -824,8 +765,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int ax = p.a_x_off[0] * zo + p.a_x_off[1] * zi, ay = p.a_y_off[0] * zo + p.a_y_off[1] * zi;
         const int bx = p.b_x_off[0] * zo + p.b_x_off[1] * zi, by = p.b_y_off[0] * zo + p.b_y_off[1] * zi;
         const int am = m0 + static_cast<int>(rank) * 128, bn = n0 + static_cast<int>(rank) * 128;
-        const int kbe = u.role == 0 && g.sk_r <= 0 ? p.kblocks : u.kb1;
-        for (int kb = u.kb0; kb < kbe; ++kb) {
+        for (int kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PAIR_STAGE_BYTES);
           uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
@@ -845,19 +785,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint32_t smem_base = smem_u32(smem);
-      UnitIter it(g, pair, npairs);
-      SkUnit u;
-      while (it.next(u)) {
+      for (int t = pair; t < total_tiles; t += npairs) {
         int lt;
-        const int pi = group_tile(g, u.t, lt);
+        const int pi = group_tile(g, t, lt);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * PAIR_BN);
-        const int nkb = u.role == 0 && g.sk_r <= 0 ? g.p[pi].kblocks : u.kb1 - u.kb0;
         if (pi == 0)
-          pair_mma_tile<A0, B0>(smem_base, full, empty, stage, phase, d_tmem, nkb);
+          pair_mma_tile<A0, B0>(smem_base, full, empty, stage, phase, d_tmem, g.p[0].kblocks);
         else
-          pair_mma_tile<A1, B1>(smem_base, full, empty, stage, phase, d_tmem, nkb);
+          pair_mma_tile<A1, B1>(smem_base, full, empty, stage, phase, d_tmem, g.p[1].kblocks);
         umma_commit_pair(&tfull[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
@@ -866,75 +803,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // ------------------------------------------------ epilogue (warps 2..9), per-tile mode dispatch
     float4* stg = stg_all + (warp - 2) * 256;
     const int q = warp & 3, half = (warp - 2) >> 2;
-    const int wid = static_cast<int>(rank) * EPI_WARPS + (warp - 2);  // this warp's 32 x 128 block of a tile
     int acc = 0;
     uint32_t acc_phase = 0;
-    UnitIter it(g, pair, npairs);
-    SkUnit u;
-    while (it.next(u)) {
+    for (int t = pair; t < total_tiles; t += npairs) {
       int lt;
-      const int pi = group_tile(g, u.t, lt);
+      const int pi = group_tile(g, t, lt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                              static_cast<uint32_t>(acc * PAIR_BN + half * (PAIR_BN / 2));
-      if (u.role == 1) {
-        // stream-K contributor: raw f32 accumulator -> partial slot, then this warp's flag
-        const int slot = 2 * pair + u.slot;
-        float4* dst = reinterpret_cast<float4*>(g.sk_ws + (static_cast<long long>(slot) * 16 + wid) * 4096);
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t v[32];
-          tmem_ld32(taddr + 32 * c, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            __stcg(dst + (c * 8 + k) * 32 + lane, make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]),
-                                                             __uint_as_float(v[4 * k + 2]), __uint_as_float(v[4 * k + 3])));
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_gpu(g.sk_flags + slot * 16 + wid, 1);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        continue;
-      }
-      if (u.role == 2) {
-        // stream-K consumer: add the partials of the earlier pairs covering this tile (ascending
-        // pair order) into the TMEM accumulator, then the tile's epilogue as usual
-        const int KB = g.p[0].kblocks;
-        const long long L = static_cast<long long>(g.sk_r) * KB;
-        const long long t0 = static_cast<long long>(u.t - (g.total - g.sk_r)) * KB;
-        const int qf = static_cast<int>(((t0 + 1) * npairs + L - 1) / L) - 1;  // first pair reaching past t0
-        for (int qq = qf; qq < pair; ++qq) {
-          if (static_cast<long long>(qq + 1) * L / npairs <= static_cast<long long>(qq) * L / npairs) continue;
-          const int slot = sk_slot(L, npairs, qq, t0);
-          int* flag = g.sk_flags + slot * 16 + wid;
-          while (ld_acquire_gpu(flag) == 0) {
-          }
-          const float4* src = reinterpret_cast<const float4*>(g.sk_ws + (static_cast<long long>(slot) * 16 + wid) * 4096);
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
-            tmem_ld32(taddr + 32 * c, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float4 a = __ldcg(src + (c * 8 + k) * 32 + lane);
-              v[4 * k] = __float_as_uint(__uint_as_float(v[4 * k]) + a.x);
-              v[4 * k + 1] = __float_as_uint(__uint_as_float(v[4 * k + 1]) + a.y);
-              v[4 * k + 2] = __float_as_uint(__uint_as_float(v[4 * k + 2]) + a.z);
-              v[4 * k + 3] = __float_as_uint(__uint_as_float(v[4 * k + 3]) + a.w);
-            }
-            tmem_st32(taddr + 32 * c, v);
-          }
-          tmem_wait_st();
-          __syncwarp();
-          if (lane == 0) *flag = 0;  // re-armed for the next launch (stream order)
-        }
-      }
       // static problem index: the parameters stay constant-bank operands
       if (pi == 0) {
 #define OASES_PAIR_BODY(T, E, A) pair_tile_epilogue<T, E, A>(g.p[0], lt, taddr, stg, q, half, lane, rank)
@@ -1209,33 +1086,6 @@ int grid_cap(int max_ctas) {
   return grid;
 }
 
-// Stream-K workspace (one per device): partial slots for 2 x (at most 74) pairs
-// of 256 x 256 f32 and their per-warp flags (zeroed once; consumers re-arm them).
-struct SkWorkspace {
-  float* ws = nullptr;
-  int* flags = nullptr;
-  int slots = 0;
-};
-SkWorkspace& sk_workspace() {
-  static SkWorkspace w;
-  return w;
-}
-// Off unless OASES_STREAMK=1. Measured on a B200 (tools/gemm_time.py, warm,
-// CUDA graph): 4096x2048x8192 97.2 -> 99.7 us, 4096x2048x2048 27.6 -> 31.9,
-// 4096x6144x2048 73.9 -> 80.8, 4096x8192x2048 93.7 -> 99.4; C2 step 77.2 ->
-// 79.9 ms. The consumer's partial adds (TMEM read-modify-write per contributor)
-// sit on the critical path at the end of the GEMM and cost more than the
-// ragged last wave (the data-parallel 1.73-wave GEMMs lose less than the 13 %
-// the wave count suggests).
-bool streamk_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("OASES_STREAMK");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
-}
-
 GemmStatus launch_pairs(const oases_gemm_desc* const* ds, const Prepared* const* pr, int n, int max_ctas,
                         cudaStream_t stream) {
   TcGroup g{};
@@ -1254,19 +1104,7 @@ GemmStatus launch_pairs(const oases_gemm_desc* const* ds, const Prepared* const*
   g.total = static_cast<int>(total);
   int pairs = grid_cap(max_ctas) / 2;
   if (pairs < 1) pairs = 1;
-  // Stream-K tail for a single problem whose tiles leave the last wave ragged
-  // (e.g. 128 tiles of a 4096 x 2048 output on 74 pairs: 1.73 waves): the
-  // remainder's k-blocks are spread over every pair.
-  g.sk_r = 0;
-  const SkWorkspace& skw = sk_workspace();
-  if (n == 1 && streamk_enabled() && g.p[0].batch == 1 && skw.ws && 2 * pairs <= skw.slots && total > 0 &&
-      total % pairs != 0 && total / pairs < 8 && g.p[0].kblocks >= 4 &&
-      static_cast<long long>(total % pairs) * g.p[0].kblocks >= pairs) {
-    g.sk_r = static_cast<int>(total % pairs);
-    g.sk_ws = skw.ws;
-    g.sk_flags = skw.flags;
-  }
-  if (g.sk_r == 0 && total < pairs) pairs = static_cast<int>(total);
+  if (total < pairs) pairs = static_cast<int>(total);
   cudaError_t e = cudaSuccess;
   if (!launch_group(maps, g, 2 * pairs, stream, &e)) {
     GemmStatus st;
@@ -1278,32 +1116,11 @@ GemmStatus launch_pairs(const oases_gemm_desc* const* ds, const Prepared* const*
 
 }  // namespace
 
-cudaError_t gemm_streamk_reserve() {
-  SkWorkspace& w = sk_workspace();
-  if (w.ws) return cudaSuccess;
-  const int slots = 2 * (sm_count() / 2);
-  cudaError_t e = cudaMalloc(&w.ws, static_cast<size_t>(slots) * 256 * 256 * sizeof(float));
-  if (e != cudaSuccess) return e;
-  e = cudaMalloc(&w.flags, static_cast<size_t>(slots) * 16 * sizeof(int));
-  if (e != cudaSuccess) return e;
-  e = cudaMemset(w.flags, 0, static_cast<size_t>(slots) * 16 * sizeof(int));
-  if (e != cudaSuccess) return e;
-  w.slots = slots;
-  return cudaDeviceSynchronize();
-}
-
 GemmStatus gemm_tc(const oases_gemm_desc& d, cudaStream_t stream) {
   GemmStatus st;
   Prepared pr;
   if (!prepare(d, pr, &st.err)) return st;
   if (pr.pair) {
-    if (!sk_workspace().ws && streamk_enabled()) {
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
-        const cudaError_t e = gemm_streamk_reserve();
-        if (e != cudaSuccess) return launch_status(e);
-      }
-    }
     const oases_gemm_desc* ds[1] = {&d};
     const Prepared* ps[1] = {&pr};
     return launch_pairs(ds, ps, 1, d.max_ctas, stream);

@@ -394,9 +394,6 @@ void Stack::alloc_all() {
     w.loss = static_cast<double*>(arena_.alloc(sizeof(double)));
     w.loss_ws = static_cast<double*>(arena_.alloc(loss_workspace()));
   }
-  // the CTA-pair GEMM's stream-K workspace (OASES_STREAMK=1), before any graph capture
-  if (dtype() == OASES_BF16 && std::getenv("OASES_STREAMK") && std::getenv("OASES_STREAMK")[0] == '1')
-    check_cuda(gemm_streamk_reserve(), "stream-K workspace");
   check_cuda(cudaDeviceSynchronize(), "stack allocation");
   // residual-stream buffers of blocks > 0 are placed when a plan is bound
   x_stored_.assign(static_cast<size_t>(nblocks_), false);
