@@ -174,12 +174,10 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg, const std::vector<int>& degrees)
                       "sub-batch tensor, which the degree changes re-slice)");
   if (mixed_ && ctx.comm_disabled) throw ConfigError("stack: mixed per-block degrees need the collectives");
   if (mixed_ && cfg.bytes == 8) throw ConfigError("stack: mixed per-block degrees run in bf16 or f32");
+  // heads per rank at the world degree: (samples per sub-batch) x (local heads) is
+  // the same at every degree, so the attention buffers are sized with it
   hl_ = cfg.attention ? cfg.heads / t : 0;
   dh_ = cfg.attention ? cfg.h / cfg.heads : 0;
-  ncol_attn_ = cfg.attention ? 3 * hl_ * dh_ : 0;
-  nrow_attn_ = cfg.attention ? hl_ * dh_ : 0;
-  ncol_ffn_ = cfg.f / t;
-  nrow_ffn_ = cfg.f / t;
   for (int b = 0; b < nblocks_; ++b) {
     const int d = degree(b);
     if (cfg.f % d) throw ConfigError("stack: ffn hidden must be divisible by the block degree");
@@ -266,10 +264,6 @@ void Stack::kernel_stats(double* gemm_ms, double* gemm_flops, int* launches) {
 int64_t Stack::param_numel(int block, int p) const {
   if (block < 0 || block >= nblocks_ || p < 0 || p >= OASES_P_COUNT) return 0;
   return workers_.front().params[static_cast<size_t>(block)].numel[p];
-}
-
-void* Stack::half(void* base, int sb, int64_t cols) const {
-  return static_cast<char*>(base) + static_cast<size_t>(sb) * tokens_sub() * cols * esize();
 }
 
 void* Stack::gp(void* base, const Worker& w, int b, int sb, int64_t cols) const {

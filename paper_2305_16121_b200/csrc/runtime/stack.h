@@ -226,7 +226,6 @@ class Stack {
   void* gp(void* base, const Worker& w, int b, int sb, int64_t cols) const;
   // half sb of a local [2 ts(b), cols] buffer
   void* lp(void* base, int b, int sb, int64_t cols) const;
-  void* half(void* base, int sb, int64_t cols) const;
 
   Context& ctx_;
   ModelCfg cfg_;
@@ -239,7 +238,7 @@ class Stack {
   bool lnp_bwd_ = false;  // persistent LayerNorm backward with folded column sums (rowpipe.cu)
   bool hbits_ = false;   // hidden-dropout keep bits cached (fused forward kernel covers the shape)
   bool colsum_ = false;  // FFN column-bias gradient partials come from the FC2 dgrad (MUL) epilogue
-  int hl_ = 0, dh_ = 0, ncol_attn_ = 0, ncol_ffn_ = 0, nrow_attn_ = 0, nrow_ffn_ = 0;
+  int hl_ = 0, dh_ = 0;  // local heads at the world degree, head dim
   std::vector<std::vector<std::array<bool, OASES_P_COUNT>>> touched_;  // [worker][block]
   // degree of the groups a gradient was computed on this step (0: untouched); < world -> dp_reduce_grads
   std::vector<std::array<int, OASES_P_COUNT>> computed_at_;  // [block] (same on every worker)

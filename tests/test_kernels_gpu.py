@@ -155,3 +155,36 @@ def test_fused_bdr_layernorm_rejects_uncovered_shape(cuda):
     with pytest.raises(capi.OasesError) as e:
         ops.bias_dropout_residual_layernorm_fwd(x, None, x, torch.empty_like(x), g, be, torch.empty_like(x))
     assert e.value.status == capi.ERR_CONFIG
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,cols", [(1000, 1024), (257, 4096), (33, 512), (4096, 2048)])
+def test_layernorm_bwd_accumulate_and_deterministic(cuda, dt, rows, cols):
+    """The persistent LayerNorm backward (rowpipe.cu): dx accumulated onto an existing
+    residual gradient, dgamma/dbeta from the folded column partials (per-CTA registers,
+    2-CTA cluster reduction, fixed-order finalize) against float64 torch, with a ragged
+    last row group, and bit-identical across repeated launches."""
+    torch.manual_seed(rows + cols)
+    x = (torch.randn(rows, cols, device=cuda) * 1.5 + 0.3).to(dt)
+    g = (1 + 0.1 * torch.randn(cols, device=cuda)).to(dt)
+    dy = torch.randn(rows, cols, device=cuda).to(dt)
+    res = torch.randn(rows, cols, device=cuda).to(dt)
+    xd = x.double().requires_grad_(True)
+    gd = g.double().requires_grad_(True)
+    bd = torch.zeros(cols, device=cuda, dtype=torch.float64, requires_grad=True)
+    ref = torch.nn.functional.layer_norm(xd, (cols,), gd, bd, eps=1e-5)
+    ref.backward(dy.double())
+    outs = []
+    for _ in range(2):
+        dx = res.clone()
+        dg = torch.zeros(cols, device=cuda)
+        dbeta = torch.zeros(cols, device=cuda)
+        ops.layernorm_bwd(x, g, dy, dx, dg, dbeta, accumulate_dx=True)
+        outs.append((dx, dg, dbeta))
+    torch.cuda.synchronize()
+    tol = 1e-5 if dt == torch.float32 else 2e-2
+    assert rel(outs[0][0], res.double() + xd.grad) < 2 * tol
+    assert rel(outs[0][1], gd.grad) < (1e-4 if dt == torch.float32 else 3e-2)
+    assert rel(outs[0][2], bd.grad) < (1e-4 if dt == torch.float32 else 3e-2)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
