@@ -87,6 +87,7 @@ struct AttnParams {
   uint32_t rk0[10], rk1[10];  // Philox round keys of `seed` (constant-bank operands of the round LOP3s)
   uint32_t* mask_bits;        // keep-bit cache [Z][causal tile][128 rows][4 words] (null: always Philox)
   int mask_mode;              // 0 generate, 1 generate + store, 2 load
+  int pv_wait;                // attn_fwd2_kernel: S(j+1) waits for PV(j) (1) or relies on in-order MMAs (0)
 };
 
 // Word index of (row, 32-column group w) of causal tile (qt, kt) of head z in
@@ -735,7 +736,10 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
       int itc[2] = {0, 0};  // items processed per tile (o_free phases; odd pairs have no tile B)
       int g = 0;
       auto issue_s = [&](int x, int st, uint32_t qa) {
-        if (cnt[x] > 0) mbar_wait(&pv_done[x], (cnt[x] - 1) & 1);  // PV read the previous P from this region
+        // PV read the previous P from this region: tcgen05.mma executes in issue
+        // order, so S(j+1) issued after PV(j) cannot overwrite P(j) before PV(j)
+        // consumed it; pv_wait = 1 keeps the explicit drain (A/B check)
+        if (p.pv_wait && cnt[x] > 0) mbar_wait(&pv_done[x], (cnt[x] - 1) & 1);
         tc_fence_after();
         const uint32_t kb = sb + C::K_OFF + st * C::TILE_BYTES;
 #pragma unroll
@@ -873,7 +877,8 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
           }
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          // O holds P_{<j} V: PV(j-1) completed before S(j) was issued (issue_s waited on it)
+          // O holds P_{<j} V: PV(j-1) was issued before S(j), and s_full(j)'s commit
+          // tracks every MMA issued before it
 #pragma unroll
           for (int c = 0; c < DH / 32; ++c) {
             uint32_t o[32];
@@ -1421,6 +1426,11 @@ GemmStatus attention_fwd(const oases_attn_desc& d, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
+  static const int pv_wait = [] {
+    const char* e = std::getenv("OASES_ATTN_PV_WAIT");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  p.pv_wait = pv_wait;
   const bool fwd2 = fwd2_on && (!p.thr || p.mask_mode == 2) && 2LL * p.Z * ((p.nq + 1) / 2) >= 3LL * nsm;
   unsigned grid = static_cast<unsigned>(fwd2 ? p.Z * ((p.nq + 1) / 2) : p.Z * p.nq);
   {

@@ -75,6 +75,7 @@ struct TcParams {
   float* rowdot;  // EPI_ROWDOT output
   int rd_group, rd_seq, rd_heads;
   float* colsum;  // EPI_MUL column-sum partials [ceil(M/32)][N] (or null)
+  int zigzag;     // causal K ranges: serpentine tile order (sched_tile)
 };
 
 struct TileInfo {
@@ -113,6 +114,16 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, int t, TileInfo& 
     ti.kb0 = ti.m0 / BK;
   }
   return ti.kb0 < ti.kb1;
+}
+
+// Tile of this CTA's r-th round. Causal K-range tiles come heaviest first
+// (decode_tile); a plain stride hands CTA b the b-th tile of every round, so
+// the low CTAs collect the heaviest tile of each round (C2 dQ: 20 vs an average
+// of 15.6 k-blocks of 128). Serpentine order (the stride reversed on odd rounds)
+// pairs each round's heavy tiles with the next round's light ones.
+__device__ __forceinline__ int sched_tile(const TcParams& p, int r) {
+  const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+  return r * G + ((p.zigzag && (r & 1)) ? G - 1 - b : b);
 }
 
 // ----------------------------------------------------------------- epilogue
@@ -457,7 +468,7 @@ __device__ __forceinline__ void epilogue_role_single(const TcParams& p, uint64_t
   const int total = p.batch * p.tiles_m * p.tiles_n;
   int acc = 0;
   uint32_t acc_phase = 0;
-  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+  for (int r = 0, t = sched_tile(p, 0); t < total; t = sched_tile(p, ++r)) {
     TileInfo ti;
     if (!decode_tile<BN>(p, t, ti)) continue;
     mbar_wait(&tfull[acc], acc_phase);
@@ -518,7 +529,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int r = 0, t = sched_tile(p, 0); t < total_tiles; t = sched_tile(p, ++r)) {
         TileInfo ti;
         if (!decode_tile<BN>(p, t, ti)) continue;
         const int zo = ti.z / p.batch_inner, zi = ti.z - zo * p.batch_inner;
@@ -559,7 +570,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint32_t smem_base = smem_u32(smem);
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int r = 0, t = sched_tile(p, 0); t < total_tiles; t = sched_tile(p, ++r)) {
         TileInfo ti;
         if (!decode_tile<BN>(p, t, ti)) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -1061,6 +1072,13 @@ bool prepare(const oases_gemm_desc& d, Prepared& out, std::string* err) {
   p.c_f32 = d.c_dtype == OASES_F32;
   p.epilogue = d.epilogue;
   p.causal = d.causal;
+  {
+    static const bool zz = [] {
+      const char* e = std::getenv("OASES_GEMM_ZIGZAG");
+      return !(e && e[0] == '0');
+    }();
+    p.zigzag = zz && (d.causal == OASES_CAUSAL_K_UPTO_M || d.causal == OASES_CAUSAL_K_FROM_M);
+  }
   p.accumulate = d.accumulate;
   p.alpha = d.alpha;
   out.pair = pair;
