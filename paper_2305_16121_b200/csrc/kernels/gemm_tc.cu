@@ -243,8 +243,9 @@ __device__ __forceinline__ void epi_prefetch(const TcParams& p, int c, int nbeg,
 // One 32-column chunk of a stripe: TMEM -> swizzled smem -> fused epilogue -> global.
 template <typename OutT, int EPI, bool ACC>
 __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, long long row0, long long col0, int lr,
-                                          int lc, int rows_left, long long step, long long lane_base, uint32_t taddr,
-                                          float4* stg, int lane, float (&racc)[StripeGeo<OutT>::IT]) {
+                                          int lc, int rows_left, long long step, uint32_t taddr, float4* stg, int lane,
+                                          float (&racc)[StripeGeo<OutT>::IT], const uint4 (&pa)[StripeGeo<OutT>::IT],
+                                          const uint4 (&pc)[StripeGeo<OutT>::IT]) {
   using G = StripeGeo<OutT>;
   constexpr int E = G::E, RPI = G::RPI, IT = G::IT;
   constexpr bool BIAS = EPI == OASES_EPI_BIAS || EPI == OASES_EPI_BIAS_GELU || EPI == OASES_EPI_BIAS_GELU_GRAD;
@@ -252,14 +253,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
   constexpr bool DG = EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL || RD;  // epilogues reading AUX
   constexpr bool CS = EPI == OASES_EPI_MUL;  // optional column-sum partials of the stored C
   const int nc = nbeg + c * 32;
-  // All of the chunk's global operand loads are in flight at once (one DRAM
-  // latency per chunk instead of one per row pair). bf16 operands (4 vectors)
-  // are issued before the TMEM drain so their latency overlaps it; f32 ones
-  // (8 vectors) after it, once the 32 TMEM registers are free again.
-  constexpr bool EARLY = true;
-  uint4 pa[IT], pc[IT];
-  if constexpr ((DG || ACC) && EARLY)
-    epi_prefetch<OutT, EPI, ACC>(p, c, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
+  // pa / pc: the chunk's global operands, loaded by epilogue_stripe ahead of time
   {
     uint32_t r[32];
     tmem_ld32(taddr + static_cast<uint32_t>(c * 32), r);
@@ -270,8 +264,6 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
       stg[lane * 8 + (j ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                                      __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
   }
-  if constexpr ((DG || ACC) && !EARLY)
-    epi_prefetch<OutT, EPI, ACC>(p, c, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
   __syncwarp();
   const int n = nc + lc * E;
   const int valid = p.N - n;  // elements of this lane's group inside the problem
@@ -398,11 +390,15 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, int c, int nbeg, lo
 // TMEM -> registers (thread = row) -> 128B-swizzled smem staging -> each lane
 // takes one 16-byte column group of a row, so a warp's global access covers
 // 32/LPR full row segments -> fused epilogue -> global.
-// Epilogues that READ global memory (the dGeLU pre-activation, the f32
-// accumulate of C) issue every load of a chunk before draining TMEM.
+// Epilogues that READ global memory (the gelu' / pre-activation operand, the
+// f32 accumulate of C) keep those loads a chunk ahead: chunk 0's are issued
+// before waiting for the accumulator (tfull), chunk c+1's before chunk c is
+// drained, so one DRAM latency per stripe is exposed instead of one per chunk
+// (NCH chunks per tile: the per-tile epilogue latency is what the double-
+// buffered accumulator must hide under the next tile's main loop).
 template <typename OutT, int EPI, bool ACC, int NCH>
 __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_base, int nbeg, uint32_t taddr,
-                                                float4* stg, int lane) {
+                                                float4* stg, int lane, uint64_t* tfull, uint32_t tphase) {
   using G = StripeGeo<OutT>;
   const int zo = z / p.batch_inner, zi = z - zo * p.batch_inner;
   const long long row0 = p.c_row_off[0] * zo + p.c_row_off[1] * zi + m_base;
@@ -414,9 +410,12 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
   float racc[G::IT];
 #pragma unroll
   for (int it = 0; it < G::IT; ++it) racc[it] = 0.f;
-#pragma unroll 1
-  for (int c = 0; c < NCH; ++c) {
-    epi_chunk<OutT, EPI, ACC>(p, c, nbeg, row0, col0, lr, lc, rows_left, step, lane_base, taddr, stg, lane, racc);
+  constexpr bool LD = EPI == OASES_EPI_DGELU || EPI == OASES_EPI_MUL || EPI == OASES_EPI_ROWDOT || ACC;
+  uint4 pa[G::IT], pc[G::IT];
+  if constexpr (LD) epi_prefetch<OutT, EPI, ACC>(p, 0, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
+  mbar_wait(tfull, tphase);
+  tc_fence_after();
+  auto rowdot_flush = [&](int c) {
     if constexpr (EPI == OASES_EPI_ROWDOT) {
       const int cend = static_cast<int>(col0) + nbeg + (c + 1) * 32;  // column after this chunk
       if (cend % p.rd_group == 0 && cend <= p.N) {
@@ -436,6 +435,30 @@ __device__ __forceinline__ void epilogue_stripe(const TcParams& p, int z, int m_
           racc[it] = 0.f;
         }
       }
+    }
+  };
+  // bf16 operands (4 vectors) run a chunk ahead in two named buffers (chunks in
+  // pairs); the f32 accumulate of C (8 vectors) would not fit twice in the
+  // register budget and is loaded at the start of its chunk
+  constexpr bool PIPE = LD && !ACC && NCH % 2 == 0;
+  if constexpr (PIPE) {
+    uint4 qa[G::IT], qc[G::IT];
+#pragma unroll 1
+    for (int c = 0; c < NCH; c += 2) {
+      epi_prefetch<OutT, EPI, ACC>(p, c + 1, nbeg, lc, lr, rows_left, lane_base, step, qa, qc);
+      epi_chunk<OutT, EPI, ACC>(p, c, nbeg, row0, col0, lr, lc, rows_left, step, taddr, stg, lane, racc, pa, pc);
+      rowdot_flush(c);
+      if (c + 2 < NCH) epi_prefetch<OutT, EPI, ACC>(p, c + 2, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
+      epi_chunk<OutT, EPI, ACC>(p, c + 1, nbeg, row0, col0, lr, lc, rows_left, step, taddr, stg, lane, racc, qa, qc);
+      rowdot_flush(c + 1);
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+      if constexpr (LD)
+        if (c > 0) epi_prefetch<OutT, EPI, ACC>(p, c, nbeg, lc, lr, rows_left, lane_base, step, pa, pc);
+      epi_chunk<OutT, EPI, ACC>(p, c, nbeg, row0, col0, lr, lc, rows_left, step, taddr, stg, lane, racc, pa, pc);
+      rowdot_flush(c);
     }
   }
 }
@@ -471,11 +494,10 @@ __device__ __forceinline__ void epilogue_role_single(const TcParams& p, uint64_t
   for (int r = 0, t = sched_tile(p, 0); t < total; t = sched_tile(p, ++r)) {
     TileInfo ti;
     if (!decode_tile<BN>(p, t, ti)) continue;
-    mbar_wait(&tfull[acc], acc_phase);
-    tc_fence_after();
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                            static_cast<uint32_t>(acc * BN + half * (BN / 2));
-    epilogue_stripe<OutT, EPI, ACC, BN / 64>(p, ti.z, ti.m0 + q * 32, ti.n0 + half * (BN / 2), taddr, stg, lane);
+    epilogue_stripe<OutT, EPI, ACC, BN / 64>(p, ti.z, ti.m0 + q * 32, ti.n0 + half * (BN / 2), taddr, stg, lane,
+                                             &tfull[acc], acc_phase);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -667,11 +689,12 @@ __device__ __forceinline__ int group_tile(const TcGroup& g, int t, int& lt) {
 
 template <typename OutT, int EPI, bool ACC>
 __device__ __forceinline__ void pair_tile_epilogue(const TcParams& p, int lt, uint32_t taddr, float4* stg, int q,
-                                                   int half, int lane, uint32_t rank) {
+                                                   int half, int lane, uint32_t rank, uint64_t* tfull,
+                                                   uint32_t tphase) {
   int z, m0, n0;
   pair_decode(p, lt, z, m0, n0);
   const int mb = m0 + static_cast<int>(rank) * 128 + q * 32;
-  epilogue_stripe<OutT, EPI, ACC, PAIR_BN / 64>(p, z, mb, n0 + half * (PAIR_BN / 2), taddr, stg, lane);
+  epilogue_stripe<OutT, EPI, ACC, PAIR_BN / 64>(p, z, mb, n0 + half * (PAIR_BN / 2), taddr, stg, lane, tfull, tphase);
 }
 
 // Producer: TMA of one k-block of a tile (compile-time operand layout).
@@ -819,17 +842,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int t = pair; t < total_tiles; t += npairs) {
       int lt;
       const int pi = group_tile(g, t, lt);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                              static_cast<uint32_t>(acc * PAIR_BN + half * (PAIR_BN / 2));
       // static problem index: the parameters stay constant-bank operands
       if (pi == 0) {
-#define OASES_PAIR_BODY(T, E, A) pair_tile_epilogue<T, E, A>(g.p[0], lt, taddr, stg, q, half, lane, rank)
+#define OASES_PAIR_BODY(T, E, A) \
+  pair_tile_epilogue<T, E, A>(g.p[0], lt, taddr, stg, q, half, lane, rank, &tfull[acc], acc_phase)
         OASES_EPI_DISPATCH(g.p[0], OASES_PAIR_BODY);
 #undef OASES_PAIR_BODY
       } else {
-#define OASES_PAIR_BODY(T, E, A) pair_tile_epilogue<T, E, A>(g.p[1], lt, taddr, stg, q, half, lane, rank)
+#define OASES_PAIR_BODY(T, E, A) \
+  pair_tile_epilogue<T, E, A>(g.p[1], lt, taddr, stg, q, half, lane, rank, &tfull[acc], acc_phase)
         OASES_EPI_DISPATCH(g.p[1], OASES_PAIR_BODY);
 #undef OASES_PAIR_BODY
       }
