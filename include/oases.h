@@ -314,6 +314,35 @@ oases_status oases_stack_create(oases_ctx* ctx, const oases_model_desc* model, o
 oases_status oases_stack_create_mixed(oases_ctx* ctx, const oases_model_desc* model, const int32_t* block_degrees,
                                       int32_t num_blocks, oases_stack** out);
 int oases_stack_block_degree(const oases_stack* s, int block);
+
+/* Rank geometry of one block (host-only: callable without a device). The
+ * stack on `world` ranks places rank `rank`'s share of block b at: tokens
+ * [token_row0, token_row0 + 2 * tokens_per_sub_batch) of the micro-batch (its
+ * data-parallel group's slice, two sub-batches), heads / FFN columns
+ * [rank_in_group * w, (rank_in_group + 1) * w) of the block's weights, w =
+ * col_width / 3 (attention QKV: q, k, v each heads_local * head_dim wide) or
+ * col_width (FFN). Tensor-parallel group = `group` (ncclCommSplit colour
+ * rank / degree), data-parallel peers share rank_in_group (colour rank %
+ * degree). Replaces the rank arithmetic the reference does inline in
+ * numerics.cpp:120-165 (uniform degree) and sim.cpp:101-175 (mixed). */
+typedef struct {
+  int32_t degree;
+  int32_t group;          /* data-parallel group of the block (0 .. groups-1) */
+  int32_t rank_in_group;  /* tensor-parallel rank inside the group */
+  int32_t groups;         /* world / degree */
+  int32_t heads_local;    /* attention blocks; 0 for FFN blocks */
+  int32_t attention;      /* 1: attention block (QKV/proj), 0: FFN block */
+  int64_t samples_per_sub_batch;
+  int64_t tokens_per_sub_batch;
+  int64_t token_row0;
+  int64_t col_width;      /* local width of the column-parallel weight (QKV | FC1) */
+  int64_t row_width;      /* local width of the row-parallel weight's input (proj | FC2) */
+} oases_block_layout;
+
+/* block_degrees: num_blocks entries (null: every block at the world degree);
+ * out: num_blocks entries. Errors as oases_stack_create_mixed would raise. */
+oases_status oases_rank_layout(const oases_model_desc* model, int32_t world, const int32_t* block_degrees,
+                               int32_t num_blocks, int32_t rank, oases_block_layout* out);
 oases_status oases_stack_destroy(oases_stack* stack);
 
 /* Parameter tensors per block, identified by (block, param id). Host f64

@@ -138,6 +138,22 @@ class ModelDesc(C.Structure):
     ]
 
 
+class BlockLayout(C.Structure):
+    _fields_ = [
+        ("degree", C.c_int32),
+        ("group", C.c_int32),
+        ("rank_in_group", C.c_int32),
+        ("groups", C.c_int32),
+        ("heads_local", C.c_int32),
+        ("attention", C.c_int32),
+        ("samples_per_sub_batch", C.c_int64),
+        ("tokens_per_sub_batch", C.c_int64),
+        ("token_row0", C.c_int64),
+        ("col_width", C.c_int64),
+        ("row_width", C.c_int64),
+    ]
+
+
 class PlanOp(C.Structure):
     _fields_ = [
         ("id", C.c_int32),
@@ -234,6 +250,8 @@ _SIGNATURES = [
     ("oases_stack_create_mixed", C.c_int,
      [C.c_void_p, C.POINTER(ModelDesc), C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_void_p)]),
     ("oases_stack_block_degree", C.c_int, [C.c_void_p, C.c_int]),
+    ("oases_rank_layout", C.c_int,
+     [C.POINTER(ModelDesc), C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.POINTER(BlockLayout)]),
     ("oases_stack_destroy", C.c_int, [C.c_void_p]),
     ("oases_stack_param_numel", C.c_int64, [C.c_void_p, C.c_int, C.c_int]),
     ("oases_stack_num_blocks", C.c_int, [C.c_void_p]),

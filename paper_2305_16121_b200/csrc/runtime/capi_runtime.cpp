@@ -150,6 +150,41 @@ oases_status oases_stack_create_mixed(oases_ctx* ctx, const oases_model_desc* mo
   });
 }
 
+oases_status oases_rank_layout(const oases_model_desc* model, int32_t world, const int32_t* block_degrees,
+                               int32_t num_blocks, int32_t rank, oases_block_layout* out) {
+  return guarded([&] {
+    if (!model || !out) throw ConfigError("oases_rank_layout: null argument");
+    const oases::ModelCfg cfg = to_cfg(*model);
+    if (cfg.b <= 0 || cfg.s <= 0 || cfg.h <= 0 || cfg.layers < 0)
+      throw ConfigError("oases_rank_layout: sizes must be positive");
+    if (cfg.b % 2) throw ConfigError("stack: global_batch must be even (two sub-batches)");
+    if (num_blocks != oases::num_blocks(cfg))
+      throw ConfigError((block_degrees ? "stack: one degree per block (" : "oases_rank_layout: num_blocks must be (") +
+                        std::to_string(oases::num_blocks(cfg)) + ")");
+    if (rank < 0 || rank >= world) throw ConfigError("oases_rank_layout: rank outside [0, world)");
+    std::vector<int> deg;
+    if (block_degrees) deg.assign(block_degrees, block_degrees + num_blocks);
+    deg = oases::resolve_degrees(cfg, world, deg, nullptr);
+    for (int b = 0; b < num_blocks; ++b) {
+      const int d = deg[static_cast<size_t>(b)];
+      const bool att = oases::attention_block(cfg, b);
+      oases_block_layout& o = out[b];
+      o = oases_block_layout{};
+      o.degree = d;
+      o.group = oases::group_of(rank, d);
+      o.rank_in_group = oases::rank_in_group(rank, d);
+      o.groups = world / d;
+      o.heads_local = att ? oases::heads_local(cfg, d) : 0;
+      o.attention = att ? 1 : 0;
+      o.samples_per_sub_batch = oases::samples_per_sub(cfg, world, d);
+      o.tokens_per_sub_batch = oases::tokens_per_sub(cfg, world, d);
+      o.token_row0 = oases::token_row0(cfg, world, d, rank);
+      o.col_width = oases::col_width(cfg, d, att);
+      o.row_width = oases::row_width(cfg, d, att);
+    }
+  });
+}
+
 int oases_stack_block_degree(const oases_stack* s, int block) {
   return (s && s->stack && block >= 0 && block < s->stack->num_blocks()) ? s->stack->degree(block) : 0;
 }

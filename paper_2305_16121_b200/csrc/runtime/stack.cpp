@@ -152,23 +152,10 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg, const std::vector<int>& degrees)
   // 16-byte vector loads in LayerNorm / softmax rows
   if ((cfg.ln && cfg.h % 8) || (cfg.attention && (cfg.s % 8 || cfg.h % 8)))
     throw ConfigError("stack: hidden (with LayerNorm/attention) and seq must be multiples of 8");
-  nblocks_ = cfg.layers * (cfg.attention ? 2 : 1);
+  nblocks_ = oases::num_blocks(cfg);
   // per-block degrees (F2): each divides the world; a degree-d block runs on N/d
   // data-parallel groups, each with an even number of samples (two sub-batches)
-  if (degrees.empty()) {
-    deg_.assign(static_cast<size_t>(nblocks_), t);
-  } else {
-    if (static_cast<int>(degrees.size()) != nblocks_)
-      throw ConfigError("stack: one degree per block (" + std::to_string(nblocks_) + ")");
-    deg_ = degrees;
-  }
-  for (int d : deg_) {
-    if (d < 1 || t % d) throw ConfigError("stack: every block degree must divide the world size " + std::to_string(t));
-    if ((static_cast<int64_t>(cfg.b) * d) % (2LL * t))
-      throw ConfigError("stack: a degree-" + std::to_string(d) + " block splits the micro-batch over " +
-                        std::to_string(t / d) + " groups of two sub-batches: global_batch * d / world must be even");
-    if (d != t) mixed_ = true;
-  }
+  deg_ = resolve_degrees(cfg, t, degrees, &mixed_);
   if (mixed_ && cfg.p_hidden > 0.f)
     throw ConfigError("stack: mixed per-block degrees need hidden_dropout 0 (hidden-dropout masks are keyed per "
                       "sub-batch tensor, which the degree changes re-slice)");
@@ -180,9 +167,6 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg, const std::vector<int>& degrees)
   dh_ = cfg.attention ? cfg.h / cfg.heads : 0;
   for (int b = 0; b < nblocks_; ++b) {
     const int d = degree(b);
-    if (cfg.f % d) throw ConfigError("stack: ffn hidden must be divisible by the block degree");
-    if (cfg.attention && (cfg.heads < 1 || cfg.h % cfg.heads || cfg.heads % d))
-      throw ConfigError("stack: hidden % heads and heads % degree must be 0");
     if (dtype() == OASES_BF16) {
       // tcgen05 tiles: K extents must be multiples of 64 (TMA zero-fill only at
       // buffer edges), attention sequences whole 128-row tiles.
@@ -233,9 +217,11 @@ Stack::Stack(Context& ctx, const ModelCfg& cfg, const std::vector<int>& degrees)
     for (int d : ds) {
       if (d == t) continue;
       ncclComm_t c = nullptr;
-      check_nccl(ncclCommSplit(ctx.nccl, ctx.rank / d, ctx.rank % d, &c, nullptr), "ncclCommSplit (tp group)");
+      check_nccl(ncclCommSplit(ctx.nccl, group_of(ctx.rank, d), rank_in_group(ctx.rank, d), &c, nullptr),
+                 "ncclCommSplit (tp group)");
       tp_comms_.emplace_back(d, c);
-      check_nccl(ncclCommSplit(ctx.nccl, ctx.rank % d, ctx.rank / d, &c, nullptr), "ncclCommSplit (dp group)");
+      check_nccl(ncclCommSplit(ctx.nccl, rank_in_group(ctx.rank, d), group_of(ctx.rank, d), &c, nullptr),
+                 "ncclCommSplit (dp group)");
       dp_comms_.emplace_back(d, c);
     }
   }

@@ -14,6 +14,7 @@
 
 #include "../../../include/oases.h"
 #include "../../../include/oases/tmpsim.hpp"
+#include "layout.h"
 
 namespace oases {
 
@@ -52,13 +53,7 @@ class DeviceArena {
 };
 
 // ------------------------------------------------------------------ stack
-struct ModelCfg {
-  int h = 0, f = 0, heads = 0, s = 0, b = 0, layers = 0;
-  int bytes = 2;
-  bool recompute = true, attention = true, ln = true, bias = true, residual = true;
-  float p_hidden = 0.f, p_attn = 0.f, eps = 1e-5f;
-  uint64_t seed = 0;
-};
+// ModelCfg and the rank geometry (tokens / heads / columns per rank and block): layout.h
 
 // Per-block parameters of one TMP worker (device layout [out, in]).
 struct BlockParams {
@@ -138,7 +133,7 @@ class Stack {
   Context& ctx() { return ctx_; }
   int num_blocks() const { return nblocks_; }
   int num_workers() const { return static_cast<int>(workers_.size()); }
-  bool is_attention(int b) const { return cfg_.attention && (b % 2 == 0); }
+  bool is_attention(int b) const { return attention_block(cfg_, b); }
   int dtype() const { return cfg_.bytes == 2 ? OASES_BF16 : (cfg_.bytes == 8 ? OASES_F64 : OASES_F32); }
   // gradient dtype: f32 (f64 in the value-level toy mode)
   int gdtype() const { return cfg_.bytes == 8 ? OASES_F64 : OASES_F32; }
@@ -215,13 +210,14 @@ class Stack {
   Workspace ws_for(Worker& w, int block, int sb);
   bool touch(const Worker& w, int block, int p, int computed_at = 0);  // true if the gradient must accumulate
   // per-block geometry (degree-dependent)
-  int hl(int b) const { return cfg_.attention ? cfg_.heads / degree(b) : 0; }
-  int64_t ncol(int b) const { return is_attention(b) ? 3LL * hl(b) * dh_ : cfg_.f / degree(b); }
-  int64_t nrow(int b) const { return is_attention(b) ? static_cast<int64_t>(hl(b)) * dh_ : cfg_.f / degree(b); }
-  int64_t bsub(int b) const { return static_cast<int64_t>(cfg_.b) * degree(b) / world() / 2; }  // samples per sub-batch
-  int64_t ts(int b) const { return bsub(b) * cfg_.s; }  // tokens per sub-batch
-  int rig(const Worker& w, int b) const { return w.rank % degree(b); }  // rank in the block's group
-  int64_t row0(const Worker& w, int b) const { return static_cast<int64_t>(w.rank / degree(b)) * 2 * ts(b); }
+  // rank geometry: layout.h (shared with the host-only oases_rank_layout)
+  int hl(int b) const { return heads_local(cfg_, degree(b)); }
+  int64_t ncol(int b) const { return col_width(cfg_, degree(b), is_attention(b)); }
+  int64_t nrow(int b) const { return row_width(cfg_, degree(b), is_attention(b)); }
+  int64_t bsub(int b) const { return samples_per_sub(cfg_, world(), degree(b)); }  // samples per sub-batch
+  int64_t ts(int b) const { return tokens_per_sub(cfg_, world(), degree(b)); }     // tokens per sub-batch
+  int rig(const Worker& w, int b) const { return rank_in_group(w.rank, degree(b)); }  // rank in the block's group
+  int64_t row0(const Worker& w, int b) const { return token_row0(cfg_, world(), degree(b), w.rank); }
   // rows of sub-batch sb of block b (this worker's group) in a token-indexed buffer
   void* gp(void* base, const Worker& w, int b, int sb, int64_t cols) const;
   // half sb of a local [2 ts(b), cols] buffer

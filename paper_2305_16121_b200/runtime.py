@@ -130,6 +130,21 @@ def unique_id() -> bytes:
     return bytes(buf)
 
 
+def rank_layout(cfg: "ModelConfig", world: int, rank: int, degrees=None) -> list:
+    """Rank `rank`'s share of every block of a stack on `world` ranks (host-only,
+    no device): one dict per block with the oases_block_layout fields -- the
+    data-parallel group and its token slice, the rank inside the tensor-parallel
+    group and the local weight widths (include/oases.h, csrc/runtime/layout.h).
+    degrees: per-block TMP degrees (None: all at `world`)."""
+    nb = cfg.layers * (2 if cfg.attention else 1)
+    out = (capi.BlockLayout * max(nb, 1))()
+    deg = None if degrees is None else (C.c_int32 * len(degrees))(*[int(x) for x in degrees])
+    d = cfg.desc()
+    check(capi.lib().oases_rank_layout(C.byref(d), int(world), deg, nb if deg is None else len(degrees), int(rank),
+                                       out))
+    return [{k: getattr(out[b], k) for k, _ in capi.BlockLayout._fields_} for b in range(nb)]
+
+
 class Context:
     def __init__(self, tp=1, rank=0, device=0, local_workers=1, unique_id: bytes | None = None, nccl_max_ctas=0,
                  gemm_max_ctas=0, comm_disabled=False):

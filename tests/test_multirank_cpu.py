@@ -1,4 +1,4 @@
-"""World-size-2 gloo tests of the N>1 host path (CPU only).
+"""World-size-2 and -4 gloo tests of the N>1 host path (CPU only).
 
 The TMP ranks of the GPU build exchange only through the AllReduce; these tests
 run the host-side partition logic (runtime.shard_parameter) in two real
@@ -95,6 +95,118 @@ def test_two_rank_partition_and_allreduce():
     for p in procs:
         p.join(timeout=60)
     assert results == {0: True, 1: True}, results
+
+
+def _mixed_worker(rank, world, port, q, degrees):
+    """One rank of a mixed-degree stack on `world` ranks: its token slice, group and
+    weight shard come from the product's rank geometry (runtime.rank_layout ->
+    oases_rank_layout, the functions Stack uses for its buffer offsets and
+    ncclCommSplit colours); the tensor-parallel AllReduce, the data-parallel
+    gradient sum and the resharding AllGather run over gloo groups built from
+    those colours. The result must be the unsharded FFN block on the whole
+    micro-batch (sim.cpp:101-175 for the group structure, numerics.cpp:158-165
+    and 206 for the sums)."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle.oracle import B_COL, W_COL, W_ROW
+        from paper_2305_16121_b200.runtime import ModelConfig, rank_layout, shard_parameter
+
+        mc = ModelConfig(hidden=32, heads=4, seq=8, batch=8, layers=len(degrees) // 2, ffn=64, dtype="f32")
+        lay = rank_layout(mc, world, rank, degrees)
+        every = [None] * world
+        dist.all_gather_object(every, lay)
+        ok = True
+        T, h, f = mc.batch * mc.seq, mc.hidden, mc.ffn
+        # the groups of every distinct degree, created in the same order on every rank
+        # (torch.distributed.new_group is collective, like ncclCommSplit)
+        tp_groups, dp_groups = {}, {}
+        for d in sorted(set(degrees)):
+            for g in range(world // d):
+                grp = dist.new_group([g * d + r for r in range(d)])
+                if g == rank // d:
+                    tp_groups[d] = grp
+            for r in range(d):
+                grp = dist.new_group([g * d + r for g in range(world // d)])
+                if r == rank % d:
+                    dp_groups[d] = grp
+        rng = np.random.default_rng(3)
+        x = rng.standard_normal((T, h))
+        for b, d in enumerate(degrees):
+            blocks = [e[b] for e in every]
+            att = b % 2 == 0
+            # partition: the groups' token slices tile the micro-batch, each group's ranks
+            # hold distinct tensor-parallel indices, widths tile the weights
+            ok &= all(L["degree"] == d and L["groups"] == world // d and L["attention"] == int(att) for L in blocks)
+            spans = sorted({(L["token_row0"], L["token_row0"] + 2 * L["tokens_per_sub_batch"]) for L in blocks})
+            ok &= spans[0][0] == 0 and spans[-1][1] == T and all(a[1] == c[0] for a, c in zip(spans, spans[1:]))
+            for g in range(world // d):
+                mem = [L for L in blocks if L["group"] == g]
+                ok &= sorted(L["rank_in_group"] for L in mem) == list(range(d))
+            ok &= blocks[rank]["col_width"] * d == (3 * h if att else f)
+            ok &= blocks[rank]["row_width"] * d == (h if att else f)
+            if att:
+                continue
+            # the FFN block on this rank's slice with its shard, then the exchanges
+            L = blocks[rank]
+            r0, n = L["token_row0"], 2 * L["tokens_per_sub_batch"]
+            w1 = rng.standard_normal((h, f)) * 0.2
+            b1 = rng.standard_normal(f) * 0.1
+            w2 = rng.standard_normal((f, h)) * 0.2
+            s1 = shard_parameter(W_COL, w1, tp=d, rank=L["rank_in_group"], attention=False)
+            sb = shard_parameter(B_COL, b1, tp=d, rank=L["rank_in_group"], attention=False)
+            s2 = shard_parameter(W_ROW, w2, tp=d, rank=L["rank_in_group"], attention=False)
+            ok &= s1.shape[1] == L["col_width"] and s2.shape[0] == L["row_width"]
+            xs = x[r0:r0 + n]
+            pre = xs @ s1 + sb
+            y = torch.tensor(_gelu(pre) @ s2)
+            dist.all_reduce(y, group=tp_groups[d])  # the block's g AllReduce inside the group
+            full = _gelu(x @ w1 + b1) @ w2
+            ok &= np.allclose(y.numpy(), full[r0:r0 + n], rtol=1e-12, atol=1e-12)
+            # resharding AllGather: the next degree's groups need every token of their slice
+            gathered = [torch.zeros_like(y) for _ in range(world // d)]
+            dist.all_gather(gathered, y, group=dp_groups[d])
+            ok &= np.allclose(torch.cat(gathered).numpy(), full, rtol=1e-12, atol=1e-12)
+            # data-parallel gradient sum: dW2 shard over the group's tokens, summed over groups
+            gy = np.ones((n, h))
+            dw2 = torch.tensor(_gelu(pre).T @ gy)
+            dist.all_reduce(dw2, group=dp_groups[d])
+            want = shard_parameter(W_ROW, _gelu(x @ w1 + b1).T @ np.ones((T, h)), tp=d, rank=L["rank_in_group"],
+                                   attention=False)
+            ok &= np.allclose(dw2.numpy(), want, rtol=1e-12, atol=1e-10)
+        q.put((rank, bool(ok)))
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world,degrees", [(2, [1, 2, 2, 1]), (4, [2, 2, 4, 4, 1, 4]), (4, [4, 1, 2, 2])])
+def test_mixed_degree_layout_and_group_exchanges(world, degrees):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000) + 17 * world + len(degrees)
+    procs = [ctx.Process(target=_mixed_worker, args=(r, world, port, q, degrees)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert results == {r: True for r in range(world)}, results
+
+
+def test_rank_layout_rejects_what_the_stack_rejects():
+    from paper_2305_16121_b200._capi import OasesError
+    from paper_2305_16121_b200.runtime import ModelConfig, rank_layout
+
+    mc = ModelConfig(hidden=32, heads=4, seq=8, batch=4, layers=1, ffn=64, dtype="f32")
+    with pytest.raises(OasesError, match="divide the world"):
+        rank_layout(mc, 4, 0, [3, 4])
+    with pytest.raises(OasesError, match="must be even"):
+        rank_layout(mc, 4, 0, [1, 4])  # 4 samples over 4 groups: one sample per group
+    with pytest.raises(OasesError, match="one degree per block"):
+        rank_layout(mc, 2, 0, [2])
+    L = rank_layout(mc, 2, 1)
+    assert [e["degree"] for e in L] == [2, 2] and L[0]["heads_local"] == 2 and L[1]["col_width"] == 32
 
 
 def test_bench_launches_one_rank_per_gpu():
