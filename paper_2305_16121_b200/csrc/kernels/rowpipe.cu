@@ -237,7 +237,7 @@ __device__ __forceinline__ void issue_item(unsigned char* stage, uint64_t* bar, 
 
 // ------------------------------------------------------------------ forward
 template <typename T, int TPR, bool BDR>
-__global__ void __launch_bounds__(Geo<TPR>::THREADS) lnp_fwd_kernel(const Lnp<T> a) {
+__global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 3 : 1) lnp_fwd_kernel(const Lnp<T> a) {
   using G = Geo<TPR>;
   constexpr int RB = G::RB, W = G::W;
   constexpr int NIN = BDR ? 2 : 1;
