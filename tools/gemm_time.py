@@ -35,5 +35,4 @@ g.replay()
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / rep * 1e3
-print(json.dumps({"shape": [M, N, K], "us": us, "tflops": 2 * M * N * K / us / 1e6,
-                  "streamk": os.environ.get("OASES_STREAMK", "1")}))
+print(json.dumps({"shape": [M, N, K], "major": [amn, bmn], "us": us, "tflops": 2 * M * N * K / us / 1e6}))
