@@ -19,9 +19,17 @@ dout = torch.randn_like(out)
 dqkv = torch.empty_like(qkv)
 ds = torch.empty(n * hl * s, s, device="cuda", dtype=torch.bfloat16)
 sc = 1 / math.sqrt(dh)
-ops.attention_fwd(qkv, out, lse, n, hl, dh, s, sc, p, 1, 2)
+# MODE 0: Philox inside the kernels; 2: cached keep bits (the stack's path)
+mode = int(os.environ.get("MODE", "2"))
+mbits = None
+if mode == 2 and p > 0:
+    d = ops._attn_desc(qkv, n, hl, dh, s, 1.0, p, 1, 2, 0, 0)
+    mbits = torch.zeros(capi.lib().oases_attention_mask_bytes(C.byref(d)) // 4, dtype=torch.int32, device="cuda")
+    ops.attention_masks(qkv, n, hl, dh, s, p, 1, 2, mbits)
+kw = dict(mask_bits=mbits, mask_mode=2) if mbits is not None else {}
+ops.attention_fwd(qkv, out, lse, n, hl, dh, s, sc, p, 1, 2, **kw)
 for _ in range(3):
-    ops.attention_bwd(qkv, out, lse, dout, dqkv, n, hl, dh, s, sc, p, 1, 2, ds=ds)
+    ops.attention_bwd(qkv, out, lse, dout, dqkv, n, hl, dh, s, sc, p, 1, 2, ds=ds, **kw)
 torch.cuda.synchronize()
 buf = (C.c_ulonglong * (8 * 64))()
 capi.lib().oases_attn_trace_dump(buf)
