@@ -501,39 +501,46 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
     for (int i = 0; i < 8; ++i) po[i] = __fadd2_rn(po[i], o[i]);
   }
   if (!a.part) return;
-  // Column partials: the RB row slots of the CTA are summed in slot order into
-  // shared memory (the ring is idle now), then the CTAs of the cluster reduce
-  // them through distributed shared memory -- CTA rank q sums column chunk q of
-  // every rank's partials in rank order -- and write one [3][cols] partial row
-  // per cluster (lnp_cluster() times fewer rows for the finalize to read).
-  float* psm = reinterpret_cast<float*>(dsm);  // [3][cols]
-  for (int rr = 0; rr < RB; ++rr) {
-    if (r == rr) {
-      float* q0 = psm + c;
+  // Column partials: every row slot stores its partials into its own
+  // [3][cols] plane of shared memory (the ring is idle now; one barrier, no
+  // read-modify-write rounds), then the CTAs of the cluster reduce them through
+  // distributed shared memory -- CTA rank q sums column chunk q of every rank's
+  // planes, slots in order within a rank, ranks in order -- and write one
+  // [3][cols] partial row per cluster (lnp_cluster() times fewer rows for the
+  // finalize to read).
+  float* psm = reinterpret_cast<float*>(dsm);  // [RB][3][cols]
+  {
+    float* q0 = psm + static_cast<size_t>(r) * 3 * cols + c;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float2* d0 = reinterpret_cast<float2*>(q0 + 2 * i);
-        float2* d1 = reinterpret_cast<float2*>(q0 + cols + 2 * i);
-        float2* d2 = reinterpret_cast<float2*>(q0 + 2 * cols + 2 * i);
-        *d0 = rr ? __fadd2_rn(*d0, pg[i]) : pg[i];
-        *d1 = rr ? __fadd2_rn(*d1, pb[i]) : pb[i];
-        *d2 = rr ? __fadd2_rn(*d2, po[i]) : po[i];
-      }
+    for (int i = 0; i < 4; ++i) {
+      reinterpret_cast<float4*>(q0)[i] = make_float4(pg[2 * i].x, pg[2 * i].y, pg[2 * i + 1].x, pg[2 * i + 1].y);
+      reinterpret_cast<float4*>(q0 + cols)[i] = make_float4(pb[2 * i].x, pb[2 * i].y, pb[2 * i + 1].x, pb[2 * i + 1].y);
+      reinterpret_cast<float4*>(q0 + 2 * cols)[i] =
+          make_float4(po[2 * i].x, po[2 * i].y, po[2 * i + 1].x, po[2 * i + 1].y);
     }
-    __syncthreads();
   }
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
-  cl.sync();
+  cl.sync();  // (also the CTA barrier for the planes)
   const int ncl = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   const int nf4 = 3 * cols / 4, chunk = (nf4 + ncl - 1) / ncl;
   const int f0 = rank * chunk, f1 = f0 + chunk < nf4 ? f0 + chunk : nf4;
   float4* out = reinterpret_cast<float4*>(a.part + static_cast<long long>(blockIdx.x / ncl) * 3 * cols);
   for (int f = f0 + tid; f < f1; f += G::THREADS) {
-    float4 t = reinterpret_cast<const float4*>(cl.map_shared_rank(psm, 0))[f];
-    for (int q = 1; q < ncl; ++q) {
-      const float4 u = reinterpret_cast<const float4*>(cl.map_shared_rank(psm, q))[f];
-      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    float4 t;
+    for (int q = 0; q < ncl; ++q) {
+      const float4* pq = reinterpret_cast<const float4*>(cl.map_shared_rank(psm, q)) + f;
+      float4 u = pq[0];
+#pragma unroll 4
+      for (int rr = 1; rr < RB; ++rr) {
+        const float4 v = pq[static_cast<size_t>(rr) * nf4];
+        u.x += v.x; u.y += v.y; u.z += v.z; u.w += v.w;
+      }
+      if (q == 0) {
+        t = u;
+      } else {
+        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      }
     }
     out[f] = t;
   }
@@ -745,7 +752,9 @@ BwdGeo bwd_geo(size_t esize, int cols, bool acc, long long rows, int max_sms) {
   // 2 CTAs per SM (the kernel's launch bounds guarantee the registers) up to 256 threads
   Plan pl = plan_with(stage, threads <= 256 ? 2 : 1);
   pl.smem += static_cast<size_t>(threads) * 16 * esize;  // private gamma slots
-  if (pl.smem < static_cast<size_t>(3) * cols * sizeof(float)) pl.smem = static_cast<size_t>(3) * cols * sizeof(float);
+  // the column-partial planes overlay the ring at kernel end: [rb][3][cols] f32
+  const size_t planes = static_cast<size_t>(rb) * 3 * cols * sizeof(float);
+  if (pl.smem < planes) pl.smem = planes;
   int sms = num_sms();
   long long clusters = bwd_max_clusters(esize, tpr, acc, threads, pl.smem);
   if (max_sms > 0 && max_sms < sms) clusters = clusters * max_sms / sms;  // leave the capped SMs' share
