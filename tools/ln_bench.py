@@ -63,6 +63,9 @@ timeit(lambda d: ops.bias_dropout_residual_layernorm_fwd(d["x"], b, d["r"], d["y
        4 * tensor_bytes, "bdr + layernorm_fwd p=0.1")
 timeit(lambda d: ops.layernorm_bwd(d["x"], g, d["r"], d["y"], dg, dbe, accumulate_dx=True), 4 * tensor_bytes,
        "layernorm_bwd acc (+dgamma/dbeta)")
+# the backward kernel alone (no parameter partials, no finalize launch)
+timeit(lambda d: ops.layernorm_bwd(d["x"], g, d["r"], d["y"], None, None, accumulate_dx=True), 4 * tensor_bytes,
+       "layernorm_bwd acc (no param grads)")
 # size-matched practical ceilings: torch's vectorised elementwise kernels moving
 # the same bytes (a copy = layernorm_fwd's traffic, a 3-operand add = 3 tensors)
 timeit(lambda d: d["y"].copy_(d["x"]), 2 * tensor_bytes, "torch copy_ (layernorm_fwd's bytes)")
