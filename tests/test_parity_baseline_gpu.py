@@ -10,6 +10,10 @@
   the depth of BASELINE's stacks is measured rather than assumed.
 * fp32 mode at C2 width (h2048, 16 heads), s256: the north star's "fp32 within
   1e-4 relative on activations, gradients and loss" at the real hidden size.
+* C3 and C4 widths at their target degree: h4096 / 32 heads and h8192 / 64 heads
+  (head_dim 128), TMP=8 as eight in-process ranks (4 and 8 local heads, the QKV /
+  FC1 column shards and proj / FC2 row shards of one TMP=8 rank, the literal-sum
+  AllReduce), reduced sequence and batch so the fp64 oracle stays in seconds.
 
 Tolerances (per tensor, ||gpu - cpu||_inf / ||cpu||_inf; stated in the tests):
   bf16: 3e-2   f32: 1e-4.
@@ -109,3 +113,16 @@ def test_depth_24_layers_vs_oracle(cuda, dtype, tol):
     every block-boundary activation x_1..x_47, every gradient and dX."""
     case = dict(hidden=256, heads=2, seq=256, batch=4, layers=24, hidden_dropout=0.1, attention_dropout=0.1)
     check(f"depth24_{dtype}", case, 1, dtype, tol)
+
+
+@pytest.mark.parametrize("name,case", [
+    ("c3_width", dict(hidden=4096, heads=32, seq=512, batch=2, layers=1, hidden_dropout=0.1, attention_dropout=0.1)),
+    ("c4_width", dict(hidden=8192, heads=64, seq=256, batch=2, layers=1, hidden_dropout=0.1, attention_dropout=0.1)),
+])
+def test_target_width_tp8_bf16_vs_oracle(cuda, name, case):
+    """BASELINE configs[2] / [3] hidden sizes and head counts at TMP=8 (eight
+    in-process ranks, every rank's shard of every gradient checked), bf16; Oases
+    and CrossPass both run and agree bitwise."""
+    out = check(f"{name}_bf16_tp8", case, 8, "bf16", BF16_TOL, variants=("Oases", "CrossPass"))
+    assert out["Oases"][0] == out["CrossPass"][0]
+    assert np.array_equal(out["Oases"][1], out["CrossPass"][1])
