@@ -279,11 +279,13 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
       if (it < nitems) issue_item<T, NIN>(dsm + s * stage_bytes, &full[s], src, it, RB, a.rows, cols);
     }
   const float inv_cols = 1.f / static_cast<float>(cols);
-  for (long long k = 0;; ++k) {
+  // ring slot s = k % S and its phase (k / S) & 1 as running counters (no 64-bit division per item)
+  int s = 0;
+  uint32_t ph = 0u;
+  for (long long k = 0;; ++k, (++s == S) ? (s = 0, ph ^= 1u) : 0u) {
     const long long item = blockIdx.x + k * gridDim.x;
     if (item >= nitems) break;
-    const int s = static_cast<int>(k % S);
-    mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
+    mbar_wait(&full[s], ph);
     const long long row = item * RB + r;
     const bool ok = row < a.rows;
     const long long base = row * cols + c;
@@ -402,10 +404,11 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
       if (it < nitems) issue_item<T, NIN>(dsm + s * stage_bytes, &full[s], src, it, RB, a.rows, cols);
     }
   const float inv_cols = 1.f / static_cast<float>(cols);
-  for (long long k = 0;; ++k) {
+  int s = 0;  // ring slot k % S and its phase (k / S) & 1, as running counters
+  uint32_t ph = 0u;
+  for (long long k = 0;; ++k, (++s == S) ? (s = 0, ph ^= 1u) : 0u) {
     const long long item = blockIdx.x + k * gridDim.x;
     if (item >= nitems) break;
-    const int s = static_cast<int>(k % S);
     const long long row = item * RB + r;
     const bool ok = row < a.rows;
     const long long base = row * cols + c;
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(Geo<TPR>::THREADS, Geo<TPR>::THREADS <= 256 ? 
     uint32_t keep = 0;
     if constexpr (DROP)
       if (a.keep_bits && ok) keep = a.keep_bits[base >> 4];
-    mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
+    mbar_wait(&full[s], ph);
     const T* srow = reinterpret_cast<const T*>(dsm + s * stage_bytes) + r * cols;
     float2 xc[8];
     Words16<T> dw, ow;
