@@ -1,10 +1,6 @@
-# end-of-round evidence: bit-identity of the LN-backward change against the previous build,
-# three default bench runs, then the round-2 profile set
-O=gpurun_out/bit; mkdir -p $O; rm -f $O/*
-for L in old new old new; do
-  if [ $L = old ]; then export OASES_LIB=$PWD/liboases_old.so; else unset OASES_LIB; fi
-  echo "$L $(timeout 300 python tools/bitcheck.py 2 2>&1 | tail -1)" >> $O/bit.log
-done
-unset OASES_LIB
+# end-of-round evidence: full GPU suite + smoke, three default bench runs, then the round-2 profile set
+O=gpurun_out/fin2; mkdir -p $O; rm -f $O/*
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo rc $? >> $O/pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo rc $? >> $O/smoke.log
 bash tools/gpu_bench3.sh
 bash tools/profile_round2.sh
