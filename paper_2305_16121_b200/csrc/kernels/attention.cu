@@ -65,7 +65,21 @@ __device__ __forceinline__ unsigned long long gtime() {
   do {                 \
     if (blockIdx.x == 0 && (g) < 64) g_attn_trace[ev][g] = gtime(); \
   } while (0)
+// per-CTA start / end / SM id of the dK/dV kernel (first 1024 CTAs; tools/attn_cta_timeline.py)
+__device__ unsigned long long g_cta_trace[3][1024];
+#define CTRACE(ev)                                                                   \
+  do {                                                                               \
+    if (threadIdx.x == 64 && blockIdx.x < 1024) {                                    \
+      unsigned smid;                                                                 \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                             \
+      g_cta_trace[ev][blockIdx.x] = gtime();                                         \
+      g_cta_trace[2][blockIdx.x] = smid;                                             \
+    }                                                                                \
+  } while (0)
 #else
+#define CTRACE(ev) \
+  do {             \
+  } while (0)
 #define ATRACE(ev, g) \
   do {                 \
   } while (0)
@@ -1029,6 +1043,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
+  CTRACE(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = static_cast<int>(blockIdx.x) / p.Z;  // longest column (kt = 0) first
   const int z = static_cast<int>(blockIdx.x) % p.Z;
@@ -1305,6 +1320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (leader) bulk_wait0();
+    CTRACE(1);
   }
   tc_fence_before();
   __syncthreads();
@@ -1376,6 +1392,9 @@ bool fill_common(AttnParams& p, const oases_attn_desc& d, std::string* err) {
 #ifdef OASES_EXP_TRACE
 extern "C" int oases_attn_trace_dump(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(unsigned long long) * 8 * 64));
+}
+extern "C" int oases_attn_cta_dump(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_cta_trace, sizeof(unsigned long long) * 3 * 1024));
 }
 #endif
 
